@@ -1,0 +1,222 @@
+/*
+ * ddnm.h -- C ABI of the B200-native batched DD NM-ROM-HR online solve.
+ *
+ * The reference (arxiv 2305.15163, /root/reference/pkg/src/ddrom) has no FFI:
+ * its hot path is the Python call chain
+ *     driver.solve_rom            driver.py:554-597
+ *       -> build_problem          driver.py:356-436
+ *       -> init_guess             driver.py:442-458 (RbfInitializer.query
+ *                                 driver.py:82-90, multiplier_least_squares
+ *                                 driver.py:461-471)
+ *       -> sqp.iterate            sqp.py:230-299
+ *            -> eval_gradients    sqp.py:117-146
+ *            -> assemble_and_solve_kkt  sqp.py:162-208
+ * Each entry point below replaces one of those calls for a whole batch of
+ * parameters mu = (a, lambda) at once; the Python package
+ * paper_2305_15163_b200 binds them with ctypes.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Host arrays are
+ * caller-owned, row-major, FP64, indices int64 (the reference's dtypes).
+ * One context per GPU; a context is not thread-safe; it owns one CUDA stream
+ * and all device buffers.  Every function returns 0 on success or a negative
+ * DDNM_E* code; ddnm_last_error() describes the most recent failure on the
+ * calling thread.
+ */
+#ifndef DDNM_H
+#define DDNM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDNM_ABI_VERSION 1
+
+/* return codes */
+#define DDNM_OK 0
+#define DDNM_EINVAL (-1)       /* bad argument / shape (reference: ValueError) */
+#define DDNM_ECUDA (-2)        /* CUDA runtime failure                          */
+#define DDNM_EUNSUPPORTED (-3) /* latent dims / sizes without a compiled kernel */
+#define DDNM_ENOMEM (-4)
+
+/* per-mu solve status (reference: SqpResult.failure_reason / exceptions) */
+#define DDNM_STATUS_OK 0           /* loop ended on tol or max_iter (sqp.py:255)   */
+#define DDNM_STATUS_LINE_SEARCH 1  /* "line_search" failure, best iterate (sqp.py:275-293) */
+#define DDNM_STATUS_KKT_SINGULAR 2 /* ConvergenceError from the KKT (sqp.py:199-207) */
+#define DDNM_STATUS_LSTSQ_RANK 3   /* multiplier least squares rank deficient:
+                                      K is then singular too (driver.py:461-471)   */
+
+/* reduction-map kinds (RomInstance.interior_maps / interface_maps) */
+#define DDNM_MAP_AUTOENCODER 0     /* sparse shallow decoder, autoencoder.py:99-174 */
+#define DDNM_MAP_LINEAR 1          /* POD LinearMap, pod.py:67-97                   */
+
+#define DDNM_ACT_SWISH 0           /* autoencoder.py:31-45 */
+#define DDNM_ACT_SIGMOID 1
+
+/* One decoder.  AUTOENCODER: g = (W2 act(W1 x + b1)) * scale + shift with W2 a
+ * CSR matrix [n_out x n_hidden] in storage (= accumulation) order
+ * (hyper.py:163-197).  LINEAR: g = Phi x, Phi = W1 [n_out x latent]. */
+typedef struct {
+  int32_t n_out;
+  int32_t n_hidden;          /* AUTOENCODER only */
+  const double* W1;          /* [n_hidden][latent] or Phi [n_out][latent] */
+  const double* b1;          /* [n_hidden] */
+  const int64_t* indptr;     /* [n_out + 1] */
+  const int64_t* indices;    /* [nnz] hidden index per entry */
+  const double* data;        /* [nnz] */
+  const double* scale;       /* [n_out] */
+  const double* shift;       /* [n_out] */
+} ddnm_decoder;
+
+/* One subdomain block as build_problem instantiates it (driver.py:360-435):
+ * interior decoder restricted to the HR outputs `io` (extract_subnet,
+ * hyper.py:200-222, or LinearMap.restrict_outputs, pod.py:95-97), the full
+ * interface decoder (WFPC keeps it whole, driver.py:398-402), the sampled
+ * residual rows and the local column order of RestrictedResidual
+ * (driver.py:392-396, partition.py:361-425), and CA = C @ A_i
+ * (driver.py:368-369). */
+typedef struct {
+  int32_t n_int, n_gam;      /* latent dims of this block */
+  ddnm_decoder interior;     /* n_out == n_io */
+  ddnm_decoder interface;    /* n_out == N_Gamma (all interface dofs) */
+  int32_t n_rows;            /* HR sample rows */
+  const int64_t* res_rows;   /* [n_rows] global residual rows, sorted */
+  int32_t n_cols;            /* n_io + n_gio */
+  const int64_t* cols;       /* [n_cols] global state columns, local order */
+  int32_t n_io;
+  int32_t n_gio;
+  const int64_t* gio;        /* [n_gio] positions in the interface outputs */
+  const double* CA;          /* [n_c][interface.n_out] */
+} ddnm_block;
+
+/* Thin-plate-spline RBF initializer (driver.py:59-90 + scipy RBFInterpolator
+ * evaluation): x0 = [phi(|qn*eps - y_i*eps|)_i, prod(((qn-shift)/scale)^p_r)_r]
+ * @ coeffs with qn = (mu - lo)/span. */
+typedef struct {
+  int32_t n_centers, n_mono;
+  const double* y;           /* [n_centers][2] */
+  const double* coeffs;      /* [n_centers + n_mono][n_D] */
+  const int64_t* powers;     /* [n_mono][2] */
+  double shift[2], scale[2], lo[2], hi[2];
+  double epsilon;
+} ddnm_rbf;
+
+typedef struct {
+  int32_t abi_version;       /* DDNM_ABI_VERSION */
+  int32_t map_kind;          /* DDNM_MAP_* (same for every block) */
+  int32_t activation;        /* DDNM_ACT_* */
+  int32_t nx, ny;            /* interior FD grid (burgers.py:67-106) */
+  double nu;
+  int32_t n_blocks;
+  int32_t n_c;               /* multipliers (WFPC test-matrix rows) */
+  const ddnm_block* blocks;  /* [n_blocks] */
+  ddnm_rbf rbf;              /* n_centers == 0: no initializer */
+} ddnm_artifacts;
+
+/* SqpConfig (sqp.py:68-81) */
+typedef struct {
+  double tol;
+  int32_t max_iter;
+  double armijo_c1;
+  double backtrack_factor;
+  int32_t max_halvings;
+  double reg_scale;
+} ddnm_sqp_cfg;
+
+typedef struct {
+  int32_t n_primal;          /* n_D = sum (n_int + n_gam) */
+  int32_t n_mult;            /* n_C */
+  int32_t n_blocks;
+  int32_t total_rows;        /* sum of HR rows over blocks */
+  int32_t total_int_out;     /* sum n_io */
+  int32_t total_gam_out;     /* sum N_Gamma */
+  int32_t total_R;           /* sum n_rows * (n_int + n_gam) */
+  int32_t total_cjac;        /* sum n_c * n_gam */
+  int32_t total_int_J;       /* sum n_io * n_int */
+  int32_t total_gam_J;       /* sum N_Gamma * n_gam */
+  int32_t slots_per_cta;     /* mu processed concurrently per CTA */
+  int32_t ctas;              /* persistent grid size */
+  int32_t smem_bytes;        /* dynamic shared memory per CTA */
+  int32_t device;
+} ddnm_info;
+
+/* Per-mu solve results; every pointer may be NULL except x and lam. */
+typedef struct {
+  double* x;                 /* [B][n_D]   SqpResult.x   (best iterate on line-search failure) */
+  double* lam;               /* [B][n_C]   SqpResult.lam */
+  int32_t* n_iter;           /* [B] accepted steps */
+  int32_t* n_evals;          /* [B] eval_gradients calls inside iterate */
+  int32_t* status;           /* [B] DDNM_STATUS_* */
+  int32_t* n_reg;            /* [B] regularized KKT solves (RuntimeWarning count) */
+  double* merit;             /* [B] merit_history[-1] */
+  double* objective;         /* [B] objective_history[-1] */
+  double* merit_hist;        /* [B][max_iter+1], NaN padded */
+  double* obj_hist;          /* [B][max_iter+1], NaN padded */
+  double* alpha_hist;        /* [B][max_iter],   NaN padded */
+  double* x0;                /* [B][n_D] initial latents used */
+  double* lam0;              /* [B][n_C] initial multipliers used */
+} ddnm_solve_out;
+
+/* One eval_gradients (sqp.py:117-146) per mu at a given (x, lam), with every
+ * intermediate of the HR closure (driver.py:404-432) for parity tests.
+ * Per-block arrays are concatenated over blocks in block order.  Any pointer
+ * may be NULL. */
+typedef struct {
+  double* rho;               /* [B][n_D] */
+  double* con;               /* [B][n_C] */
+  double* merit;             /* [B] */
+  double* objective;         /* [B] */
+  double* Br;                /* [B][total_rows] */
+  double* R;                 /* [B][total_R]  per block [n_rows][n_int+n_gam] = [R_int | R_gam] */
+  double* cval;              /* [B][n_blocks][n_C] */
+  double* cjac;              /* [B][total_cjac] per block [n_C][n_gam] */
+  double* int_g;             /* [B][total_int_out] interior subnet outputs */
+  double* int_J;             /* [B][total_int_J] */
+  double* gam_g;             /* [B][total_gam_out] full interface decoder */
+  double* gam_J;             /* [B][total_gam_J] */
+  double* bvals;             /* [B][total_rows][3] sampled (bx, by, c) of assemble() */
+  double* step;              /* [B][n_D + n_C] KKT step (s, s_lam) at (x, lam) */
+  int32_t* kkt_status;       /* [B] 0 ok, 1 regularized, 2 singular */
+} ddnm_eval_out;
+
+typedef struct ddnm_ctx ddnm_ctx;
+
+const char* ddnm_last_error(void);
+int ddnm_abi_version(void);
+
+/* Upload the artifacts and plan the kernels.  device < 0 selects the current
+ * device.  slots_per_cta <= 0 picks the default for the instance. */
+int ddnm_ctx_create(int32_t device, const ddnm_artifacts* art,
+                    int32_t slots_per_cta, ddnm_ctx** out);
+int ddnm_ctx_destroy(ddnm_ctx* ctx);
+int ddnm_ctx_info(const ddnm_ctx* ctx, ddnm_info* info);
+
+/* Batched solve_rom (driver.py:554-597, compute_error=False) for B parameters
+ * mu[B][2] = (a, lambda).  x0 == NULL: RBF initial latents on device
+ * (driver.py:82-90); lam0 == NULL: least-squares multipliers on device
+ * (driver.py:461-471).  Host pointers; copies are synchronous. */
+int ddnm_solve_batch(ddnm_ctx* ctx, int32_t B, const double* mu,
+                     const double* x0, const double* lam0,
+                     const ddnm_sqp_cfg* cfg, ddnm_solve_out* out);
+
+/* Same with device-resident inputs/outputs, asynchronous on `stream`
+ * (a cudaStream_t; NULL = the context's stream). */
+int ddnm_solve_batch_device(ddnm_ctx* ctx, int32_t B, const double* d_mu,
+                            const double* d_x0, const double* d_lam0,
+                            const ddnm_sqp_cfg* cfg, ddnm_solve_out* d_out,
+                            void* stream);
+
+/* Batched eval_gradients at (x, lam) with all intermediates (host pointers). */
+int ddnm_eval_batch(ddnm_ctx* ctx, int32_t B, const double* mu,
+                    const double* x, const double* lam, double reg_scale,
+                    ddnm_eval_out* out);
+
+/* Device work counters of the last solve (for the roofline): total block
+ * evaluations and KKT solves executed. */
+int ddnm_last_counters(const ddnm_ctx* ctx, int64_t* evals, int64_t* kkts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDNM_H */

@@ -1,0 +1,612 @@
+// C ABI of libddnm.so (include/ddnm.h): context management, host-side setup
+// of the device tables (the RestrictedResidual stencil of partition.py:361-425
+// in local-column form), kernel planning and launches.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/ddnm.h"
+#include "ddnm_solve.cuh"
+
+using namespace ddnm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(DDNM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+// one compiled specialisation of the kernels
+struct Kernels {
+  int ni, ng, g;
+  const void* solve;
+  const void* eval;
+};
+
+template <int G, int NI, int NG>
+Kernels make_kernels() {
+  return Kernels{NI, NG, G, (const void*)&k_solve<G, NI, NG>, (const void*)&k_eval<G, NI, NG>};
+}
+
+// (n_int, n_gam) pairs with compiled kernels: config 0/2 NM (6,4), config 1
+// LS (20,8), configs 3/4 (8,5), and the small test instances (4,3), (8,4).
+const std::vector<Kernels>& kernel_table() {
+  static const std::vector<Kernels> t = {
+      make_kernels<1, 6, 4>(),  make_kernels<2, 6, 4>(),  make_kernels<4, 6, 4>(),
+      make_kernels<1, 4, 3>(),  make_kernels<2, 4, 3>(),
+      make_kernels<1, 8, 4>(),  make_kernels<2, 8, 4>(),
+      make_kernels<1, 20, 8>(),
+      make_kernels<1, 8, 5>(),  make_kernels<2, 8, 5>(),
+  };
+  return t;
+}
+
+}  // namespace
+
+struct ddnm_ctx {
+  int device = 0;
+  int sms = 0;
+  Params P{};                 // template params (work fields filled per call)
+  Kernels K{};
+  int threads = 256;
+  int ctas = 0;               // persistent grid
+  size_t smem = 0;
+  int n_D = 0, n_C = 0, nb = 0;
+  int tot_rows = 0, tot_iout = 0, tot_gout = 0, tot_R = 0, tot_cjac = 0, tot_intJ = 0,
+      tot_gamJ = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> allocs;  // weights, tables
+  double* gbv = nullptr;      // boundary values per global slot
+  size_t gbv_slots = 0;
+  int* work = nullptr;
+  unsigned long long* counters = nullptr;
+  unsigned long long last_counters[2] = {0, 0};
+  // host-API staging buffers
+  std::map<std::string, std::pair<void*, size_t>> io;
+};
+
+namespace {
+
+template <typename T>
+int upload(ddnm_ctx* c, const T* h, size_t n, T** d) {
+  *d = nullptr;
+  if (n == 0) return 0;
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, n * sizeof(T)));
+  c->allocs.push_back(p);
+  CUDA_TRY(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+  *d = static_cast<T*>(p);
+  return 0;
+}
+
+int upload_i32(ddnm_ctx* c, const int64_t* h, size_t n, int** d) {
+  std::vector<int> v(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (h[i] < INT32_MIN || h[i] > INT32_MAX) return fail(DDNM_EINVAL, "index out of int32 range");
+    v[i] = (int)h[i];
+  }
+  return upload(c, v.data(), n, d);
+}
+
+int io_buf(ddnm_ctx* c, const std::string& name, size_t bytes, void** p) {
+  auto it = c->io.find(name);
+  if (it != c->io.end() && it->second.second >= bytes) {
+    *p = it->second.first;
+    return 0;
+  }
+  if (it != c->io.end()) cudaFree(it->second.first);
+  void* q = nullptr;
+  CUDA_TRY(cudaMalloc(&q, std::max<size_t>(bytes, 8)));
+  c->io[name] = {q, bytes};
+  *p = q;
+  return 0;
+}
+
+// RestrictedResidual rows (partition.py:361-425) in local-column form.
+int build_stencil(const ddnm_artifacts* a, const ddnm_block& blk, std::vector<StRow>& out) {
+  const int nx = a->nx, ny = a->ny;
+  const int n = nx * ny;
+  const double hx = 2.0 / (nx + 1), hy = 0.05 / (ny + 1), nu = a->nu;
+  const double cx = -1.0 / (2.0 * hx), cyy = -1.0 / (2.0 * hy);
+  const double dx = nu / (hx * hx), dy = nu / (hy * hy);
+  std::vector<int> lookup(2 * (size_t)n, -1);
+  for (int k = 0; k < blk.n_cols; ++k) {
+    const int64_t c = blk.cols[k];
+    if (c < 0 || c >= 2 * (int64_t)n) return fail(DDNM_EINVAL, "column index out of range");
+    lookup[c] = k;
+  }
+  out.resize(blk.n_rows);
+  for (int r = 0; r < blk.n_rows; ++r) {
+    const int64_t gr = blk.res_rows[r];
+    if (gr < 0 || gr >= 2 * (int64_t)n) return fail(DDNM_EINVAL, "residual row out of range");
+    const bool isv = gr >= n;
+    const int p = (int)(isv ? gr - n : gr);
+    const int off = isv ? n : 0;
+    const int i = p % nx, j = p / nx;
+    // global column -> (bx, by, cd) coefficients, columns sorted ascending
+    std::map<int, std::array<double, 3>> ent;
+    auto add = [&](int gc, int which, double w) { ent[gc][which] = w; };
+    if (i > 0) add(off + p - 1, 0, cx * -1.0);
+    if (i < nx - 1) add(off + p + 1, 0, cx * 1.0);
+    if (j > 0) add(off + p - nx, 1, cyy * -1.0);
+    if (j < ny - 1) add(off + p + nx, 1, cyy * 1.0);
+    if (j > 0) add(off + p - nx, 2, dy * 1.0);
+    if (i > 0) add(off + p - 1, 2, dx * 1.0);
+    add(off + p, 2, dx * -2.0 + dy * -2.0);
+    if (i < nx - 1) add(off + p + 1, 2, dx * 1.0);
+    if (j < ny - 1) add(off + p + nx, 2, dy * 1.0);
+    ent[isv ? p : n + p];  // cross-component diagonal (E_u / E_v)
+    if ((int)ent.size() > MAXE) return fail(DDNM_EINVAL, "stencil row wider than 6");
+    StRow& row = out[r];
+    std::memset(&row, 0, sizeof(row));
+    row.gu = lookup[p];
+    row.gv = lookup[n + p];
+    if (row.gu < 0 || row.gv < 0)
+      return fail(DDNM_EINVAL, "diagonal coupling column missing from the provided column set");
+    int e = 0;
+    for (auto& kv : ent) {
+      const int lc = lookup[kv.first];
+      if (lc < 0)
+        return fail(DDNM_EINVAL, "restricted rows reference columns outside the provided column set");
+      row.col[e] = lc;
+      row.bxc[e] = kv.second[0];
+      row.byc[e] = kv.second[1];
+      row.cdc[e] = kv.second[2];
+      ++e;
+    }
+    row.nent = e;
+    row.bflags = (i == 0 ? 1 : 0) | (i == nx - 1 ? 2 : 0) | (j == 0 ? 4 : 0) |
+                 (j == ny - 1 ? 8 : 0) | (isv ? 16 : 0);
+    row.xc = -1.0 + hx * (i + 1);
+    row.yc = hy * (j + 1);
+  }
+  return 0;
+}
+
+int check_decoder(const ddnm_decoder& d, int lat, int kind, const char* what) {
+  char buf[160];
+  if (d.n_out < 0 || !d.W1) {
+    snprintf(buf, sizeof buf, "%s decoder: missing weights", what);
+    return fail(DDNM_EINVAL, buf);
+  }
+  if (kind == DDNM_MAP_AUTOENCODER) {
+    if (d.n_hidden <= 0 || !d.b1 || !d.indptr || !d.indices || !d.data || !d.scale || !d.shift) {
+      snprintf(buf, sizeof buf, "%s decoder: incomplete autoencoder arrays", what);
+      return fail(DDNM_EINVAL, buf);
+    }
+    if (d.indptr[0] != 0) return fail(DDNM_EINVAL, "CSR indptr must start at 0");
+    for (int o = 0; o < d.n_out; ++o)
+      if (d.indptr[o + 1] < d.indptr[o]) return fail(DDNM_EINVAL, "CSR indptr not monotone");
+    const int64_t nnz = d.indptr[d.n_out];
+    for (int64_t e = 0; e < nnz; ++e)
+      if (d.indices[e] < 0 || d.indices[e] >= d.n_hidden)
+        return fail(DDNM_EINVAL, "CSR hidden index out of range");
+  }
+  (void)lat;
+  return 0;
+}
+
+int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev& d) {
+  d.n_out = h.n_out;
+  d.n_hidden = kind == DDNM_MAP_AUTOENCODER ? h.n_hidden : 0;
+  int rc;
+  if (kind == DDNM_MAP_AUTOENCODER) {
+    const size_t nnz = (size_t)h.indptr[h.n_out];
+    if ((rc = upload(c, h.W1, (size_t)h.n_hidden * lat, const_cast<double**>(&d.W1)))) return rc;
+    if ((rc = upload(c, h.b1, (size_t)h.n_hidden, const_cast<double**>(&d.b1)))) return rc;
+    if ((rc = upload_i32(c, h.indptr, (size_t)h.n_out + 1, const_cast<int**>(&d.indptr)))) return rc;
+    if ((rc = upload_i32(c, h.indices, nnz, const_cast<int**>(&d.indices)))) return rc;
+    if ((rc = upload(c, h.data, nnz, const_cast<double**>(&d.data)))) return rc;
+    if ((rc = upload(c, h.scale, (size_t)h.n_out, const_cast<double**>(&d.scale)))) return rc;
+    if ((rc = upload(c, h.shift, (size_t)h.n_out, const_cast<double**>(&d.shift)))) return rc;
+  } else {
+    if ((rc = upload(c, h.W1, (size_t)h.n_out * lat, const_cast<double**>(&d.W1)))) return rc;
+    d.b1 = nullptr; d.indptr = nullptr; d.indices = nullptr; d.data = nullptr;
+    d.scale = nullptr; d.shift = nullptr;
+  }
+  return 0;
+}
+
+int64_t nnz_of(const ddnm_decoder& d, int kind) {
+  return kind == DDNM_MAP_AUTOENCODER ? d.indptr[d.n_out] : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ddnm_last_error(void) { return g_err.c_str(); }
+int ddnm_abi_version(void) { return DDNM_ABI_VERSION; }
+
+int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm_ctx** out) {
+  if (!a || !out) return fail(DDNM_EINVAL, "null argument");
+  *out = nullptr;
+  if (a->abi_version != DDNM_ABI_VERSION) return fail(DDNM_EINVAL, "ABI version mismatch");
+  if (a->n_blocks < 1 || a->n_blocks > MAXB) return fail(DDNM_EINVAL, "need 1..16 blocks");
+  if (a->n_c < 1) return fail(DDNM_EINVAL, "multiplier dimension must be positive");
+  if (a->nx < 2 || a->ny < 2 || !(a->nu > 0)) return fail(DDNM_EINVAL, "bad grid");
+  if (a->map_kind != DDNM_MAP_AUTOENCODER && a->map_kind != DDNM_MAP_LINEAR)
+    return fail(DDNM_EINVAL, "unknown map kind");
+  const int ni = a->blocks[0].n_int, ng = a->blocks[0].n_gam;
+  for (int b = 0; b < a->n_blocks; ++b) {
+    const ddnm_block& k = a->blocks[b];
+    if (k.n_int != ni || k.n_gam != ng)
+      return fail(DDNM_EUNSUPPORTED, "blocks with different latent dims are not compiled");
+    if (k.interior.n_out != k.n_io) return fail(DDNM_EINVAL, "interior decoder outputs != n_io");
+    if (k.n_cols != k.n_io + k.n_gio) return fail(DDNM_EINVAL, "n_cols != n_io + n_gio");
+    if (k.n_rows < 1) return fail(DDNM_EINVAL, "sample row set is empty");
+    if (!k.CA) return fail(DDNM_EINVAL, "missing CA");
+    int rc;
+    if ((rc = check_decoder(k.interior, ni, a->map_kind, "interior"))) return rc;
+    if ((rc = check_decoder(k.interface, ng, a->map_kind, "interface"))) return rc;
+    for (int g = 0; g < k.n_gio; ++g)
+      if (k.gio[g] < 0 || k.gio[g] >= k.interface.n_out) return fail(DDNM_EINVAL, "gio out of range");
+  }
+  auto* c = new ddnm_ctx();
+  int rc = 0;
+  auto bail = [&](int r) {
+    ddnm_ctx_destroy(c);
+    return r;
+  };
+  if (device < 0) {
+    if (cudaGetDevice(&device) != cudaSuccess) return bail(fail(DDNM_ECUDA, "no CUDA device"));
+  }
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DDNM_ECUDA, "cudaSetDevice failed"));
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return bail(fail(DDNM_ECUDA, "cudaGetDeviceProperties failed"));
+  if (prop.major != 10) return bail(fail(DDNM_EUNSUPPORTED, "libddnm is built for sm_100a (B200)"));
+  c->sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(DDNM_ECUDA, "stream create failed"));
+
+  Params& P = c->P;
+  std::memset(&P, 0, sizeof(P));
+  P.nb = a->n_blocks;
+  P.n_C = a->n_c;
+  P.map_kind = a->map_kind;
+  P.act = a->activation;
+  P.nx = a->nx;
+  P.ny = a->ny;
+  P.nu = a->nu;
+  P.hx = 2.0 / (a->nx + 1);
+  P.hy = 0.05 / (a->ny + 1);
+  const int W = ni + ng;
+  int xoff = 0, row_off = 0, iout = 0, gout = 0, Roff = 0, cjoff = 0, ijoff = 0, gjoff = 0, eboff = 0;
+  int max_nh = 0, max_io = 0, max_gam = 0, max_rows = 0;
+  for (int b = 0; b < P.nb; ++b) {
+    const ddnm_block& k = a->blocks[b];
+    BlockDev& B = P.blk[b];
+    B.ni = ni; B.ng = ng; B.w = W;
+    B.nrows = k.n_rows; B.n_io = k.n_io; B.n_gio = k.n_gio;
+    B.xoff = xoff; B.row_off = row_off; B.iout_off = iout; B.gout_off = gout; B.R_off = Roff;
+    B.cjac_off = cjoff; B.intJ_off = ijoff; B.gamJ_off = gjoff; B.eb_off = eboff;
+    if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, B.in))) return bail(rc);
+    if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, B.ga))) return bail(rc);
+    std::vector<StRow> rows;
+    if ((rc = build_stencil(a, k, rows))) return bail(rc);
+    if ((rc = upload(c, rows.data(), rows.size(), const_cast<StRow**>(&B.rows)))) return bail(rc);
+    if ((rc = upload_i32(c, k.gio, (size_t)k.n_gio, const_cast<int**>(&B.gio)))) return bail(rc);
+    if ((rc = upload(c, k.CA, (size_t)P.n_C * k.interface.n_out, const_cast<double**>(&B.CA)))) return bail(rc);
+    xoff += W; row_off += k.n_rows; iout += k.n_io; gout += k.interface.n_out;
+    Roff += k.n_rows * W; cjoff += P.n_C * ng; ijoff += k.n_io * ni; gjoff += k.interface.n_out * ng;
+    eboff += W * W + W + P.n_C + P.n_C * ng + 1;
+    max_nh = std::max(max_nh, B.in.n_hidden + B.ga.n_hidden);
+    max_io = std::max(max_io, k.n_io);
+    max_gam = std::max(max_gam, k.interface.n_out);
+    max_rows = std::max(max_rows, k.n_rows);
+  }
+  P.n_D = xoff;
+  P.nK = P.n_D + P.n_C;
+  P.total_rows = row_off;
+  P.tot_iout = iout; P.tot_gout = gout; P.tot_R = Roff; P.tot_cjac = cjoff;
+  P.tot_intJ = ijoff; P.tot_gamJ = gjoff;
+  c->n_D = P.n_D; c->n_C = P.n_C; c->nb = P.nb;
+  c->tot_rows = row_off; c->tot_iout = iout; c->tot_gout = gout; c->tot_R = Roff;
+  c->tot_cjac = cjoff; c->tot_intJ = ijoff; c->tot_gamJ = gjoff;
+  // RBF
+  const ddnm_rbf& r = a->rbf;
+  P.rbf_P = r.n_centers; P.rbf_R = r.n_mono;
+  if (r.n_centers > 0) {
+    if ((rc = upload(c, r.y, (size_t)r.n_centers * 2, const_cast<double**>(&P.rbf_y)))) return bail(rc);
+    if ((rc = upload(c, r.coeffs, (size_t)(r.n_centers + r.n_mono) * P.n_D,
+                     const_cast<double**>(&P.rbf_coeffs)))) return bail(rc);
+    if ((rc = upload_i32(c, r.powers, (size_t)r.n_mono * 2, const_cast<int**>(&P.rbf_pow)))) return bail(rc);
+    for (int k = 0; k < 2; ++k) {
+      P.rbf_shift[k] = r.shift[k]; P.rbf_scale[k] = r.scale[k];
+      P.rbf_lo[k] = r.lo[k]; P.rbf_hi[k] = r.hi[k];
+    }
+    P.rbf_eps = r.epsilon;
+  }
+  // shared-memory plan (doubles)
+  const bool ae = a->map_kind == DDNM_MAP_AUTOENCODER;
+  int scr = 0;
+  P.scr_sig = scr; scr += ae ? max_nh : 0;
+  P.scr_dsig = scr; scr += ae ? max_nh : 0;
+  P.scr_gint = scr; scr += max_io;
+  P.scr_jint = scr; scr += ae ? max_io * ni : 0;
+  P.scr_ggam = scr; scr += max_gam;
+  P.scr_jgam = scr; scr += ae ? max_gam * ng : 0;
+  P.scr_R = scr; scr += max_rows * W;
+  P.scr_r = scr; scr += max_rows;
+  const int kkt_need = P.nK * (P.nK + 1) + 5 * P.nK;
+  const int ls_need = P.nb * ng * P.n_C + P.nb * ng;
+  const int rbf_need = r.n_centers + r.n_mono;
+  P.scr_size = std::max(std::max(scr, kkt_need), std::max(ls_need, rbf_need));
+  P.scr_size = (P.scr_size + 1) & ~1;
+  P.eb_size = eboff + P.n_D + P.n_C + 2;
+  P.eb_rho = eboff; P.eb_con = eboff + P.n_D; P.eb_scal = eboff + P.n_D + P.n_C;
+  P.eb_size = (P.eb_size + 1) & ~1;
+  const int state_d = (int)((sizeof(SlotState) + 7) / 8);
+  // pick G: the largest compiled G whose footprint fits 227 KB
+  const size_t smem_cap = (size_t)prop.sharedMemPerBlockOptin - 1024;
+  auto footprint = [&](int G) {
+    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + P.scr_size)) * 8;
+  };
+  const Kernels* kern = nullptr;
+  for (const auto& k : kernel_table()) {
+    if (k.ni != ni || k.ng != ng) continue;
+    if (slots > 0 && k.g != slots) continue;
+    if (footprint(k.g) > smem_cap) continue;
+    if (!kern || k.g > kern->g) kern = &k;
+    if (slots <= 0 && kern->g >= 2) break;
+  }
+  if (!kern) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "no compiled kernel for n_int=%d n_gam=%d slots=%d fitting %zu B smem",
+             ni, ng, slots, smem_cap);
+    return bail(fail(DDNM_EUNSUPPORTED, buf));
+  }
+  c->K = *kern;
+  P.G = kern->g;
+  P.sm_state = 0;
+  P.sm_vec = state_d * P.G;
+  P.sm_eb = P.sm_vec + P.G * 8 * P.nK;
+  P.sm_scr = P.sm_eb + P.G * 2 * P.eb_size;
+  c->smem = footprint(P.G);
+  if (cudaFuncSetAttribute(kern->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
+      cudaFuncSetAttribute(kern->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess)
+    return bail(fail(DDNM_ECUDA, "cannot reserve dynamic shared memory"));
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern->solve, c->threads, c->smem) != cudaSuccess || occ < 1)
+    return bail(fail(DDNM_ECUDA, "kernel does not fit on an SM"));
+  c->ctas = occ * c->sms;
+  if (cudaMalloc(&c->work, 4 * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->counters, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(DDNM_ECUDA, "cudaMalloc failed"));
+  *out = c;
+  return 0;
+}
+
+int ddnm_ctx_destroy(ddnm_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto& kv : c->io) cudaFree(kv.second.first);
+  if (c->gbv) cudaFree(c->gbv);
+  if (c->work) cudaFree(c->work);
+  if (c->counters) cudaFree(c->counters);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+int ddnm_ctx_info(const ddnm_ctx* c, ddnm_info* i) {
+  if (!c || !i) return fail(DDNM_EINVAL, "null argument");
+  i->n_primal = c->n_D;
+  i->n_mult = c->n_C;
+  i->n_blocks = c->nb;
+  i->total_rows = c->tot_rows;
+  i->total_int_out = c->tot_iout;
+  i->total_gam_out = c->tot_gout;
+  i->total_R = c->tot_R;
+  i->total_cjac = c->tot_cjac;
+  i->total_int_J = c->tot_intJ;
+  i->total_gam_J = c->tot_gamJ;
+  i->slots_per_cta = c->P.G;
+  i->ctas = c->ctas;
+  i->smem_bytes = (int32_t)c->smem;
+  i->device = c->device;
+  return 0;
+}
+
+static int ensure_gbv(ddnm_ctx* c, size_t slots) {
+  if (c->gbv_slots >= slots) return 0;
+  if (c->gbv) cudaFree(c->gbv);
+  c->gbv = nullptr;
+  CUDA_TRY(cudaMalloc(&c->gbv, std::max<size_t>(slots, 1) * c->tot_rows * 3 * sizeof(double)));
+  c->gbv_slots = slots;
+  return 0;
+}
+
+static int fill_nan(cudaStream_t s, double* p, size_t n) {
+  if (!p || n == 0) return 0;
+  k_fill<<<148, 256, 0, s>>>(p, n, NAN);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0,
+                            const double* d_lam0, const ddnm_sqp_cfg* cfg, ddnm_solve_out* o,
+                            void* stream) {
+  if (!c || !cfg || !o || !d_mu || !o->x || !o->lam) return fail(DDNM_EINVAL, "null argument");
+  if (B < 0) return fail(DDNM_EINVAL, "negative batch");
+  if (!(cfg->tol > 0) || cfg->max_iter < 1 || !(cfg->armijo_c1 > 0) || !(cfg->backtrack_factor > 0) ||
+      !(cfg->backtrack_factor < 1) || cfg->max_halvings < 0)
+    return fail(DDNM_EINVAL, "invalid solver configuration");
+  if (!d_x0 && c->P.rbf_P == 0) return fail(DDNM_EINVAL, "instance has no fitted initializer");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if (B == 0) return 0;
+  const int ctas = std::min(c->ctas, (B + c->P.G - 1) / c->P.G);
+  int rc;
+  if ((rc = ensure_gbv(c, (size_t)ctas * c->P.G))) return rc;
+  Params P = c->P;
+  P.B = B;
+  P.mu = d_mu;
+  P.x0_in = d_x0;
+  P.lam0_in = d_lam0;
+  P.cfg.tol = cfg->tol;
+  P.cfg.c1 = cfg->armijo_c1;
+  P.cfg.factor = cfg->backtrack_factor;
+  P.cfg.reg_scale = cfg->reg_scale;
+  P.cfg.max_iter = cfg->max_iter;
+  P.cfg.max_halvings = cfg->max_halvings;
+  P.so.x = o->x; P.so.lam = o->lam; P.so.merit = o->merit; P.so.objective = o->objective;
+  P.so.merit_hist = o->merit_hist; P.so.obj_hist = o->obj_hist; P.so.alpha_hist = o->alpha_hist;
+  P.so.x0 = o->x0; P.so.lam0 = o->lam0;
+  P.so.n_iter = o->n_iter; P.so.n_evals = o->n_evals; P.so.status = o->status; P.so.n_reg = o->n_reg;
+  P.gbv = c->gbv;
+  P.work = c->work;
+  P.counters = c->counters;
+  if ((rc = fill_nan(s, o->merit_hist, (size_t)B * (cfg->max_iter + 1)))) return rc;
+  if ((rc = fill_nan(s, o->obj_hist, (size_t)B * (cfg->max_iter + 1)))) return rc;
+  if ((rc = fill_nan(s, o->alpha_hist, (size_t)B * cfg->max_iter))) return rc;
+  CUDA_TRY(cudaMemsetAsync(c->work, 0, 4 * sizeof(int), s));
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(unsigned long long), s));
+  void* args[] = {&P};
+  CUDA_TRY(cudaLaunchKernel(c->K.solve, dim3(ctas), dim3(c->threads), args, c->smem, s));
+  return 0;
+}
+
+int ddnm_last_counters(const ddnm_ctx* c, int64_t* evals, int64_t* kkts) {
+  if (!c) return fail(DDNM_EINVAL, "null argument");
+  unsigned long long h[2] = {0, 0};
+  CUDA_TRY(cudaMemcpy(h, c->counters, sizeof h, cudaMemcpyDeviceToHost));
+  if (evals) *evals = (int64_t)h[0];
+  if (kkts) *kkts = (int64_t)h[1];
+  return 0;
+}
+
+int ddnm_solve_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x0, const double* lam0,
+                     const ddnm_sqp_cfg* cfg, ddnm_solve_out* o) {
+  if (!c || !cfg || !o || !mu || !o->x || !o->lam) return fail(DDNM_EINVAL, "null argument");
+  if (B <= 0) return B == 0 ? 0 : fail(DDNM_EINVAL, "negative batch");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t nD = c->n_D, nC = c->n_C, K1 = cfg->max_iter + 1, K = cfg->max_iter;
+  cudaStream_t s = c->stream;
+  struct Field { const char* name; void* host; size_t bytes; bool in; };
+  ddnm_solve_out d{};
+  void* dmu = nullptr; void* dx0 = nullptr; void* dl0 = nullptr;
+  int rc;
+  if ((rc = io_buf(c, "mu", B * 2 * 8, &dmu))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dmu, mu, B * 2 * 8, cudaMemcpyHostToDevice, s));
+  if (x0) {
+    if ((rc = io_buf(c, "x0in", B * nD * 8, &dx0))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(dx0, x0, B * nD * 8, cudaMemcpyHostToDevice, s));
+  }
+  if (lam0) {
+    if ((rc = io_buf(c, "l0in", B * nC * 8, &dl0))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(dl0, lam0, B * nC * 8, cudaMemcpyHostToDevice, s));
+  }
+  Field f[] = {
+      {"x", o->x, B * nD * 8, false},           {"lam", o->lam, B * nC * 8, false},
+      {"n_iter", o->n_iter, B * 4ul, false},    {"n_evals", o->n_evals, B * 4ul, false},
+      {"status", o->status, B * 4ul, false},    {"n_reg", o->n_reg, B * 4ul, false},
+      {"merit", o->merit, B * 8ul, false},      {"objective", o->objective, B * 8ul, false},
+      {"merit_hist", o->merit_hist, B * K1 * 8, false}, {"obj_hist", o->obj_hist, B * K1 * 8, false},
+      {"alpha_hist", o->alpha_hist, B * K * 8, false},  {"x0", o->x0, B * nD * 8, false},
+      {"lam0", o->lam0, B * nC * 8, false},
+  };
+  void* dp[13];
+  for (int i = 0; i < 13; ++i) {
+    dp[i] = nullptr;
+    if (f[i].host && (rc = io_buf(c, std::string("o_") + f[i].name, f[i].bytes, &dp[i]))) return rc;
+  }
+  d.x = (double*)dp[0]; d.lam = (double*)dp[1]; d.n_iter = (int*)dp[2]; d.n_evals = (int*)dp[3];
+  d.status = (int*)dp[4]; d.n_reg = (int*)dp[5]; d.merit = (double*)dp[6]; d.objective = (double*)dp[7];
+  d.merit_hist = (double*)dp[8]; d.obj_hist = (double*)dp[9]; d.alpha_hist = (double*)dp[10];
+  d.x0 = (double*)dp[11]; d.lam0 = (double*)dp[12];
+  if ((rc = ddnm_solve_batch_device(c, B, (double*)dmu, (double*)dx0, (double*)dl0, cfg, &d, s))) return rc;
+  for (int i = 0; i < 13; ++i)
+    if (f[i].host) CUDA_TRY(cudaMemcpyAsync(f[i].host, dp[i], f[i].bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, const double* lam,
+                    double reg_scale, ddnm_eval_out* o) {
+  if (!c || !o || !mu || !x || !lam) return fail(DDNM_EINVAL, "null argument");
+  if (B <= 0) return B == 0 ? 0 : fail(DDNM_EINVAL, "negative batch");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t nD = c->n_D, nC = c->n_C;
+  int rc;
+  void *dmu, *dx, *dl;
+  if ((rc = io_buf(c, "mu", B * 2 * 8, &dmu)) || (rc = io_buf(c, "ex", B * nD * 8, &dx)) ||
+      (rc = io_buf(c, "el", B * nC * 8, &dl)))
+    return rc;
+  CUDA_TRY(cudaMemcpyAsync(dmu, mu, B * 2 * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(dx, x, B * nD * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(dl, lam, B * nC * 8, cudaMemcpyHostToDevice, s));
+  struct Field { const char* name; void* host; size_t bytes; };
+  Field f[] = {
+      {"rho", o->rho, B * nD * 8},
+      {"con", o->con, B * nC * 8},
+      {"merit", o->merit, B * 8ul},
+      {"objective", o->objective, B * 8ul},
+      {"Br", o->Br, B * (size_t)c->tot_rows * 8},
+      {"R", o->R, B * (size_t)c->tot_R * 8},
+      {"cval", o->cval, B * (size_t)c->nb * nC * 8},
+      {"cjac", o->cjac, B * (size_t)c->tot_cjac * 8},
+      {"int_g", o->int_g, B * (size_t)c->tot_iout * 8},
+      {"int_J", o->int_J, B * (size_t)c->tot_intJ * 8},
+      {"gam_g", o->gam_g, B * (size_t)c->tot_gout * 8},
+      {"gam_J", o->gam_J, B * (size_t)c->tot_gamJ * 8},
+      {"bvals", o->bvals, B * (size_t)c->tot_rows * 3 * 8},
+      {"step", o->step, B * (nD + nC) * 8},
+      {"kkt_status", o->kkt_status, B * 4ul},
+  };
+  constexpr int NF = 15;
+  void* dp[NF];
+  for (int i = 0; i < NF; ++i) {
+    dp[i] = nullptr;
+    if (f[i].host && (rc = io_buf(c, std::string("e_") + f[i].name, f[i].bytes, &dp[i]))) return rc;
+  }
+  const int G = c->P.G;
+  const int ctas = (B + G - 1) / G;
+  if ((rc = ensure_gbv(c, (size_t)ctas * G))) return rc;
+  Params P = c->P;
+  P.B = B;
+  P.mu = (double*)dmu;
+  P.x0_in = (double*)dx;
+  P.lam0_in = (double*)dl;
+  P.cfg.reg_scale = reg_scale;
+  P.eo.rho = (double*)dp[0]; P.eo.con = (double*)dp[1]; P.eo.merit = (double*)dp[2];
+  P.eo.objective = (double*)dp[3]; P.eo.Br = (double*)dp[4]; P.eo.R = (double*)dp[5];
+  P.eo.cval = (double*)dp[6]; P.eo.cjac = (double*)dp[7]; P.eo.int_g = (double*)dp[8];
+  P.eo.int_J = (double*)dp[9]; P.eo.gam_g = (double*)dp[10]; P.eo.gam_J = (double*)dp[11];
+  P.eo.bvals = (double*)dp[12]; P.eo.step = (double*)dp[13]; P.eo.kkt_status = (int*)dp[14];
+  P.eval_mode = 1;
+  P.eval_step = (o->step || o->kkt_status) ? 1 : 0;
+  P.gbv = c->gbv;
+  P.work = c->work;
+  P.counters = c->counters;
+  void* args[] = {&P};
+  CUDA_TRY(cudaLaunchKernel(c->K.eval, dim3(ctas), dim3(c->threads), args, c->smem, s));
+  for (int i = 0; i < NF; ++i)
+    if (f[i].host) CUDA_TRY(cudaMemcpyAsync(f[i].host, dp[i], f[i].bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

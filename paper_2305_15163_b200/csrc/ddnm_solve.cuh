@@ -1,0 +1,982 @@
+// Persistent batched SQP megakernel: see ddnm_device.cuh for the design.
+#pragma once
+#include "ddnm_device.cuh"
+
+namespace ddnm {
+
+// --------------------------------------------------------------------------
+// shared-memory views
+
+struct View {
+  const Params& P;
+  double* sm;
+  __device__ View(const Params& p, double* s) : P(p), sm(s) {}
+  __device__ SlotState* st() const { return reinterpret_cast<SlotState*>(sm + P.sm_state); }
+  // vectors: 0 x, 1 lam, 2 s, 3 slam, 4 xt, 5 lt, 6 best x, 7 best lam
+  __device__ double* vec(int s, int which) const { return sm + P.sm_vec + (s * 8 + which) * P.nK; }
+  __device__ double* eb(int s, int which) const { return sm + P.sm_eb + (s * 2 + which) * P.eb_size; }
+  __device__ double* scr(int s) const { return sm + P.sm_scr + s * P.scr_size; }
+};
+
+// block pieces inside an eval buffer
+__device__ __forceinline__ double* eb_H(double* e, const BlockDev& B) { return e + B.eb_off; }
+__device__ __forceinline__ double* eb_proj(double* e, const BlockDev& B) { return e + B.eb_off + B.w * B.w; }
+__device__ __forceinline__ double* eb_cval(double* e, const BlockDev& B) { return e + B.eb_off + B.w * B.w + B.w; }
+__device__ __forceinline__ double* eb_cjac(double* e, const BlockDev& B, int nC) {
+  return e + B.eb_off + B.w * B.w + B.w + nC;
+}
+__device__ __forceinline__ double* eb_rr(double* e, const BlockDev& B, int nC) {
+  return e + B.eb_off + B.w * B.w + B.w + nC + nC * B.ng;
+}
+
+// --------------------------------------------------------------------------
+// phase A: one hidden unit for all active slots.
+// z accumulates latent column by latent column with separately rounded
+// products, exactly as hyper.py:184-188 / autoencoder.py:134-140.
+template <int G, int L>
+__device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int k, int xo,
+                                            int sig_off, unsigned mask) {
+  double w[L];
+#pragma unroll
+  for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1 + (size_t)k * L + d);
+  const double b = __ldg(D.b1 + k);
+#pragma unroll
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    const double* x = V.vec(s, 4) + xo;
+    double z = b;
+#pragma unroll
+    for (int d = 0; d < L; ++d) z = __dadd_rn(z, __dmul_rn(w[d], x[d]));
+    double a, da;
+    act_pair(V.P.act, z, a, da);
+    double* sc = V.scr(s);
+    sc[V.P.scr_sig + sig_off + k] = a;
+    sc[V.P.scr_dsig + sig_off + k] = da;
+  }
+}
+
+// phase B: one decoder output (value + latent Jacobian row) for all slots.
+// CSR row sweep in storage order (hyper.py:190-197):
+//   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e W2_e act'_e W1[k_e, d]) * scale
+template <int G, int L>
+__device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int sig_off,
+                                             int g_off, int j_off, unsigned mask) {
+  double ag[G], aj[G][L];
+#pragma unroll
+  for (int s = 0; s < G; ++s) {
+    ag[s] = 0.0;
+#pragma unroll
+    for (int d = 0; d < L; ++d) aj[s][d] = 0.0;
+  }
+  const int e0 = __ldg(D.indptr + o), e1 = __ldg(D.indptr + o + 1);
+  for (int e = e0; e < e1; ++e) {
+    const double v = __ldg(D.data + e);
+    const int k = __ldg(D.indices + e);
+    double w[L];
+#pragma unroll
+    for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1 + (size_t)k * L + d);
+#pragma unroll
+    for (int s = 0; s < G; ++s) {
+      if (!((mask >> s) & 1u)) continue;
+      const double* sc = V.scr(s);
+      const double a = sc[V.P.scr_sig + sig_off + k];
+      const double da = sc[V.P.scr_dsig + sig_off + k];
+      ag[s] = fma(v, a, ag[s]);
+      const double t = v * da;
+#pragma unroll
+      for (int d = 0; d < L; ++d) aj[s][d] = fma(t, w[d], aj[s][d]);
+    }
+  }
+  const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
+#pragma unroll
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    double* sc = V.scr(s);
+    sc[g_off + o] = __dadd_rn(__dmul_rn(ag[s], scl), sh);
+#pragma unroll
+    for (int d = 0; d < L; ++d) sc[j_off + o * L + d] = aj[s][d] * scl;
+  }
+}
+
+// phase B for a LinearMap (pod.py:86-93): g = Phi x
+template <int G, int L>
+__device__ __forceinline__ void linear_output(const View& V, const DecDev& D, int o, int xo,
+                                              int g_off, unsigned mask) {
+  double w[L];
+#pragma unroll
+  for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1 + (size_t)o * L + d);
+#pragma unroll
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    const double* x = V.vec(s, 4) + xo;
+    double g = 0.0;
+#pragma unroll
+    for (int d = 0; d < L; ++d) g = fma(w[d], x[d], g);
+    V.scr(s)[g_off + o] = g;
+  }
+}
+
+// phase C (stencil): residual row, dense Jacobian row, chain rule.
+// partition.py:427-464 and driver.py:422-429.
+template <int NI, int NG>
+__device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, int s, int row,
+                                            const double* bv) {
+  const Params& P = V.P;
+  double* sc = V.scr(s);
+  const double* gint = sc + P.scr_gint;
+  const double* ggam = sc + P.scr_ggam;
+  const bool lin = P.map_kind == MAP_LINEAR;
+  const double* Jint = lin ? B.in.W1 : sc + P.scr_jint;   // [n_io][NI]
+  const double* Jgam = lin ? B.ga.W1 : sc + P.scr_jgam;   // [N_gam][NG]
+  const StRow& rw = B.rows[row];
+  auto val = [&](int c) -> double {
+    return c < B.n_io ? gint[c] : ggam[__ldg(B.gio + (c - B.n_io))];
+  };
+  const int ne = rw.nent;
+  double xe[MAXE];
+  double sx = 0.0, sy = 0.0, scd = 0.0;
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    if (e < ne) {
+      xe[e] = val(rw.col[e]);
+      if (rw.bxc[e] != 0.0) sx = __dadd_rn(sx, __dmul_rn(rw.bxc[e], xe[e]));
+      if (rw.byc[e] != 0.0) sy = __dadd_rn(sy, __dmul_rn(rw.byc[e], xe[e]));
+      if (rw.cdc[e] != 0.0) scd = __dadd_rn(scd, __dmul_rn(rw.cdc[e], xe[e]));
+    }
+  }
+  const double xu = val(rw.gu), xv = val(rw.gv);
+  const double bx = bv[0], by = bv[1], bc = bv[2];
+  const double tx = sx - bx, ty = sy - by;
+  // xu*(Bx x - bx) + xv*(By x - by) + Cd x + c  (partition.py:434-441)
+  const double r = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(xu, tx), __dmul_rn(xv, ty)), scd), bc);
+  double Ri[NI], Rg[NG];
+#pragma unroll
+  for (int d = 0; d < NI; ++d) Ri[d] = 0.0;
+#pragma unroll
+  for (int d = 0; d < NG; ++d) Rg[d] = 0.0;
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    if (e < ne) {
+      const int c = rw.col[e];
+      // diag(Bx x - b)E_u + diag(x_u)Bx + diag(x_v)By + diag(By x - b)E_v + Cd
+      double j = 0.0;
+      if (c == rw.gu) j = tx;
+      if (c == rw.gv) j = __dadd_rn(j, ty);
+      if (rw.bxc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xu, rw.bxc[e]));
+      if (rw.byc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xv, rw.byc[e]));
+      if (rw.cdc[e] != 0.0) j = __dadd_rn(j, rw.cdc[e]);
+      if (c < B.n_io) {
+        const double* jr = Jint + (size_t)c * NI;
+#pragma unroll
+        for (int d = 0; d < NI; ++d) Ri[d] = fma(j, jr[d], Ri[d]);
+      } else {
+        const double* jr = Jgam + (size_t)__ldg(B.gio + (c - B.n_io)) * NG;
+#pragma unroll
+        for (int d = 0; d < NG; ++d) Rg[d] = fma(j, jr[d], Rg[d]);
+      }
+    }
+  }
+  double* R = sc + P.scr_R + (size_t)row * (NI + NG);
+#pragma unroll
+  for (int d = 0; d < NI; ++d) R[d] = Ri[d];
+#pragma unroll
+  for (int d = 0; d < NG; ++d) R[NI + d] = Rg[d];
+  sc[P.scr_r + row] = r;
+}
+
+// --------------------------------------------------------------------------
+// one eval_gradients (sqp.py:117-146) for every slot in `mask` at (xt, lt).
+// Results land in eval buffer `ebi[s]` of each slot.
+template <int G, int NI, int NG>
+__device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gslot0,
+                            bool dump) {
+  const Params& P = V.P;
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  SlotState* st = V.st();
+  constexpr int W = NI + NG;
+  for (int b = 0; b < P.nb; ++b) {
+    const BlockDev& B = P.blk[b];
+    const int nhi = P.map_kind == MAP_AE ? B.in.n_hidden : 0;
+    // ---- phase A: hidden layer of both decoders ----
+    if (P.map_kind == MAP_AE) {
+      const int nht = nhi + B.ga.n_hidden;
+      for (int it = tid; it < nht; it += T) {
+        if (it < nhi)
+          hidden_unit<G, NI>(V, B.in, it, B.xoff, 0, mask);
+        else
+          hidden_unit<G, NG>(V, B.ga, it - nhi, B.xoff + NI, nhi, mask);
+      }
+      __syncthreads();
+    }
+    // ---- phase B: outputs (+ Jacobian rows) ----
+    {
+      const int noi = B.in.n_out, not_ = noi + B.ga.n_out;
+      for (int it = tid; it < not_; it += T) {
+        if (P.map_kind == MAP_AE) {
+          if (it < noi)
+            sweep_output<G, NI>(V, B.in, it, 0, P.scr_gint, P.scr_jint, mask);
+          else
+            sweep_output<G, NG>(V, B.ga, it - noi, nhi, P.scr_ggam, P.scr_jgam, mask);
+        } else {
+          if (it < noi)
+            linear_output<G, NI>(V, B.in, it, B.xoff, P.scr_gint, mask);
+          else
+            linear_output<G, NG>(V, B.ga, it - noi, B.xoff + NI, P.scr_ggam, mask);
+        }
+      }
+      __syncthreads();
+    }
+    // ---- phase C: WFPC constraint (warp tasks) + HR stencil rows ----
+    {
+      const int ngo = B.ga.n_out;
+      for (int t = warp; t < G * P.n_C; t += nw) {
+        const int s = t / P.n_C, c = t - s * P.n_C;
+        if (!((mask >> s) & 1u)) continue;
+        const double* sc = V.scr(s);
+        const double* gg = sc + P.scr_ggam;
+        const double* Jg = P.map_kind == MAP_LINEAR ? B.ga.W1 : sc + P.scr_jgam;
+        const double* ca = B.CA + (size_t)c * ngo;
+        double a0 = 0.0, aj[NG];
+#pragma unroll
+        for (int d = 0; d < NG; ++d) aj[d] = 0.0;
+        for (int j = lane; j < ngo; j += WARP) {
+          const double cj = __ldg(ca + j);
+          a0 = fma(cj, gg[j], a0);
+#pragma unroll
+          for (int d = 0; d < NG; ++d) aj[d] = fma(cj, Jg[(size_t)j * NG + d], aj[d]);
+        }
+        a0 = warp_sum(a0);
+#pragma unroll
+        for (int d = 0; d < NG; ++d) aj[d] = warp_sum(aj[d]);
+        if (lane == 0) {
+          double* e = V.eb(s, ebi[s]);
+          eb_cval(e, B)[c] = a0;
+#pragma unroll
+          for (int d = 0; d < NG; ++d) eb_cjac(e, B, P.n_C)[c * NG + d] = aj[d];
+        }
+      }
+      for (int it = tid; it < G * B.nrows; it += T) {
+        const int s = it / B.nrows, row = it - s * B.nrows;
+        if (!((mask >> s) & 1u)) continue;
+        const double* bv = P.gbv + ((size_t)(gslot0 + s) * P.total_rows + B.row_off + row) * 3;
+        stencil_row<NI, NG>(V, B, s, row, bv);
+      }
+      __syncthreads();
+    }
+    // ---- optional dumps of every intermediate (ddnm_eval_batch) ----
+    if (dump) {
+      const EvalOut& o = P.eo;
+      for (int s = 0; s < G; ++s) {
+        if (!((mask >> s) & 1u)) continue;
+        const size_t mu = (size_t)st[s].mu;
+        const double* sc = V.scr(s);
+        const bool lin = P.map_kind == MAP_LINEAR;
+        const double* Jint = lin ? B.in.W1 : sc + P.scr_jint;
+        const double* Jgam = lin ? B.ga.W1 : sc + P.scr_jgam;
+        if (o.int_g)
+          for (int i = tid; i < B.in.n_out; i += T) o.int_g[mu * P.tot_iout + B.iout_off + i] = sc[P.scr_gint + i];
+        if (o.int_J)
+          for (int i = tid; i < B.in.n_out * NI; i += T) o.int_J[mu * P.tot_intJ + B.intJ_off + i] = Jint[i];
+        if (o.gam_g)
+          for (int i = tid; i < B.ga.n_out; i += T) o.gam_g[mu * P.tot_gout + B.gout_off + i] = sc[P.scr_ggam + i];
+        if (o.gam_J)
+          for (int i = tid; i < B.ga.n_out * NG; i += T) o.gam_J[mu * P.tot_gamJ + B.gamJ_off + i] = Jgam[i];
+        if (o.Br)
+          for (int i = tid; i < B.nrows; i += T) o.Br[mu * P.total_rows + B.row_off + i] = sc[P.scr_r + i];
+        if (o.R)
+          for (int i = tid; i < B.nrows * W; i += T) o.R[mu * P.tot_R + B.R_off + i] = sc[P.scr_R + i];
+        if (o.bvals)
+          for (int i = tid; i < B.nrows * 3; i += T)
+            o.bvals[(mu * P.total_rows + B.row_off) * 3 + i] =
+                P.gbv[((size_t)(gslot0 + s) * P.total_rows + B.row_off) * 3 + i];
+        const double* e = V.eb(s, ebi[s]);
+        if (o.cval)
+          for (int i = tid; i < P.n_C; i += T) o.cval[(mu * P.nb + b) * P.n_C + i] = eb_cval(const_cast<double*>(e), B)[i];
+        if (o.cjac)
+          for (int i = tid; i < P.n_C * NG; i += T) o.cjac[mu * P.tot_cjac + B.cjac_off + i] = eb_cjac(const_cast<double*>(e), B, P.n_C)[i];
+      }
+    }
+    // ---- phase D: Gram block, projections, r^T r ----
+    {
+      const int ntri = W * (W + 1) / 2, nt = ntri + W + 1;
+      for (int t = warp; t < G * nt; t += nw) {
+        const int s = t / nt;
+        int q = t - s * nt;
+        if (!((mask >> s) & 1u)) continue;
+        const double* sc = V.scr(s);
+        const double* R = sc + P.scr_R;
+        const double* rv = sc + P.scr_r;
+        int i = 0, j = 0, kind = 0;
+        if (q < ntri) {
+          while (q >= W - i) { q -= W - i; ++i; }
+          j = i + q;
+        } else if (q < ntri + W) {
+          kind = 1; i = q - ntri;
+        } else {
+          kind = 2;
+        }
+        double acc = 0.0;
+        for (int r = lane; r < B.nrows; r += WARP) {
+          const double a = kind == 2 ? rv[r] : R[(size_t)r * W + i];
+          const double bb = kind == 0 ? R[(size_t)r * W + j] : rv[r];
+          acc = fma(a, bb, acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          double* e = V.eb(s, ebi[s]);
+          if (kind == 0) {
+            eb_H(e, B)[i * W + j] = acc;
+            eb_H(e, B)[j * W + i] = acc;
+          } else if (kind == 1) {
+            eb_proj(e, B)[i] = acc;
+          } else {
+            *eb_rr(e, B, P.n_C) = acc;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// phase E for one slot (one warp): rho with multipliers lt, con, merit, obj.
+template <int NI, int NG>
+__device__ void finalize_eval(const View& V, int s, double* e, const double* lt) {
+  const Params& P = V.P;
+  const int lane = threadIdx.x & 31;
+  constexpr int W = NI + NG;
+  double* rho = e + P.eb_rho;
+  double* con = e + P.eb_con;
+  double ss = 0.0;
+  for (int i = lane; i < P.n_D; i += WARP) {
+    const int b = i / W, li = i - b * W;
+    const BlockDev& B = P.blk[b];
+    double v = eb_proj(e, B)[li];
+    if (li >= NI) {
+      const int d = li - NI;
+      const double* cj = eb_cjac(e, B, P.n_C);
+      double t = 0.0;
+      for (int c = 0; c < P.n_C; ++c) t = fma(cj[c * NG + d], lt[c], t);
+      v = v + t;
+    }
+    rho[i] = v;
+    ss = fma(v, v, ss);
+  }
+  for (int c = lane; c < P.n_C; c += WARP) {
+    double v = 0.0;
+    for (int b = 0; b < P.nb; ++b) v = v + eb_cval(e, P.blk[b])[c];
+    con[c] = v;
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) {
+    double obj = 0.0;
+    for (int b = 0; b < P.nb; ++b) obj = obj + *eb_rr(e, P.blk[b], P.n_C);
+    e[P.eb_scal] = sqrt(ss);
+    e[P.eb_scal + 1] = 0.5 * obj;
+  }
+  __syncwarp();
+}
+
+// --------------------------------------------------------------------------
+// warp-level dense LU with partial pivoting (LAPACK dgetf2 semantics:
+// idamax pivot = first max, scale by reciprocal when |pivot| >= sfmin).
+// K row-major with leading dimension ld.  Returns 0 or k+1 for a zero pivot.
+__device__ int warp_lu(double* K, int ld, int n, int* piv) {
+  const int lane = threadIdx.x & 31;
+  int info = 0;
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + lane; i < n; i += WARP) {
+      const double a = fabs(K[i * ld + k]);
+      if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) piv[k] = bi;
+    const double pv = K[bi * ld + k];
+    if (pv != 0.0) {
+      if (bi != k)
+        for (int j = lane; j < n; j += WARP) {
+          const double t = K[k * ld + j];
+          K[k * ld + j] = K[bi * ld + j];
+          K[bi * ld + j] = t;
+        }
+      __syncwarp();
+      if (fabs(pv) >= 2.2250738585072014e-308) {
+        const double r = 1.0 / pv;
+        for (int i = k + 1 + lane; i < n; i += WARP) K[i * ld + k] *= r;
+      } else {
+        for (int i = k + 1 + lane; i < n; i += WARP) K[i * ld + k] /= pv;
+      }
+    } else if (info == 0) {
+      info = k + 1;
+    }
+    __syncwarp();
+    // rank-1 update of the trailing block, lanes over columns
+    for (int j = k + 1 + lane; j < n; j += WARP) {
+      const double ukj = K[k * ld + j];
+      for (int i = k + 1; i < n; ++i) K[i * ld + j] = fma(-K[i * ld + k], ukj, K[i * ld + j]);
+    }
+    __syncwarp();
+  }
+  return info;
+}
+
+// warp-level getrs: b <- inv(LU) P b, in place.
+__device__ void warp_lu_solve(const double* K, int ld, int n, const int* piv, double* b) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int k = 0; k < n; ++k) {
+      const int p = piv[k];
+      if (p != k) { const double t = b[k]; b[k] = b[p]; b[p] = t; }
+    }
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {      // unit lower
+    const double bk = b[k];
+    for (int i = k + 1 + lane; i < n; i += WARP) b[i] = fma(-K[i * ld + k], bk, b[i]);
+    __syncwarp();
+  }
+  for (int k = n - 1; k >= 0; --k) { // upper
+    if (lane == 0) b[k] = b[k] / K[k * ld + k];
+    __syncwarp();
+    const double bk = b[k];
+    for (int i = lane; i < k; i += WARP) b[i] = fma(-K[i * ld + k], bk, b[i]);
+    __syncwarp();
+  }
+}
+
+// y = K x from the compact eval buffer (blockdiag H + delta I, E, E^T)
+template <int NI, int NG>
+__device__ void kkt_matvec(const Params& P, const double* e, double delta, const double* x,
+                           double* y) {
+  const int lane = threadIdx.x & 31;
+  constexpr int W = NI + NG;
+  for (int i = lane; i < P.nK; i += WARP) {
+    double v = 0.0;
+    if (i < P.n_D) {
+      const int b = i / W, li = i - b * W;
+      const BlockDev& B = P.blk[b];
+      const double* H = eb_H(const_cast<double*>(e), B) + li * W;
+      const double* xb = x + b * W;
+      for (int j = 0; j < W; ++j) v = fma(H[j], xb[j], v);
+      if (delta != 0.0) v = fma(delta, x[i], v);
+      if (li >= NI) {
+        const double* cj = eb_cjac(const_cast<double*>(e), B, P.n_C);
+        for (int c = 0; c < P.n_C; ++c) v = fma(cj[c * NG + (li - NI)], x[P.n_D + c], v);
+      }
+    } else {
+      const int c = i - P.n_D;
+      for (int b = 0; b < P.nb; ++b) {
+        const BlockDev& B = P.blk[b];
+        const double* cj = eb_cjac(const_cast<double*>(e), B, P.n_C) + c * NG;
+        const double* xb = x + b * W + NI;
+        for (int d = 0; d < NG; ++d) v = fma(cj[d], xb[d], v);
+      }
+    }
+    y[i] = v;
+  }
+  __syncwarp();
+}
+
+// assemble_and_solve_kkt (sqp.py:162-208) for one slot, one warp.
+// Returns 0 ok, 1 ok after regularization, 2 singular (ConvergenceError).
+// Solution (s, s_lam) written to sol[nK].
+template <int NI, int NG>
+__device__ int warp_kkt(const Params& P, const double* e, double* work, double* sol) {
+  const int lane = threadIdx.x & 31;
+  constexpr int W = NI + NG;
+  const int n = P.nK, ld = n + 1;
+  double* K = work;
+  int* piv = reinterpret_cast<int*>(work + (size_t)n * ld);
+  double* rhs = work + (size_t)n * ld + n;
+  double* res = rhs + n;
+  double* tmp = res + n;
+  const double* rho = e + P.eb_rho;
+  const double* con = e + P.eb_con;
+  double ss = 0.0;
+  for (int i = lane; i < n; i += WARP) {
+    const double v = -(i < P.n_D ? rho[i] : con[i - P.n_D]);
+    rhs[i] = v;
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  const double rhs_norm = fmax(sqrt(ss), 1e-300);
+  double delta = 0.0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt == 1) {
+      // delta = reg_scale * max(trace(K[:n,:n]), 1)
+      double tr = 0.0;
+      if (lane == 0) {
+        for (int b = 0; b < P.nb; ++b)
+          for (int i = 0; i < W; ++i) tr = tr + eb_H(const_cast<double*>(e), P.blk[b])[i * W + i];
+      }
+      tr = __shfl_sync(0xffffffffu, tr, 0);
+      delta = P.cfg.reg_scale * fmax(tr, 1.0);
+    }
+    // assemble dense K (sqp.py:149-159)
+    for (int idx = lane; idx < n * n; idx += WARP) {
+      const int i = idx / n, j = idx - i * n;
+      double v = 0.0;
+      if (i < P.n_D && j < P.n_D) {
+        const int bi = i / W, bj = j / W;
+        if (bi == bj) v = eb_H(const_cast<double*>(e), P.blk[bi])[(i - bi * W) * W + (j - bj * W)];
+        if (i == j) v += delta;
+      } else if (i < P.n_D && j >= P.n_D) {
+        const int b = i / W, li = i - b * W;
+        if (li >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(j - P.n_D) * NG + (li - NI)];
+      } else if (i >= P.n_D && j < P.n_D) {
+        const int b = j / W, lj = j - b * W;
+        if (lj >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(i - P.n_D) * NG + (lj - NI)];
+      }
+      K[i * ld + j] = v;
+    }
+    __syncwarp();
+    warp_lu(K, ld, n, piv);
+    for (int i = lane; i < n; i += WARP) sol[i] = rhs[i];
+    __syncwarp();
+    warp_lu_solve(K, ld, n, piv, sol);
+    bool finite = true;
+    for (int i = lane; i < n; i += WARP) finite = finite && isfinite(sol[i]);
+    finite = __all_sync(0xffffffffu, finite);
+    double rel = INFINITY;
+    if (finite) {
+      // one round of iterative refinement
+      kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
+      for (int i = lane; i < n; i += WARP) res[i] = rhs[i] - tmp[i];
+      __syncwarp();
+      warp_lu_solve(K, ld, n, piv, res);
+      for (int i = lane; i < n; i += WARP) sol[i] += res[i];
+      __syncwarp();
+      finite = true;
+      for (int i = lane; i < n; i += WARP) finite = finite && isfinite(sol[i]);
+      finite = __all_sync(0xffffffffu, finite);
+      if (finite) {
+        kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
+        double r2 = 0.0;
+        for (int i = lane; i < n; i += WARP) {
+          const double d = rhs[i] - tmp[i];
+          r2 = fma(d, d, r2);
+        }
+        r2 = warp_sum(r2);
+        rel = sqrt(r2) / rhs_norm;
+      }
+    }
+    if (rel <= 1e-10) return attempt;
+  }
+  return 2;
+}
+
+// multiplier_least_squares (driver.py:461-471) for one slot, one warp:
+// argmin || A lam - rhs ||, A = vstack(cjac_b^T) [sum ng x n_C],
+// rhs = -rho_Gamma(lam = 0).  Householder QR (full column rank; a rank-
+// deficient A makes K singular, reported as ST_LSTSQ_RANK).
+template <int NI, int NG>
+__device__ bool warp_lstsq(const Params& P, const double* e, double* work, double* lam) {
+  const int lane = threadIdx.x & 31;
+  constexpr int W = NI + NG;
+  const int m = P.nb * NG, n = P.n_C;
+  double* A = work;               // column-major [n][m]
+  double* bvec = work + (size_t)m * n;
+  const double* rho = e + P.eb_rho;
+  for (int idx = lane; idx < m * n; idx += WARP) {
+    const int c = idx / m, r = idx - c * m;
+    const int b = r / NG, d = r - b * NG;
+    A[idx] = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[c * NG + d];
+  }
+  for (int r = lane; r < m; r += WARP) {
+    const int b = r / NG, d = r - b * NG;
+    bvec[r] = -rho[b * W + NI + d];
+  }
+  __syncwarp();
+  if (m < n) return false;
+  double rmax = 0.0;
+  bool ok = true;
+  for (int k = 0; k < n; ++k) {
+    double* a = A + (size_t)k * m;
+    double s2 = 0.0;
+    for (int i = k + lane; i < m; i += WARP) s2 = fma(a[i], a[i], s2);
+    s2 = warp_sum(s2);
+    const double nrm = sqrt(s2);
+    const double akk = a[k];
+    const double alpha = akk >= 0.0 ? -nrm : nrm;
+    const double v0 = akk - alpha;
+    const double vn2 = s2 - akk * akk + v0 * v0;
+    __syncwarp();
+    if (nrm == 0.0 || vn2 == 0.0) { ok = false; break; }
+    // apply H = I - 2 v v^T / (v^T v) to trailing columns and rhs, v = [v0, a[k+1:]]
+    for (int j = k + 1; j <= n; ++j) {
+      double* c = j < n ? A + (size_t)j * m : bvec;
+      double t = 0.0;
+      for (int i = k + lane; i < m; i += WARP) t = fma(i == k ? v0 : a[i], c[i], t);
+      t = warp_sum(t);
+      const double f = 2.0 * t / vn2;
+      __syncwarp();
+      for (int i = k + lane; i < m; i += WARP) c[i] = fma(-f, i == k ? v0 : a[i], c[i]);
+      __syncwarp();
+    }
+    if (lane == 0) a[k] = alpha;
+    __syncwarp();
+    rmax = fmax(rmax, fabs(alpha));
+  }
+  if (ok) {
+    const double tol = 2.220446049250313e-16 * (double)(m > n ? m : n) * rmax;
+    for (int k = 0; k < n; ++k) ok = ok && fabs(A[(size_t)k * m + k]) > tol;
+  }
+  if (!ok) return false;
+  if (lane == 0) {
+    for (int k = n - 1; k >= 0; --k) {
+      double v = bvec[k];
+      for (int j = k + 1; j < n; ++j) v = fma(-A[(size_t)j * m + k], lam[j], v);
+      lam[k] = v / A[(size_t)k * m + k];
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+// RBF initializer (driver.py:82-90, thin plate spline + linear tail)
+__device__ void warp_rbf(const Params& P, double a, double lm, double* x0, double* work) {
+  const int lane = threadIdx.x & 31;
+  const double q0 = a, q1 = lm;
+  const double sp0 = P.rbf_hi[0] > P.rbf_lo[0] ? P.rbf_hi[0] - P.rbf_lo[0] : 1.0;
+  const double sp1 = P.rbf_hi[1] > P.rbf_lo[1] ? P.rbf_hi[1] - P.rbf_lo[1] : 1.0;
+  const double n0 = (q0 - P.rbf_lo[0]) / sp0, n1 = (q1 - P.rbf_lo[1]) / sp1;
+  const int nv = P.rbf_P + P.rbf_R;
+  for (int i = lane; i < nv; i += WARP) {
+    double v;
+    if (i < P.rbf_P) {
+      const double d0 = n0 * P.rbf_eps - __ldg(P.rbf_y + 2 * i) * P.rbf_eps;
+      const double d1 = n1 * P.rbf_eps - __ldg(P.rbf_y + 2 * i + 1) * P.rbf_eps;
+      const double r = sqrt(d0 * d0 + d1 * d1);
+      v = r == 0.0 ? 0.0 : r * r * log(r);
+    } else {
+      const int k = i - P.rbf_P;
+      const double h0 = (n0 - P.rbf_shift[0]) / P.rbf_scale[0];
+      const double h1 = (n1 - P.rbf_shift[1]) / P.rbf_scale[1];
+      const int p0 = P.rbf_pow[2 * k], p1 = P.rbf_pow[2 * k + 1];
+      double f0 = 1.0, f1 = 1.0;
+      for (int t = 0; t < p0; ++t) f0 *= h0;
+      for (int t = 0; t < p1; ++t) f1 *= h1;
+      v = f0 * f1;
+    }
+    work[i] = v;
+  }
+  __syncwarp();
+  for (int j = lane; j < P.n_D; j += WARP) {
+    double acc = 0.0;
+    for (int i = 0; i < nv; ++i) acc = fma(work[i], __ldg(P.rbf_coeffs + (size_t)i * P.n_D + j), acc);
+    x0[j] = acc;
+  }
+  __syncwarp();
+}
+
+// boundary values (bx, by, c) of assemble() at every sampled row
+// (burgers.py:188-210): ghost points just outside the edges the node touches.
+__device__ void row_bvals(const Params& P, const StRow& rw, double a, double lm, double* out) {
+  const double hx = P.hx, hy = P.hy, nu = P.nu;
+  const bool isv = (rw.bflags >> 4) & 1;
+  double exl = 0.0, exr = 0.0, eyb = 0.0, eyt = 0.0, u, v;
+  if (rw.bflags & 1) { exact_uv(a, lm, -1.0, rw.yc, nu, u, v); exl = isv ? v : u; }
+  if (rw.bflags & 2) { exact_uv(a, lm, 1.0, rw.yc, nu, u, v); exr = isv ? v : u; }
+  if (rw.bflags & 4) { exact_uv(a, lm, rw.xc, 0.0, nu, u, v); eyb = isv ? v : u; }
+  if (rw.bflags & 8) { exact_uv(a, lm, rw.xc, 0.05, nu, u, v); eyt = isv ? v : u; }
+  out[0] = (-1.0 / (2.0 * hx)) * (exl - exr);
+  out[1] = (-1.0 / (2.0 * hy)) * (eyb - eyt);
+  out[2] = (nu / (hx * hx)) * (exl + exr) + (nu / (hy * hy)) * (eyb + eyt);
+}
+
+// --------------------------------------------------------------------------
+// the persistent kernel
+
+template <int G, int NI, int NG>
+__global__ void __launch_bounds__(256) k_solve(const __grid_constant__ Params P) {
+  extern __shared__ __align__(16) double smem[];
+  View V(P, smem);
+  SlotState* st = V.st();
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int W = NI + NG;
+  const int gslot0 = blockIdx.x * G;
+  __shared__ int s_cur[G];
+  __shared__ int s_ebi[G];
+  __shared__ unsigned s_mask;
+  __shared__ unsigned s_newmask;
+  __shared__ unsigned long long s_evals, s_kkts;
+  if (tid < G) { st[tid].mu = -1; st[tid].phase = PH_DONE; s_cur[tid] = 0; }
+  if (tid == 0) { s_evals = 0; s_kkts = 0; }
+  __syncthreads();
+  const SqpCfg& cfg = P.cfg;
+  for (;;) {
+    // ---- retire finished slots, fetch new mu ----
+    if (tid == 0) {
+      unsigned nm = 0;
+      for (int s = 0; s < G; ++s) {
+        if (st[s].phase == PH_DONE) {
+          const int mu = atomicAdd(P.work, 1);
+          if (mu < P.B) {
+            st[s].mu = mu; st[s].phase = PH_INIT; st[s].n_iter = 0; st[s].n_trials = 0;
+            st[s].n_evals = 0; st[s].n_reg = 0; st[s].status = ST_OK; st[s].need_kkt = 0;
+            st[s].alpha = 1.0;
+            nm |= 1u << s;
+          } else {
+            st[s].mu = -1; st[s].phase = PH_IDLE;
+          }
+        }
+      }
+      unsigned m = 0;
+      for (int s = 0; s < G; ++s) if (st[s].phase == PH_INIT || st[s].phase == PH_TRIAL) m |= 1u << s;
+      s_mask = m;
+      s_newmask = nm;
+    }
+    __syncthreads();
+    const unsigned mask = s_mask, newmask = s_newmask;
+    if (mask == 0) break;
+    // ---- initialise new slots: boundary values (CTA-wide), x0 / lam0 (warp per slot) ----
+    if (newmask) {
+      for (int s = 0; s < G; ++s) {
+        if (!((newmask >> s) & 1u)) continue;
+        const int mu = st[s].mu;
+        const double a = P.mu[2 * mu], lm = P.mu[2 * mu + 1];
+        double* gb = P.gbv + (size_t)(gslot0 + s) * P.total_rows * 3;
+        for (int b = 0; b < P.nb; ++b) {
+          const BlockDev& B = P.blk[b];
+          for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows[r], a, lm, gb + (B.row_off + r) * 3);
+        }
+      }
+      if (warp < G && ((newmask >> warp) & 1u)) {
+        const int s = warp, mu = st[s].mu;
+        double* xt = V.vec(s, 4);
+        double* lt = V.vec(s, 5);
+        if (P.x0_in) {
+          for (int j = lane; j < P.n_D; j += WARP) xt[j] = P.x0_in[(size_t)mu * P.n_D + j];
+        } else {
+          warp_rbf(P, P.mu[2 * mu], P.mu[2 * mu + 1], xt, V.scr(s));
+        }
+        for (int c = lane; c < P.n_C; c += WARP) lt[c] = P.lam0_in ? P.lam0_in[(size_t)mu * P.n_C + c] : 0.0;
+        if (lane == 0) st[s].lam_given = P.lam0_in != nullptr;
+        __syncwarp();
+        if (P.so.x0) for (int j = lane; j < P.n_D; j += WARP) P.so.x0[(size_t)mu * P.n_D + j] = xt[j];
+      }
+      __syncthreads();
+    }
+    // ---- one eval_gradients per active slot ----
+    if (tid < G) s_ebi[tid] = st[tid].phase == PH_INIT ? s_cur[tid] : 1 - s_cur[tid];
+    __syncthreads();
+    eval_blocks<G, NI, NG>(V, mask, s_ebi, gslot0, false);
+    if (tid == 0) s_evals += (unsigned long long)__popc(mask) * P.nb;
+    // ---- per-slot state machine (warp s) ----
+    if (warp < G && ((mask >> warp) & 1u)) {
+      const int s = warp;
+      SlotState& S = st[s];
+      const int mu = S.mu;
+      double* e = V.eb(s, s_ebi[s]);
+      double* lt = V.vec(s, 5);
+      double* x = V.vec(s, 0);
+      double* lam = V.vec(s, 1);
+      double* xt = V.vec(s, 4);
+      finalize_eval<NI, NG>(V, s, e, lt);
+      bool check = false;
+      if (S.phase == PH_INIT) {
+        if (!S.lam_given) {
+          // multiplier least squares at lam = 0, then rho at lam0
+          const bool ok = warp_lstsq<NI, NG>(P, e, V.scr(s), lt);
+          if (!ok) {
+            if (lane == 0) { S.status = ST_LSTSQ_RANK; }
+          }
+          __syncwarp();
+          finalize_eval<NI, NG>(V, s, e, lt);
+        }
+        if (P.so.lam0) for (int c = lane; c < P.n_C; c += WARP) P.so.lam0[(size_t)mu * P.n_C + c] = lt[c];
+        for (int j = lane; j < P.n_D; j += WARP) { x[j] = xt[j]; V.vec(s, 6)[j] = xt[j]; }
+        for (int c = lane; c < P.n_C; c += WARP) { lam[c] = lt[c]; V.vec(s, 7)[c] = lt[c]; }
+        if (lane == 0) {
+          S.merit = e[P.eb_scal]; S.obj = e[P.eb_scal + 1]; S.best_merit = S.merit;
+          S.n_evals = 1;
+          if (P.so.merit_hist) P.so.merit_hist[(size_t)mu * (cfg.max_iter + 1)] = S.merit;
+          if (P.so.obj_hist) P.so.obj_hist[(size_t)mu * (cfg.max_iter + 1)] = S.obj;
+        }
+        check = true;
+      } else {  // PH_TRIAL
+        const double tm = e[P.eb_scal];
+        const double rhs = (1.0 - cfg.c1 * S.alpha) * S.merit;
+        if (lane == 0) S.n_evals += 1;
+        if (tm <= rhs) {
+          for (int j = lane; j < P.n_D; j += WARP) x[j] = xt[j];
+          for (int c = lane; c < P.n_C; c += WARP) lam[c] = lt[c];
+          __syncwarp();
+          if (lane == 0) {
+            s_cur[s] = s_ebi[s];
+            if (P.so.alpha_hist) P.so.alpha_hist[(size_t)mu * cfg.max_iter + S.n_iter] = S.alpha;
+            S.n_iter += 1;
+            S.merit = tm; S.obj = e[P.eb_scal + 1];
+            if (P.so.merit_hist) P.so.merit_hist[(size_t)mu * (cfg.max_iter + 1) + S.n_iter] = S.merit;
+            if (P.so.obj_hist) P.so.obj_hist[(size_t)mu * (cfg.max_iter + 1) + S.n_iter] = S.obj;
+          }
+          const bool better = tm < S.best_merit;
+          __syncwarp();
+          if (better) {
+            for (int j = lane; j < P.n_D; j += WARP) V.vec(s, 6)[j] = x[j];
+            for (int c = lane; c < P.n_C; c += WARP) V.vec(s, 7)[c] = lam[c];
+            if (lane == 0) S.best_merit = tm;
+          }
+          check = true;
+        } else {
+          const int tr = S.n_trials + 1;
+          __syncwarp();
+          if (tr >= cfg.max_halvings + 1) {
+            // line-search failure: return the best iterate (sqp.py:275-293)
+            for (int j = lane; j < P.n_D; j += WARP) x[j] = V.vec(s, 6)[j];
+            for (int c = lane; c < P.n_C; c += WARP) lam[c] = V.vec(s, 7)[c];
+            if (lane == 0) { S.status = ST_LINE_SEARCH; S.phase = PH_DONE; S.n_trials = tr; }
+          } else {
+            const double al = S.alpha * cfg.factor;
+            const double* sv = V.vec(s, 2);
+            const double* sl = V.vec(s, 3);
+            for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], __dmul_rn(al, sv[j]));
+            for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], __dmul_rn(al, sl[c]));
+            if (lane == 0) { S.alpha = al; S.n_trials = tr; }
+          }
+        }
+      }
+      __syncwarp();
+      if (check) {
+        if (S.status == ST_LSTSQ_RANK) {
+          if (lane == 0) S.phase = PH_DONE;
+        } else if (!(S.merit >= cfg.tol && S.n_iter < cfg.max_iter)) {
+          if (lane == 0) S.phase = PH_DONE;
+        } else {
+          if (lane == 0) S.need_kkt = 1;
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- KKT solves (warp per slot) ----
+    if (warp < G && st[warp].need_kkt) {
+      const int s = warp;
+      SlotState& S = st[s];
+      double* e = V.eb(s, s_cur[s]);
+      double* work = V.scr(s);
+      double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
+      const int r = warp_kkt<NI, NG>(P, e, work, sol);
+      if (lane == 0) { S.need_kkt = 0; atomicAdd(&s_kkts, 1ull); }
+      if (r == 2) {
+        if (lane == 0) { S.status = ST_KKT_SINGULAR; S.phase = PH_DONE; }
+      } else {
+        if (lane == 0) S.n_reg += r;
+        double* sv = V.vec(s, 2);
+        double* sl = V.vec(s, 3);
+        const double* x = V.vec(s, 0);
+        const double* lam = V.vec(s, 1);
+        for (int j = lane; j < P.n_D; j += WARP) sv[j] = sol[j];
+        for (int c = lane; c < P.n_C; c += WARP) sl[c] = sol[P.n_D + c];
+        __syncwarp();
+        double* xt = V.vec(s, 4);
+        double* lt = V.vec(s, 5);
+        for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], sv[j]);
+        for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], sl[c]);
+        if (lane == 0) { S.alpha = 1.0; S.n_trials = 0; S.phase = PH_TRIAL; }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- write results of finished slots ----
+    if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) {
+      const int s = warp;
+      SlotState& S = st[s];
+      const int mu = S.mu;
+      const double* x = V.vec(s, 0);
+      const double* lam = V.vec(s, 1);
+      for (int j = lane; j < P.n_D; j += WARP) P.so.x[(size_t)mu * P.n_D + j] = x[j];
+      for (int c = lane; c < P.n_C; c += WARP) P.so.lam[(size_t)mu * P.n_C + c] = lam[c];
+      if (lane == 0) {
+        if (P.so.n_iter) P.so.n_iter[mu] = S.n_iter;
+        if (P.so.n_evals) P.so.n_evals[mu] = S.n_evals;
+        if (P.so.status) P.so.status[mu] = S.status;
+        if (P.so.n_reg) P.so.n_reg[mu] = S.n_reg;
+        if (P.so.merit) P.so.merit[mu] = S.merit;
+        if (P.so.objective) P.so.objective[mu] = S.obj;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    atomicAdd(P.counters, s_evals);
+    atomicAdd(P.counters + 1, s_kkts);
+  }
+}
+
+}  // namespace ddnm
+
+namespace ddnm {
+
+// ddnm_eval_batch: one eval_gradients per mu at a given (x, lam), dumping every
+// intermediate, plus (optionally) the KKT step at that point.  mu = CTA*G + s.
+template <int G, int NI, int NG>
+__global__ void __launch_bounds__(256) k_eval(const __grid_constant__ Params P) {
+  extern __shared__ __align__(16) double smem[];
+  View V(P, smem);
+  SlotState* st = V.st();
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int gslot0 = blockIdx.x * G;
+  __shared__ int s_ebi[G];
+  __shared__ unsigned s_mask;
+  if (tid == 0) {
+    unsigned m = 0;
+    for (int s = 0; s < G; ++s) {
+      const int mu = gslot0 + s;
+      st[s].mu = mu < P.B ? mu : -1;
+      if (mu < P.B) m |= 1u << s;
+      s_ebi[s] = 0;
+    }
+    s_mask = m;
+  }
+  __syncthreads();
+  const unsigned mask = s_mask;
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    const int mu = st[s].mu;
+    const double a = P.mu[2 * mu], lm = P.mu[2 * mu + 1];
+    double* gb = P.gbv + (size_t)(gslot0 + s) * P.total_rows * 3;
+    for (int b = 0; b < P.nb; ++b) {
+      const BlockDev& B = P.blk[b];
+      for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows[r], a, lm, gb + (B.row_off + r) * 3);
+    }
+    for (int j = tid; j < P.n_D; j += T) V.vec(s, 4)[j] = P.x0_in[(size_t)mu * P.n_D + j];
+    for (int c = tid; c < P.n_C; c += T) V.vec(s, 5)[c] = P.lam0_in[(size_t)mu * P.n_C + c];
+  }
+  __syncthreads();
+  eval_blocks<G, NI, NG>(V, mask, s_ebi, gslot0, true);
+  if (warp < G && ((mask >> warp) & 1u)) {
+    const int s = warp;
+    const size_t mu = (size_t)st[s].mu;
+    double* e = V.eb(s, 0);
+    finalize_eval<NI, NG>(V, s, e, V.vec(s, 5));
+    const EvalOut& o = P.eo;
+    if (o.rho) for (int j = lane; j < P.n_D; j += WARP) o.rho[mu * P.n_D + j] = e[P.eb_rho + j];
+    if (o.con) for (int c = lane; c < P.n_C; c += WARP) o.con[mu * P.n_C + c] = e[P.eb_con + c];
+    if (lane == 0) {
+      if (o.merit) o.merit[mu] = e[P.eb_scal];
+      if (o.objective) o.objective[mu] = e[P.eb_scal + 1];
+    }
+    if (P.eval_step) {
+      double* work = V.scr(s);
+      double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
+      const int r = warp_kkt<NI, NG>(P, e, work, sol);
+      if (o.step) for (int j = lane; j < P.nK; j += WARP) o.step[mu * P.nK + j] = sol[j];
+      if (lane == 0 && o.kkt_status) o.kkt_status[mu] = r;
+    }
+  }
+}
+
+__global__ void k_fill(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+}  // namespace ddnm

@@ -1,0 +1,440 @@
+"""Online ROM driver: instances, batched solves and per-block evaluation.
+
+Mirrors the online half of ``ddrom.driver`` (driver.py:93-152, 356-597):
+
+* :class:`RomInstance` -- the artifacts ``build_problem`` consumes
+  (driver.py:356-436), loaded from a reference-free ``.npz`` and uploaded
+  once per GPU into a ``libddnm`` context;
+* :func:`solve_rom_batch` -- ``solve_rom`` (driver.py:554-597,
+  ``compute_error=False``) for a whole batch of parameters on the device;
+* :func:`solve_rom` / :func:`init_guess` / :func:`build_problem` -- the
+  reference's single-parameter entry points, on top of the batched kernel;
+* :func:`eval_gradients_batch` -- ``eval_gradients`` (sqp.py:117-146) with
+  every intermediate of the HR closure (driver.py:404-432), for parity.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import threading
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .burgers import Grid2D, ParameterPoint
+from .errors import ConvergenceError
+from .sqp import SqpBlock, SqpConfig, SqpProblem, SqpResult
+
+_FAILURE = {N.STATUS_OK: None, N.STATUS_LINE_SEARCH: "line_search",
+            N.STATUS_KKT_SINGULAR: "kkt_singular", N.STATUS_LSTSQ_RANK: "lstsq_rank"}
+
+
+class RomInstance:
+    """Everything the online solve of one DD ROM configuration needs.
+
+    Built from the artifact dictionary written by ``tools/make_golden.py``
+    (the reference's ``RomInstance`` after ``attach_hr`` and
+    ``fit_initializer``, restricted to what ``build_problem`` reads)."""
+
+    def __init__(self, arrays: dict):
+        self.arrays = {k: np.asarray(v) for k, v in arrays.items()}
+        self.meta = json.loads(str(self.arrays["meta_json"]))
+        m = self.meta
+        self.kind = m["kind"]
+        self.grid = Grid2D(m["nx"], m["ny"], m["nu"])
+        self.n_blocks = m["nblocks"]
+        self.latent_layout = [(int(a), int(b)) for a, b in zip(m["n_int"], m["n_gam"])]
+        self.n_mult = int(m["n_c"])
+        self.n_primal = sum(a + b for a, b in self.latent_layout)
+        self.provenance = dict(m.get("provenance", {}))
+        self._ctx = {}
+        self._lock = threading.Lock()
+        self._keep = []
+
+    @classmethod
+    def load(cls, path: str) -> "RomInstance":
+        with np.load(path, allow_pickle=False) as z:
+            return cls(dict(z))
+
+    def split_latent(self, x):
+        out, off = [], 0
+        for ni, ng in self.latent_layout:
+            out.append((x[off:off + ni], x[off + ni:off + ni + ng]))
+            off += ni + ng
+        return out
+
+    # -- native context ----------------------------------------------------
+
+    def _artifacts_struct(self):
+        a = self.arrays
+        m = self.meta
+        keep = []
+
+        def arr(x, kind="f"):
+            x = N.f64(x) if kind == "f" else N.i64(x)
+            keep.append(x)
+            return N.ptr(x, C.c_double if kind == "f" else C.c_int64)
+
+        blocks = (N.Block * self.n_blocks)()
+        ae = self.kind == "nm"
+        for b in range(self.n_blocks):
+            p = f"b{b}_"
+            blk = blocks[b]
+            blk.n_int, blk.n_gam = self.latent_layout[b]
+            io, gio = a[p + "io"], a[p + "gio"]
+            for dec, pre in ((blk.interior, "int_"), (blk.interface, "gam_")):
+                if ae:
+                    dec.n_out = a[p + pre + "scale"].size
+                    dec.n_hidden = a[p + pre + "b1"].size
+                    dec.W1 = arr(a[p + pre + "W1"])
+                    dec.b1 = arr(a[p + pre + "b1"])
+                    dec.indptr = arr(a[p + pre + "W2_indptr"], "i")
+                    dec.indices = arr(a[p + pre + "W2_indices"], "i")
+                    dec.data = arr(a[p + pre + "W2_data"])
+                    dec.scale = arr(a[p + pre + "scale"])
+                    dec.shift = arr(a[p + pre + "shift"])
+                else:
+                    Phi = a[p + pre + "Phi"]
+                    dec.n_out = Phi.shape[0]
+                    dec.n_hidden = 0
+                    dec.W1 = arr(Phi)
+            blk.n_rows = a[p + "res_rows"].size
+            blk.res_rows = arr(a[p + "res_rows"], "i")
+            blk.n_cols = a[p + "cols"].size
+            blk.cols = arr(a[p + "cols"], "i")
+            blk.n_io = io.size
+            blk.n_gio = gio.size
+            blk.gio = arr(gio, "i")
+            blk.CA = arr(a[p + "CA"])
+        art = N.Artifacts()
+        art.abi_version = N.ABI_VERSION
+        art.map_kind = N.MAP_AUTOENCODER if ae else N.MAP_LINEAR
+        act = m.get("activation", "swish")
+        art.activation = N.ACT_SIGMOID if act == "sigmoid" else N.ACT_SWISH
+        art.nx, art.ny, art.nu = m["nx"], m["ny"], m["nu"]
+        art.n_blocks = self.n_blocks
+        art.n_c = self.n_mult
+        art.blocks = blocks
+        if "rbf_coeffs" in a:
+            if m.get("rbf_kernel", "thin_plate_spline") != "thin_plate_spline":
+                raise NotImplementedError("only thin-plate-spline RBF initializers")
+            art.rbf.n_centers = a["rbf_y"].shape[0]
+            art.rbf.n_mono = a["rbf_powers"].shape[0]
+            art.rbf.y = arr(a["rbf_y"])
+            art.rbf.coeffs = arr(a["rbf_coeffs"])
+            art.rbf.powers = arr(a["rbf_powers"], "i")
+            for k in range(2):
+                art.rbf.shift[k] = float(a["rbf_shift"][k])
+                art.rbf.scale[k] = float(a["rbf_scale"][k])
+                art.rbf.lo[k] = float(a["rbf_lo"][k])
+                art.rbf.hi[k] = float(a["rbf_hi"][k])
+            art.rbf.epsilon = float(m.get("rbf_epsilon", 1.0))
+        keep.append(blocks)
+        return art, keep
+
+    def context(self, device: int = -1, slots: int = 0):
+        """The libddnm context of this instance on ``device`` (created once)."""
+        key = (device, slots)
+        with self._lock:
+            if key not in self._ctx:
+                L = N.lib()
+                art, keep = self._artifacts_struct()
+                h = C.c_void_p()
+                N.check(L.ddnm_ctx_create(device, C.byref(art), slots, C.byref(h)))
+                self._ctx[key] = _Context(h, self)
+            return self._ctx[key]
+
+    def close(self):
+        with self._lock:
+            for c in self._ctx.values():
+                c.close()
+            self._ctx.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Context:
+    def __init__(self, handle, inst):
+        self.h = handle
+        self.info = N.Info()
+        N.check(N.lib().ddnm_ctx_info(self.h, C.byref(self.info)))
+
+    def close(self):
+        if self.h:
+            N.lib().ddnm_ctx_destroy(self.h)
+            self.h = None
+
+    def counters(self):
+        e, k = C.c_int64(), C.c_int64()
+        N.check(N.lib().ddnm_last_counters(self.h, C.byref(e), C.byref(k)))
+        return e.value, k.value
+
+
+def _cfg_struct(cfg: SqpConfig):
+    c = N.SqpCfg()
+    c.tol, c.max_iter, c.armijo_c1 = cfg.tol, cfg.max_iter, cfg.armijo_c1
+    c.backtrack_factor, c.max_halvings = cfg.backtrack_factor, cfg.max_halvings
+    c.reg_scale = cfg.reg_scale
+    return c
+
+
+def _mu_array(mus) -> np.ndarray:
+    if isinstance(mus, ParameterPoint):
+        mus = [mus]
+    if isinstance(mus, (list, tuple)) and mus and isinstance(mus[0], ParameterPoint):
+        return np.array([[p.a, p.lam] for p in mus], dtype=float)
+    mu = np.ascontiguousarray(mus, dtype=float)
+    if mu.ndim != 2 or mu.shape[1] != 2:
+        raise ValueError("parameters must be an array of shape (B, 2) = (a, lambda)")
+    if not np.all(np.isfinite(mu)):
+        raise ValueError("parameters must be finite")
+    return mu
+
+
+@dataclass(eq=False)
+class BatchResult:
+    """Per-parameter outputs of :func:`solve_rom_batch` (row k = mu k)."""
+
+    mu: np.ndarray
+    x: np.ndarray
+    lam: np.ndarray
+    n_iter: np.ndarray
+    n_evals: np.ndarray
+    status: np.ndarray
+    n_reg: np.ndarray
+    merit: np.ndarray
+    objective: np.ndarray
+    merit_hist: np.ndarray
+    obj_hist: np.ndarray
+    alpha_hist: np.ndarray
+    x0: np.ndarray
+    lam0: np.ndarray
+    seconds: float = 0.0
+    tol: float = 1e-4
+    counters: tuple = field(default=(0, 0))
+
+    @property
+    def converged(self) -> np.ndarray:
+        """sqp.py:294-295: merit below tol and no failure."""
+        return (self.status == N.STATUS_OK) & (self.merit < self.tol)
+
+    def failure_reason(self, k):
+        return _FAILURE[int(self.status[k])]
+
+    def result(self, k: int, cfg: SqpConfig = SqpConfig()) -> SqpResult:
+        n = int(self.n_iter[k])
+        if int(self.status[k]) == N.STATUS_KKT_SINGULAR:
+            raise ConvergenceError("KKT back-substitution residual exceeds 1e-10 after "
+                                   "regularization (device solve)")
+        if int(self.status[k]) == N.STATUS_LSTSQ_RANK:
+            raise ConvergenceError("multiplier least squares is rank deficient: the KKT "
+                                   "matrix is singular")
+        return SqpResult(
+            x=self.x[k].copy(), lam=self.lam[k].copy(), converged=bool(self.converged[k]),
+            n_iter=n, merit_history=self.merit_hist[k, :n + 1].tolist(),
+            objective_history=self.obj_hist[k, :n + 1].tolist(),
+            alpha_history=self.alpha_hist[k, :n].tolist(),
+            failure_reason=self.failure_reason(k), n_evals=int(self.n_evals[k]),
+            n_regularized=int(self.n_reg[k]))
+
+
+def _solve_arrays(inst: RomInstance, mu: np.ndarray, cfg: SqpConfig, x0=None, lam0=None,
+                  device: int = -1, slots: int = 0) -> BatchResult:
+    ctx = inst.context(device, slots)
+    B = mu.shape[0]
+    nD, nC, K = inst.n_primal, inst.n_mult, cfg.max_iter
+    out = dict(
+        x=np.empty((B, nD)), lam=np.empty((B, nC)), n_iter=np.zeros(B, np.int32),
+        n_evals=np.zeros(B, np.int32), status=np.zeros(B, np.int32),
+        n_reg=np.zeros(B, np.int32), merit=np.empty(B), objective=np.empty(B),
+        merit_hist=np.empty((B, K + 1)), obj_hist=np.empty((B, K + 1)),
+        alpha_hist=np.empty((B, K)), x0=np.empty((B, nD)), lam0=np.empty((B, nC)))
+    so = N.SolveOut()
+    for k, v in out.items():
+        setattr(so, k, N.ptr(v, C.c_int32 if v.dtype == np.int32 else C.c_double))
+    if x0 is not None:
+        x0 = N.f64(x0).reshape(B, nD)
+    if lam0 is not None:
+        lam0 = N.f64(lam0).reshape(B, nC)
+    t0 = time.perf_counter()
+    N.check(N.lib().ddnm_solve_batch(ctx.h, B, N.ptr(mu), N.ptr(x0), N.ptr(lam0),
+                                     C.byref(_cfg_struct(cfg)), C.byref(so)))
+    dt = time.perf_counter() - t0
+    return BatchResult(mu=mu, seconds=dt, tol=cfg.tol, counters=ctx.counters(), **out)
+
+
+def solve_rom_batch(instance: RomInstance, mus, cfg: SqpConfig = SqpConfig(), *,
+                    x0=None, lam0=None, device: int = -1, slots: int = 0) -> BatchResult:
+    """``solve_rom`` (driver.py:554-597, compute_error=False) for every mu.
+
+    ``mus``: (B, 2) array of (a, lambda) or a list of ParameterPoint.
+    ``x0``/``lam0``: optional (B, n_D) / (B, n_C) starting points; when absent
+    the device evaluates the RBF initializer (driver.py:82-90) and the
+    least-squares multipliers (driver.py:461-471), as ``init_guess`` does."""
+    mu = _mu_array(mus)
+    span_lo = instance.arrays.get("rbf_lo")
+    if x0 is None and span_lo is not None:
+        lo, hi = instance.arrays["rbf_lo"], instance.arrays["rbf_hi"]
+        span = np.where(hi > lo, hi - lo, 1.0)
+        qn = (mu - lo) / span
+        if np.any(qn < -0.1) or np.any(qn > 1.1):
+            warnings.warn("initializing far outside the training box", RuntimeWarning,
+                          stacklevel=2)
+    return _solve_arrays(instance, mu, cfg, x0, lam0, device, slots)
+
+
+@dataclass(eq=False)
+class RomSolution:
+    """driver.py:513-519.  ``states`` (the full decode) is not produced by
+    the online kernel; see DESIGN.md (out of scope this round)."""
+
+    x_latent: np.ndarray
+    lam: np.ndarray
+    states: list = field(repr=False, default=None)
+    sqp: SqpResult = field(repr=False, default=None)
+    error: float = np.nan
+
+
+def solve_rom(instance: RomInstance, p: ParameterPoint, cfg: SqpConfig = SqpConfig(), *,
+              x0=None, lam0=None, compute_error: bool = False, label: str = ""):
+    """Solve the ROM at ``p`` (driver.py:554-597) on the GPU.
+
+    Returns ``(RomSolution, record_dict)``.  ``compute_error`` needs the FOM
+    (out of scope for the online kernel) and is rejected."""
+    if compute_error:
+        raise NotImplementedError("compute_error needs the full-order solve, which is "
+                                  "not part of the online GPU path")
+    mu = np.array([[p.a, p.lam]], dtype=float)
+    res = solve_rom_batch(instance, mu, cfg,
+                          x0=None if x0 is None else np.asarray(x0, float)[None, :],
+                          lam0=None if lam0 is None else np.asarray(lam0, float)[None, :])
+    r = res.result(0, cfg)
+    rec = {"label": label or instance.provenance.get("rom", "rom"), "a": p.a, "lam": p.lam,
+           "rom_seconds": res.seconds, "n_iter": r.n_iter, "converged": r.converged,
+           "final_merit": r.final_merit,
+           "status": "ok" if r.failure_reason is None else r.failure_reason}
+    return RomSolution(x_latent=r.x, lam=r.lam, sqp=r), rec
+
+
+def init_guess(instance: RomInstance, p: ParameterPoint):
+    """RBF latents plus least-squares multipliers (driver.py:442-458),
+    evaluated on the device."""
+    mu = np.array([[p.a, p.lam]], dtype=float)
+    res = solve_rom_batch(instance, mu, SqpConfig(max_iter=1, tol=1e300))
+    return res.x0[0].copy(), res.lam0[0].copy()
+
+
+@dataclass(eq=False)
+class EvalBatch:
+    rho: np.ndarray
+    con: np.ndarray
+    merit: np.ndarray
+    objective: np.ndarray
+    Br: np.ndarray
+    R: np.ndarray
+    cval: np.ndarray
+    cjac: np.ndarray
+    int_g: np.ndarray
+    int_J: np.ndarray
+    gam_g: np.ndarray
+    gam_J: np.ndarray
+    bvals: np.ndarray
+    step: np.ndarray
+    kkt_status: np.ndarray
+    layout: dict = field(default_factory=dict)
+
+    def block(self, k: int, b: int) -> dict:
+        """Per-block views for mu k, block b, in the reference's shapes."""
+        L = self.layout[b]
+        ni, ng = L["n_int"], L["n_gam"]
+        w = ni + ng
+        r0, r1 = L["row"]
+        R = self.R[k, L["R"][0]:L["R"][1]].reshape(r1 - r0, w)
+        return {
+            "Br": self.Br[k, r0:r1], "R_int": R[:, :ni], "R_gam": R[:, ni:],
+            "con_val": self.cval[k, b], "con_jac": self.cjac[k, L["cjac"][0]:L["cjac"][1]]
+            .reshape(-1, ng),
+            "int_g": self.int_g[k, L["iout"][0]:L["iout"][1]],
+            "int_J": self.int_J[k, L["intJ"][0]:L["intJ"][1]].reshape(-1, ni),
+            "gam_g": self.gam_g[k, L["gout"][0]:L["gout"][1]],
+            "gam_J": self.gam_J[k, L["gamJ"][0]:L["gamJ"][1]].reshape(-1, ng),
+            "bvals": self.bvals[k, r0:r1],
+        }
+
+
+def eval_gradients_batch(instance: RomInstance, mus, x, lam, *, reg_scale: float = 1e-12,
+                         step: bool = True, device: int = -1) -> EvalBatch:
+    """``eval_gradients`` (sqp.py:117-146) at (x[k], lam[k]) for every mu,
+    with all HR-closure intermediates, and optionally the KKT step
+    (sqp.py:162-208) at that point."""
+    mu = _mu_array(mus)
+    B = mu.shape[0]
+    ctx = instance.context(device)
+    inf = ctx.info
+    nD, nC = inf.n_primal, inf.n_mult
+    x = N.f64(x).reshape(B, nD)
+    lam = N.f64(lam).reshape(B, nC)
+    o = dict(rho=np.empty((B, nD)), con=np.empty((B, nC)), merit=np.empty(B),
+             objective=np.empty(B), Br=np.empty((B, inf.total_rows)),
+             R=np.empty((B, inf.total_R)), cval=np.empty((B, inf.n_blocks, nC)),
+             cjac=np.empty((B, inf.total_cjac)), int_g=np.empty((B, inf.total_int_out)),
+             int_J=np.empty((B, inf.total_int_J)), gam_g=np.empty((B, inf.total_gam_out)),
+             gam_J=np.empty((B, inf.total_gam_J)), bvals=np.empty((B, inf.total_rows, 3)),
+             step=np.empty((B, nD + nC)) if step else None,
+             kkt_status=np.zeros(B, np.int32) if step else None)
+    eo = N.EvalOut()
+    for k, v in o.items():
+        if v is not None:
+            setattr(eo, k, N.ptr(v, C.c_int32 if v.dtype == np.int32 else C.c_double))
+    N.check(N.lib().ddnm_eval_batch(ctx.h, B, N.ptr(mu), N.ptr(x), N.ptr(lam), reg_scale,
+                                    C.byref(eo)))
+    layout, offs = {}, dict(row=0, R=0, cjac=0, iout=0, intJ=0, gout=0, gamJ=0)
+    a = instance.arrays
+    for b, (ni, ng) in enumerate(instance.latent_layout):
+        p = f"b{b}_"
+        nrows = a[p + "res_rows"].size
+        nio = a[p + "io"].size
+        ngo = int(a[p + "n_interface"])
+        sizes = dict(row=nrows, R=nrows * (ni + ng), cjac=nC * ng, iout=nio,
+                     intJ=nio * ni, gout=ngo, gamJ=ngo * ng)
+        layout[b] = {"n_int": ni, "n_gam": ng}
+        for key, sz in sizes.items():
+            layout[b][key] = (offs[key], offs[key] + sz)
+            offs[key] += sz
+    return EvalBatch(layout=layout, **o)
+
+
+def build_problem(instance: RomInstance, p: ParameterPoint) -> SqpProblem:
+    """``build_problem`` (driver.py:356-436) at one parameter: blocks whose
+    residual/constraint closures evaluate on the GPU (one eval per call), so
+    the reference's own ``sqp.iterate`` can drive them."""
+    mu = np.array([[p.a, p.lam]], dtype=float)
+    offs = np.cumsum([0] + [a + b for a, b in instance.latent_layout])
+    nD, nC = instance.n_primal, instance.n_mult
+    blocks = []
+    for b, (ni, ng) in enumerate(instance.latent_layout):
+        def _eval(xi, xg, b=b, ni=ni, ng=ng):
+            x = np.zeros(nD)
+            x[offs[b]:offs[b] + ni] = xi
+            x[offs[b] + ni:offs[b] + ni + ng] = xg
+            ev = eval_gradients_batch(instance, mu, x[None], np.zeros((1, nC)), step=False)
+            return ev.block(0, b)
+
+        def residual(xi, xg, _e=_eval):
+            d = _e(np.asarray(xi, float), np.asarray(xg, float))
+            return d["Br"].copy(), d["R_int"].copy(), d["R_gam"].copy()
+
+        def constraint(xg, _e=_eval, ni=ni):
+            d = _e(np.zeros(ni), np.asarray(xg, float))
+            return d["con_val"].copy(), d["con_jac"].copy()
+
+        blocks.append(SqpBlock(ni, ng, residual, constraint))
+    return SqpProblem(blocks, nC, instance=instance, param=p)

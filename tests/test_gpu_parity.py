@@ -1,0 +1,221 @@
+"""CUDA path vs the CPU oracle (and the reference goldens), through the C ABI.
+
+Tolerances: the north star's FP64 gate is 1e-9 relative on latents and
+multipliers; per-component quantities are compared tighter (1e-12..1e-13)
+because they involve no ill-conditioned solve."""
+
+import numpy as np
+import pytest
+
+import paper_2305_15163_b200 as P
+from oracle import ddnm_oracle as O
+
+from .conftest import NAMES
+from .test_oracle_golden import merit_noise, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_eval_blocks_match_oracle(name, gpu_instances, oracle_instances, goldens):
+    """ddnm_eval_batch vs oracle eval_gradients piece by piece at (x0, lam0)."""
+    inst, oi, g = gpu_instances[name], oracle_instances[name], goldens[name]
+    B = 6
+    mu, x, lam = g["mu"][:B], g["x0"][:B], g["lam0"][:B]
+    ev = P.eval_gradients_batch(inst, mu, x, lam)
+    for k in range(B):
+        bbs = oi.boundary(*mu[k])
+        oev = O.eval_gradients(oi, bbs, x[k], lam[k])
+        assert rel(ev.rho[k], oev.rho) < 1e-11
+        assert rel(ev.con[k], oev.con) < 1e-12
+        assert abs(ev.merit[k] - oev.merit) <= 1e-11 * oev.merit
+        assert abs(ev.objective[k] - oev.objective) <= 1e-11 * oev.objective
+        for b, be in enumerate(oev.blocks):
+            d = ev.block(k, b)
+            blk = oi.blocks[b]
+            xi, xg = oi.split(x[k])[b]
+            assert rel(d["bvals"][:, 0], bbs[b][0]) < 1e-13
+            assert rel(d["bvals"][:, 1], bbs[b][1]) < 1e-13
+            assert rel(d["bvals"][:, 2], bbs[b][2]) < 1e-13
+            assert rel(d["int_g"], blk.int_map.decode(xi)) < 1e-13
+            assert rel(d["int_J"], blk.int_map.jacobian(xi)) < 1e-13
+            assert rel(d["gam_g"], blk.gam_map.decode(xg)) < 1e-13
+            assert rel(d["gam_J"], blk.gam_map.jacobian(xg)) < 1e-13
+            assert rel(d["Br"], be[0]) < 1e-10
+            assert rel(d["R_int"], be[1]) < 1e-12
+            assert rel(d["R_gam"], be[2]) < 1e-12
+            assert rel(d["con_val"], be[3]) < 1e-12
+            assert rel(d["con_jac"], be[4]) < 1e-12
+        s, sl, reg = O.solve_kkt(oi, oev)
+        assert ev.kkt_status[k] == 0
+        assert rel(ev.step[k, :oi.n_primal], s) < 1e-8
+        assert rel(ev.step[k, oi.n_primal:], sl) < 1e-8
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_eval_matches_reference_golden(name, gpu_instances, goldens):
+    inst, g = gpu_instances[name], goldens[name]
+    ev = P.eval_gradients_batch(inst, g["mu"][:3], g["x0"][:3], g["lam0"][:3])
+    for k in range(3):
+        assert rel(ev.rho[k], g[f"d{k}_rho"]) < 1e-11
+        assert rel(ev.step[k, :ev.rho.shape[1]], g[f"d{k}_step"]) < 1e-8
+        for b in range(inst.n_blocks):
+            d = ev.block(k, b)
+            q = f"d{k}_b{b}_"
+            assert rel(d["R_int"], g[q + "R_int"]) < 1e-12
+            assert rel(d["R_gam"], g[q + "R_gam"]) < 1e-12
+            assert rel(d["con_jac"], g[q + "con_jac"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_solve_batch_matches_oracle(name, gpu_instances, oracle_instances, goldens):
+    """Full batched solve (device RBF init, LS multipliers, SQP loop) vs the
+    oracle: x, lam to 1e-9; trajectory identical whenever no decision was
+    within the merit noise floor."""
+    inst, oi, g = gpu_instances[name], oracle_instances[name], goldens[name]
+    mu = g["mu"]
+    res = P.solve_rom_batch(inst, mu)
+    robust = 0
+    for k in range(mu.shape[0]):
+        r = O.solve(oi, *mu[k])
+        assert rel(res.x0[k], g["x0"][k]) < 1e-13
+        assert rel(res.lam0[k], g["lam0"][k]) < 1e-10
+        assert rel(res.x[k], r.x) < 1e-9, k
+        assert rel(res.lam[k], r.lam) < 1e-9, k
+        assert rel(res.x[k], g["x"][k]) < 1e-9, k          # and the reference itself
+        assert rel(res.lam[k], g["lam"][k]) < 1e-9, k
+        if min(r.margins) > merit_noise(r.merit_history[0]):
+            robust += 1
+            assert res.n_iter[k] == r.n_iter == g["n_iter"][k]
+            n = r.n_iter
+            np.testing.assert_array_equal(res.alpha_hist[k, :n], r.alpha_history)
+            assert res.failure_reason(k) == r.failure_reason
+            assert res.n_evals[k] == r.n_evals
+        assert res.n_reg[k] == 0
+    assert robust >= (0 if name == "c0_ls" else 1)
+
+
+def test_solve_invariants_large_batch(gpu_instances):
+    """Size-independent properties at the benchmark batch (4096 mu):
+    Armijo inequality on every accepted step (sqp.py:268), alpha = 2^-j,
+    converged <=> merit < tol, n_iter <= max_iter, finite results."""
+    inst = gpu_instances["c0_nm"]
+    cfg = P.SqpConfig()
+    mu = P.seeded_parameters(4096, seed=123)
+    res = P.solve_rom_batch(inst, mu, cfg)
+    assert np.all(np.isfinite(res.x)) and np.all(np.isfinite(res.lam))
+    assert np.all(res.n_iter <= cfg.max_iter)
+    assert np.all(res.status != P.driver.N.STATUS_KKT_SINGULAR)
+    for k in range(0, 4096, 7):
+        n = res.n_iter[k]
+        m = res.merit_hist[k, :n + 1]
+        a = res.alpha_hist[k, :n]
+        assert np.all(m[1:] <= (1 - cfg.armijo_c1 * a) * m[:-1])
+        assert np.all(np.log2(a) == np.round(np.log2(a)))
+        assert np.all(np.isnan(res.merit_hist[k, n + 1:]))
+    ok = res.status == 0
+    assert np.array_equal(res.converged[ok], res.merit[ok] < cfg.tol)
+    assert res.counters[0] == int(res.n_evals.sum()) * inst.n_blocks
+
+
+def test_batch_composition_invariance(gpu_instances):
+    """A mu solved alone, in a batch, or with a different slot count gives
+    bitwise-identical results (slots are independent state machines)."""
+    inst = gpu_instances["c0_nm"]
+    mu = P.seeded_parameters(64, seed=5)
+    full = P.solve_rom_batch(inst, mu)
+    for k in (0, 17, 63):
+        one = P.solve_rom_batch(inst, mu[k:k + 1])
+        np.testing.assert_array_equal(one.x[0], full.x[k])
+        np.testing.assert_array_equal(one.lam[0], full.lam[k])
+        assert one.n_iter[0] == full.n_iter[k]
+    g1 = P.solve_rom_batch(inst, mu, slots=1)
+    np.testing.assert_array_equal(g1.x, full.x)
+    np.testing.assert_array_equal(g1.n_evals, full.n_evals)
+
+
+def test_given_initial_point_and_multipliers(gpu_instances, oracle_instances, goldens):
+    """solve_rom with x0 (LS multipliers) and with (x0, lam0) (driver.py:571-575)."""
+    inst, oi, g = gpu_instances["c0_nm"], oracle_instances["c0_nm"], goldens["c0_nm"]
+    mu, x0, lam0 = g["mu"][:4], g["x0"][:4] * 1.01, g["lam0"][:4] * 0.5
+    r1 = P.solve_rom_batch(inst, mu, x0=x0)
+    r2 = P.solve_rom_batch(inst, mu, x0=x0, lam0=lam0)
+    for k in range(4):
+        o1 = O.solve(oi, *mu[k], x0=x0[k])
+        o2 = O.solve(oi, *mu[k], x0=x0[k], lam0=lam0[k])
+        assert rel(r1.x[k], o1.x) < 1e-9 and rel(r1.lam[k], o1.lam) < 1e-9
+        assert rel(r2.x[k], o2.x) < 1e-9 and rel(r2.lam[k], o2.lam) < 1e-9
+        np.testing.assert_array_equal(r2.lam0[k], lam0[k])
+
+
+def test_edge_cases(gpu_instances, oracle_instances):
+    inst, oi = gpu_instances["tiny_nm"], oracle_instances["tiny_nm"]
+    # empty batch
+    r = P.solve_rom_batch(inst, np.zeros((0, 2)))
+    assert r.x.shape == (0, inst.n_primal)
+    # max_iter = 1 and a loose tol (immediate convergence, n_iter = 0)
+    mu = P.seeded_parameters(8, seed=1)
+    r1 = P.solve_rom_batch(inst, mu, P.SqpConfig(max_iter=1))
+    assert np.all(r1.n_iter <= 1)
+    r0 = P.solve_rom_batch(inst, mu, P.SqpConfig(tol=1e300))
+    assert np.all(r0.n_iter == 0) and np.all(r0.converged)
+    np.testing.assert_array_equal(r0.x, r0.x0)
+    # forced line-search failure: max_halvings = 0 (one trial only)
+    cfg = P.SqpConfig(max_halvings=0)
+    r2 = P.solve_rom_batch(inst, mu, cfg)
+    for k in range(8):
+        o = O.solve(oi, *mu[k], cfg=O.SqpConfig(max_halvings=0))
+        assert r2.failure_reason(k) == o.failure_reason
+        assert rel(r2.x[k], o.x) < 1e-9
+    # bad arguments raise like the reference (ValueError)
+    with pytest.raises(ValueError):
+        P.solve_rom_batch(inst, np.zeros((3, 3)))
+    with pytest.raises(ValueError):
+        P.SqpConfig(tol=-1.0)
+    with pytest.raises(ValueError):
+        P.solve_rom_batch(inst, mu, x0=np.zeros((8, 3)))
+
+
+def test_singular_kkt_reports_convergence_error(goldens):
+    """n_c above rank(E): K singular -> ConvergenceError (sqp.py:199-207), here
+    surfaced per mu as a status (finding 1 of SURVEY §0)."""
+    import json
+    from .conftest import golden_path
+    arrays = dict(np.load(golden_path("tiny_nm", "artifacts")))
+    meta = json.loads(str(arrays["meta_json"]))
+    rng = np.random.default_rng(0)
+    n_c = 4 * meta["n_gam"][0] + 2          # > sum of interface latent dims
+    for b in range(meta["nblocks"]):
+        CA = arrays[f"b{b}_CA"]
+        arrays[f"b{b}_CA"] = np.vstack([CA, rng.standard_normal((n_c - CA.shape[0], CA.shape[1]))])
+    meta["n_c"] = n_c
+    arrays["meta_json"] = np.array(json.dumps(meta))
+    inst = P.RomInstance(arrays)
+    mu = P.seeded_parameters(4, seed=2)
+    res = P.solve_rom_batch(inst, mu)
+    assert np.all(res.status == P.driver.N.STATUS_LSTSQ_RANK)
+    with pytest.raises(P.ConvergenceError):
+        res.result(0)
+    lam0 = np.zeros((4, n_c))
+    res2 = P.solve_rom_batch(inst, mu, lam0=lam0)
+    assert np.all(res2.status == P.driver.N.STATUS_KKT_SINGULAR)
+    assert np.all(res2.n_reg == 0)
+
+
+def test_single_mu_api(gpu_instances, oracle_instances, goldens):
+    """solve_rom / init_guess / build_problem+iterate mirror the reference."""
+    inst, oi, g = gpu_instances["tiny_nm"], oracle_instances["tiny_nm"], goldens["tiny_nm"]
+    p = P.ParameterPoint(*g["mu"][0])
+    sol, rec = P.solve_rom(inst, p)
+    assert rel(sol.x_latent, g["x"][0]) < 1e-9
+    assert rec["n_iter"] == g["n_iter"][0]
+    x0, lam0 = P.init_guess(inst, p)
+    assert rel(x0, g["x0"][0]) < 1e-13 and rel(lam0, g["lam0"][0]) < 1e-10
+    prob = P.build_problem(inst, p)
+    r = P.iterate(prob, x0, lam0)
+    assert rel(r.x, g["x"][0]) < 1e-9
+    # block closures (reference SqpBlock duck type)
+    Br, Ri, Rg = prob.blocks[0].residual(*prob.split(x0)[0])
+    assert rel(Br, g["d0_b0_Br"]) < 1e-10
+    cval, cjac = prob.blocks[0].constraint(prob.split(x0)[0][1])
+    assert rel(cjac, g["d0_b0_con_jac"]) < 1e-12

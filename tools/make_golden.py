@@ -1,0 +1,233 @@
+"""Turn reference ROM instances into committed, reference-free fixtures.
+
+Run in the build container only (imports the reference from
+``/root/reference/pkg/src``; nothing on the GPU box reads it).  For every
+instance pickled by ``tools/make_artifacts.py`` it writes
+
+* ``tests/golden/<name>_artifacts.npz`` -- everything the online solve
+  consumes, extracted exactly the way ``driver.build_problem`` builds it
+  (driver.py:356-436): per block the decoder subnet (hyper.py:200-222) or the
+  restricted POD basis (pod.py:95-97), the full interface decoder
+  (autoencoder.py:104-112), the sampled residual rows and local column order
+  of ``RestrictedResidual`` (driver.py:392-396), ``CA = C @ A_i``
+  (driver.py:368-369), and the fitted RBF initializer (driver.py:59-90 with
+  scipy's private ``_coeffs/_shift/_scale/powers``);
+* ``tests/golden/<name>_golden.npz`` -- reference outputs on a seeded mu
+  batch: ``init_guess`` (driver.py:442-458), the full ``solve_rom`` result
+  (driver.py:554-597; x, lam, n_iter, merit/objective/alpha histories,
+  failure), and for the first few mu the per-block ``eval_gradients`` pieces
+  at (x0, lam0) (sqp.py:117-146), both decoders' values/Jacobians, the
+  sampled boundary vectors, the dense restricted Jacobian and the first KKT
+  step (sqp.py:162-208).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pickle
+import sys
+import warnings
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def extract(inst) -> dict:
+    from ddrom.autoencoder import Autoencoder
+    from ddrom.hyper import extract_subnet, hr_rows_for_subdomain
+    from ddrom.pod import LinearMap
+
+    part = inst.partition
+    grid = part.grid
+    out = {}
+    kind = "nm" if isinstance(inst.interior_maps[0], Autoencoder) else "ls"
+    n_int = [m.latent_dim for m in inst.interior_maps]
+    n_gam = [g.latent_dim for g in inst.interface_maps]
+    act = inst.interior_maps[0].activation if kind == "nm" else "linear"
+    for i, sub in enumerate(part.subdomains):
+        hr = inst.hr[i]
+        rows = hr.apply_B_rows()
+        io, gio = hr_rows_for_subdomain(part, i, rows)
+        cols = np.concatenate([sub.interior_cols[io], sub.interface_cols[gio]])
+        p = f"b{i}_"
+        out[p + "res_rows"] = sub.res_rows[rows].astype(np.int64)
+        out[p + "cols"] = cols.astype(np.int64)
+        out[p + "io"] = io.astype(np.int64)
+        out[p + "gio"] = gio.astype(np.int64)
+        out[p + "n_interior"] = np.int64(sub.n_interior)
+        out[p + "n_interface"] = np.int64(sub.n_interface)
+        out[p + "CA"] = inst.wfpc_C @ inst.fom_constraints.blocks[i].toarray()
+        im, gm = inst.interior_maps[i], inst.interface_maps[i]
+        if kind == "nm":
+            sn = extract_subnet(im, io)
+            out[p + "int_W1"] = np.ascontiguousarray(sn.W1)
+            out[p + "int_b1"] = sn.b1.copy()
+            out[p + "int_W2_indptr"] = sn.W2.indptr.astype(np.int64)
+            out[p + "int_W2_indices"] = sn.W2.indices.astype(np.int64)
+            out[p + "int_W2_data"] = sn.W2.data.copy()
+            out[p + "int_scale"] = sn.scale.copy()
+            out[p + "int_shift"] = sn.shift.copy()
+            out[p + "int_hidden_idx"] = sn.hidden_idx.astype(np.int64)
+            W2g = gm.W2g.tocsr()
+            out[p + "gam_W1"] = np.ascontiguousarray(gm.W1g)
+            out[p + "gam_b1"] = gm.b1g.copy()
+            out[p + "gam_W2_indptr"] = W2g.indptr.astype(np.int64)
+            out[p + "gam_W2_indices"] = W2g.indices.astype(np.int64)
+            out[p + "gam_W2_data"] = W2g.data.copy()
+            out[p + "gam_scale"] = gm.norm.scale.copy()
+            out[p + "gam_shift"] = gm.norm.shift.copy()
+        else:
+            assert isinstance(im, LinearMap) and isinstance(gm, LinearMap)
+            out[p + "int_Phi"] = np.ascontiguousarray(im.restrict_outputs(io).Phi)
+            out[p + "gam_Phi"] = np.ascontiguousarray(gm.Phi)
+    ini = inst.initializer
+    rbf = ini._rbf
+    meta = {
+        "kind": kind, "activation": act, "nx": grid.nx, "ny": grid.ny,
+        "nu": grid.nu, "nsub_x": part.nsub_x, "nsub_y": part.nsub_y,
+        "nblocks": len(part.subdomains), "n_int": n_int, "n_gam": n_gam,
+        "n_c": int(inst.n_mult), "rbf_kernel": rbf.kernel,
+        "rbf_epsilon": float(rbf.epsilon),
+        "provenance": {k: (v if isinstance(v, (int, float, str)) else str(v))
+                       for k, v in inst.provenance.items()},
+    }
+    out["rbf_lo"] = ini.lo.copy()
+    out["rbf_hi"] = ini.hi.copy()
+    out["rbf_y"] = np.ascontiguousarray(rbf.y)
+    out["rbf_coeffs"] = np.ascontiguousarray(rbf._coeffs)
+    out["rbf_shift"] = np.asarray(rbf._shift, dtype=float)
+    out["rbf_scale"] = np.asarray(rbf._scale, dtype=float)
+    out["rbf_powers"] = np.asarray(rbf.powers, dtype=np.int64)
+    out["meta_json"] = np.array(json.dumps(meta))
+    return out
+
+
+def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
+    from ddrom.burgers import ParameterPoint, assemble
+    from ddrom.driver import build_problem, init_guess, solve_rom
+    from ddrom.errors import ConvergenceError
+    from ddrom.hyper import extract_subnet, hr_rows_for_subdomain
+    from ddrom.partition import RestrictedResidual
+    from ddrom.sqp import SqpConfig, assemble_and_solve_kkt, eval_gradients
+
+    cfg = SqpConfig()
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(1.0, 1.0e4, B)
+    lam = rng.uniform(5.0, 25.0, B)
+    mu = np.stack([a, lam], axis=1)
+    n_D = sum(ni + ng for ni, ng in inst.latent_layout)
+    n_C = inst.n_mult
+    K = cfg.max_iter
+    g = {
+        "mu": mu, "seed": np.int64(seed),
+        "x0": np.zeros((B, n_D)), "lam0": np.zeros((B, n_C)),
+        "x": np.zeros((B, n_D)), "lam": np.zeros((B, n_C)),
+        "n_iter": np.zeros(B, np.int64), "converged": np.zeros(B, np.int64),
+        "failure": np.zeros(B, np.int64),           # 0 none, 1 line_search, 2 kkt
+        "merit_hist": np.full((B, K + 1), np.nan),
+        "obj_hist": np.full((B, K + 1), np.nan),
+        "alpha_hist": np.full((B, K), np.nan),
+    }
+    part = inst.partition
+    for k in range(B):
+        p = ParameterPoint(float(a[k]), float(lam[k]))
+        ops = assemble(part.grid, p)
+        prob = build_problem(inst, ops)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            x0, lam0 = init_guess(inst, p, ops=ops, prob=prob)
+        g["x0"][k], g["lam0"][k] = x0, lam0
+        try:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                sol, rec = solve_rom(inst, p, cfg, compute_error=False)
+        except ConvergenceError:
+            g["failure"][k] = 2
+            continue
+        r = sol.sqp
+        g["x"][k], g["lam"][k] = r.x, r.lam
+        g["n_iter"][k] = r.n_iter
+        g["converged"][k] = int(r.converged)
+        g["failure"][k] = 0 if r.failure_reason is None else 1
+        g["merit_hist"][k, :len(r.merit_history)] = r.merit_history
+        g["obj_hist"][k, :len(r.objective_history)] = r.objective_history
+        g["alpha_hist"][k, :len(r.alpha_history)] = r.alpha_history
+        if k < n_detail:
+            ev = eval_gradients(prob, x0, lam0)
+            g[f"d{k}_rho"] = ev.rho
+            g[f"d{k}_con"] = ev.con
+            g[f"d{k}_merit"] = np.float64(ev.merit)
+            g[f"d{k}_objective"] = np.float64(ev.objective)
+            s, s_lam = assemble_and_solve_kkt(prob, ev, cfg.reg_scale)
+            g[f"d{k}_step"] = s
+            g[f"d{k}_step_lam"] = s_lam
+            for i, be in enumerate(ev.blocks):
+                q = f"d{k}_b{i}_"
+                g[q + "Br"] = be.Br
+                g[q + "R_int"] = be.R_int
+                g[q + "R_gam"] = be.R_gam
+                g[q + "con_val"] = be.con_val
+                g[q + "con_jac"] = be.con_jac
+            for i, (xi, xg) in enumerate(inst.split_latent(x0)):
+                q = f"d{k}_b{i}_"
+                sub = part.subdomains[i]
+                rows = inst.hr[i].apply_B_rows()
+                io, gio = hr_rows_for_subdomain(part, i, rows)
+                im, gm = inst.interior_maps[i], inst.interface_maps[i]
+                if hasattr(im, "restrict_outputs"):
+                    si = im.restrict_outputs(io)
+                else:
+                    si = extract_subnet(im, io)
+                g[q + "int_g"] = si.decode(xi)
+                g[q + "int_J"] = np.asarray(si.jacobian(xi))
+                g[q + "gam_g"] = gm.decode(xg)
+                g[q + "gam_J"] = np.asarray(gm.jacobian(xg))
+                cols = np.concatenate([sub.interior_cols[io],
+                                       sub.interface_cols[gio]])
+                rr = RestrictedResidual(ops, sub.res_rows[rows], cols)
+                v = np.concatenate([g[q + "int_g"], g[q + "gam_g"][gio]])
+                g[q + "stencil_r"] = rr.residual(v)
+                g[q + "stencil_Jd"] = rr.jacobian(v).toarray()
+                n = part.grid.nnode
+                rws = sub.res_rows[rows]
+                node = np.where(rws < n, rws, rws - n)
+                isu = rws < n
+                g[q + "bx"] = np.where(isu, ops.bux[node], ops.bvx[node])
+                g[q + "by"] = np.where(isu, ops.buy[node], ops.bvy[node])
+                g[q + "bc"] = np.where(isu, ops.cu[node], ops.cv[node])
+    return g
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cache", default=os.path.join(ROOT, "artifacts_cache"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden"))
+    ap.add_argument("--names", nargs="*",
+                    default=["tiny_nm", "tiny_ls", "c0_nm", "c0_ls"])
+    ap.add_argument("--B", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--detail", type=int, default=3)
+    a = ap.parse_args()
+    os.makedirs(a.out, exist_ok=True)
+    for name in a.names:
+        with open(os.path.join(a.cache, f"{name}.pkl"), "rb") as f:
+            inst = pickle.load(f)
+        art = extract(inst)
+        np.savez_compressed(os.path.join(a.out, f"{name}_artifacts.npz"), **art)
+        gd = goldens(inst, a.B, a.seed, a.detail)
+        np.savez_compressed(os.path.join(a.out, f"{name}_golden.npz"), **gd)
+        print(name, "n_iter", gd["n_iter"].tolist(), "failure",
+              gd["failure"].tolist(), flush=True)
+
+
+if __name__ == "__main__":
+    main()
