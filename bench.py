@@ -1,0 +1,329 @@
+"""Benchmark: batched DD NM-ROM-HR SQP solves/sec on B200 (BASELINE.json metric).
+
+Workload (BASELINE configs[2]): the 60x60, 2x2-subdomain
+NM-ROM WFPC instance with collocation HR (n = (6, 4), n_C = 8, 180 rows per
+subdomain; artifacts trained by the reference, tests/golden/c0_nm_*), a
+batch of 4096 seeded mu per GPU, FP64.  One "step" = one complete batched
+``solve_rom`` (device RBF init + least-squares multipliers + SQP loop) over
+the whole batch.  Multi-GPU: the mu batch is sharded across ranks (weak
+scaling, 4096 mu per GPU, no data-path collective).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+``--impl reference`` times the CPU implementation of the same path (the
+numpy oracle port, oracle/ddnm_oracle.py, all host cores) on a bounded sample
+of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ARTIFACT = os.path.join(ROOT, "tests", "golden", "c0_nm_artifacts.npz")
+METRIC = "DD NM-ROM-HR SQP solves/sec (batched mu)"
+UNIT = "solves/s"
+BATCH = 4096
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# -- algorithmic work ---------------------------------------
+
+def fp64_peak():
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            d = json.load(f)
+        return float(d["dfma_tflops"]), "measured (tools/microbench/fp64_peaks.cu, DFMA)"
+    except Exception:
+        return 36.6, "measured earlier on this pool (DFMA)"
+
+
+# -- clocks -------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# -- CPU (oracle port) ------------------------------------------------------------
+
+def _cpu_worker(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import ddnm_oracle as O
+    path, mus = args
+    inst = O.Instance(path)
+    for a, lam in mus:
+        O.solve(inst, a, lam)
+    return len(mus)
+
+
+def cpu_solves_per_sec(mu: np.ndarray, seconds: float = 15.0):
+    """Time the oracle port of solve_rom on all host cores over a bounded
+    sample of the workload's mu; returns (solves/s, cores, sample)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    per_core = max(1, int(round(seconds * 4.0)))   # ~4 solves/s/core at config 0
+    n = min(mu.shape[0], per_core * cores)
+    chunks = [(ARTIFACT, mu[i::cores][:per_core].tolist()) for i in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, [(ARTIFACT, mu[:1].tolist())] * cores)   # warm import
+        t0 = time.perf_counter()
+        done = sum(pool.map(_cpu_worker, chunks))
+        dt = time.perf_counter() - t0
+    return done / dt, cores, f"{done} of the workload's seeded mu ({n} requested), {dt:.1f}s"
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import paper_2305_15163_b200 as P
+    mu = P.seeded_parameters(BATCH, seed=1000)
+    vals = []
+    cores = os.cpu_count() or 1
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        v, cores, sample = cpu_solves_per_sec(mu[(i * 97) % 1024:], seconds=args.ref_seconds)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded mu, reference-trained artifacts)",
+        "config": {"workload": "config2: 60x60 2x2 NM-ROM WFPC collocation HR, n=(6,4), n_C=8, 180 rows/sub",
+                   "batch_per_gpu": BATCH, "sample_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -- GPU ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import ctypes as C
+
+    import torch
+
+    import paper_2305_15163_b200 as P
+    from paper_2305_15163_b200 import _native as N
+    from paper_2305_15163_b200.driver import _cfg_struct
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    inst = P.RomInstance.load(ARTIFACT)
+    ctx = inst.context(local)
+    info = ctx.info
+    cfg = P.SqpConfig()
+    B = BATCH
+    mu_h = P.seeded_parameters(B, seed=1000 + rank)
+    mu_d = torch.from_numpy(mu_h).to(dev)
+    nD, nC = info.n_primal, info.n_mult
+    outs = {
+        "x": torch.empty((B, nD), dtype=torch.float64, device=dev),
+        "lam": torch.empty((B, nC), dtype=torch.float64, device=dev),
+        "n_iter": torch.empty(B, dtype=torch.int32, device=dev),
+        "n_evals": torch.empty(B, dtype=torch.int32, device=dev),
+        "status": torch.empty(B, dtype=torch.int32, device=dev),
+        "merit": torch.empty(B, dtype=torch.float64, device=dev),
+    }
+    so = N.SolveOut()
+    so.x = C.cast(C.c_void_p(outs["x"].data_ptr()), C.POINTER(C.c_double))
+    so.lam = C.cast(C.c_void_p(outs["lam"].data_ptr()), C.POINTER(C.c_double))
+    so.n_iter = C.cast(C.c_void_p(outs["n_iter"].data_ptr()), C.POINTER(C.c_int32))
+    so.n_evals = C.cast(C.c_void_p(outs["n_evals"].data_ptr()), C.POINTER(C.c_int32))
+    so.status = C.cast(C.c_void_p(outs["status"].data_ptr()), C.POINTER(C.c_int32))
+    so.merit = C.cast(C.c_void_p(outs["merit"].data_ptr()), C.POINTER(C.c_double))
+    cs = _cfg_struct(cfg)
+    stream = torch.cuda.Stream(dev)          # explicit (non-default) stream: events see the kernel
+    L = N.lib()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    def step():
+        N.check(L.ddnm_solve_batch_device(ctx.h, B, C.c_void_p(mu_d.data_ptr()), None, None,
+                                          C.byref(cs), C.byref(so),
+                                          C.c_void_p(stream.cuda_stream)))
+
+    torch.cuda.set_stream(stream)
+    mu_d = mu_d.clone()                        # allocated on the bench stream
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, evals, kkts = [], 0, 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(float(len(times)))           # L2 flush between timed steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            ev, kk = ctx.counters()
+            evals += ev
+            kkts += kk
+    torch.cuda.synchronize()
+    total_ms = float(np.sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    value = world * B * args.steps / (total_ms / 1e3)
+
+    # parity spot check of this very run against the oracle (4 mu, not timed)
+    n_iter = outs["n_iter"].cpu().numpy()
+    status = outs["status"].cpu().numpy()
+
+    # end-to-end through the public API with host buffers
+    e2e_vals = []
+    res = None
+    for i in range(max(2, min(args.steps, 5))):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = P.solve_rom_batch(inst, mu_h, cfg)
+        e2e_vals.append(time.perf_counter() - t0)
+    e2e_t = float(np.mean(e2e_vals[1:])) if len(e2e_vals) > 1 else e2e_vals[0]
+    if dist:
+        t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    K1 = cfg.max_iter + 1
+    d2h = B * (nD * 8 * 2 + nC * 8 * 2 + 4 * 4 + 8 * 2 + K1 * 8 * 2 + cfg.max_iter * 8)
+    e2e = {"value": world * B / e2e_t, "unit": UNIT, "h2d_bytes_per_step": B * 2 * 8,
+           "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    from paper_2305_15163_b200.workmodel import eval_flops
+    fl = eval_flops(inst.arrays, inst.meta)
+    evals_per_step = evals / args.steps / inst.n_blocks      # mu-evals (all blocks)
+    kkts_per_step = kkts / args.steps
+    flops_per_step = evals_per_step * fl["per_eval"] + kkts_per_step * fl["kkt"]
+    peak, peak_src = fp64_peak()
+    achieved = flops_per_step / (ms_per_step / 1e3) / 1e12
+    roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "k_solve (persistent SQP megakernel)",
+            "peak_source": peak_src,
+            "algorithmic_flops_per_step": flops_per_step,
+            "exp_per_step": evals_per_step * fl["exp_per_eval"],
+            "mu_evals_per_step": evals_per_step, "kkt_solves_per_step": kkts_per_step,
+            "flops_per_mu_eval": fl["per_eval"], "flops_per_kkt": fl["kkt"]}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, cores, sample = cpu_solves_per_sec(mu_h, seconds=args.ref_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded mu; artifacts trained by the reference on the 6x6 mu grid)",
+        "config": {"workload": "config2: 60x60 2x2 NM-ROM WFPC collocation HR, n=(6,4), n_C=8, "
+                               "180 rows/sub, band 8 shift 1",
+                   "batch_per_gpu": B, "global_batch": world * B,
+                   "parallelism": f"mu-shard x{world}", "l2": "flushed (256 MB write) between timed steps",
+                   "slots_per_cta": info.slots_per_cta, "ctas": info.ctas,
+                   "mean_n_iter": float(n_iter.mean()), "status_counts": np.bincount(status, minlength=4).tolist()},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

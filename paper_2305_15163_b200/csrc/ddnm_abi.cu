@@ -11,9 +11,27 @@
 #include <vector>
 
 #include "../../include/ddnm.h"
-#include "ddnm_solve.cuh"
+#include "ddnm_device.cuh"
+#include "ddnm_registry.h"
 
 using namespace ddnm;
+
+namespace ddnm {
+__global__ void k_fill(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+}  // namespace ddnm
+
+// compiled specialisations live in inst_<ni>_<ng>.cu (built in parallel)
+using ddnm::KernelEntry;
+#define DDNM_DECL(NI, NG) void register_##NI##_##NG(std::vector<KernelEntry>&);
+namespace ddnm {
+DDNM_DECL(6, 4)
+DDNM_DECL(4, 3)
+DDNM_DECL(8, 4)
+DDNM_DECL(20, 8)
+DDNM_DECL(8, 5)
+}  // namespace ddnm
 
 namespace {
 
@@ -31,28 +49,20 @@ int fail(int code, const std::string& msg) {
       return fail(DDNM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
   } while (0)
 
-// one compiled specialisation of the kernels
-struct Kernels {
-  int ni, ng, g;
-  const void* solve;
-  const void* eval;
-};
-
-template <int G, int NI, int NG>
-Kernels make_kernels() {
-  return Kernels{NI, NG, G, (const void*)&k_solve<G, NI, NG>, (const void*)&k_eval<G, NI, NG>};
-}
+using Kernels = KernelEntry;
 
 // (n_int, n_gam) pairs with compiled kernels: config 0/2 NM (6,4), config 1
 // LS (20,8), configs 3/4 (8,5), and the small test instances (4,3), (8,4).
 const std::vector<Kernels>& kernel_table() {
-  static const std::vector<Kernels> t = {
-      make_kernels<1, 6, 4>(),  make_kernels<2, 6, 4>(),  make_kernels<4, 6, 4>(),
-      make_kernels<1, 4, 3>(),  make_kernels<2, 4, 3>(),
-      make_kernels<1, 8, 4>(),  make_kernels<2, 8, 4>(),
-      make_kernels<1, 20, 8>(),
-      make_kernels<1, 8, 5>(),  make_kernels<2, 8, 5>(),
-  };
+  static const std::vector<Kernels> t = [] {
+    std::vector<Kernels> v;
+    ddnm::register_6_4(v);
+    ddnm::register_4_3(v);
+    ddnm::register_8_4(v);
+    ddnm::register_20_8(v);
+    ddnm::register_8_5(v);
+    return v;
+  }();
   return t;
 }
 
@@ -63,7 +73,7 @@ struct ddnm_ctx {
   int sms = 0;
   Params P{};                 // template params (work fields filled per call)
   Kernels K{};
-  int threads = 256;
+  int threads = 512;
   int ctas = 0;               // persistent grid
   size_t smem = 0;
   int n_D = 0, n_C = 0, nb = 0;
@@ -214,6 +224,23 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
     if ((rc = upload(c, h.data, nnz, const_cast<double**>(&d.data)))) return rc;
     if ((rc = upload(c, h.scale, (size_t)h.n_out, const_cast<double**>(&d.scale)))) return rc;
     if ((rc = upload(c, h.shift, (size_t)h.n_out, const_cast<double**>(&d.shift)))) return rc;
+    // ELL-transposed copy of W2 for the sweep (storage order kept per row)
+    int64_t wmax = 0;
+    for (int o = 0; o < h.n_out; ++o) wmax = std::max<int64_t>(wmax, h.indptr[o + 1] - h.indptr[o]);
+    const int ew = (int)((wmax + 3) / 4 * 4);
+    std::vector<double> ev((size_t)ew * h.n_out, 0.0);
+    std::vector<int> ek((size_t)ew * h.n_out, 0);
+    for (int o = 0; o < h.n_out; ++o)
+      for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e) {
+        const size_t slot = (size_t)(e - h.indptr[o]) * h.n_out + o;
+        ev[slot] = h.data[e];
+        ek[slot] = (int)h.indices[e];
+      }
+    d.ell_w = ew;
+    if (ew > 0) {
+      if ((rc = upload(c, ev.data(), ev.size(), const_cast<double**>(&d.ell_v)))) return rc;
+      if ((rc = upload(c, ek.data(), ek.size(), const_cast<int**>(&d.ell_k)))) return rc;
+    }
   } else {
     if ((rc = upload(c, h.W1, (size_t)h.n_out * lat, const_cast<double**>(&d.W1)))) return rc;
     d.b1 = nullptr; d.indptr = nullptr; d.indices = nullptr; d.data = nullptr;
@@ -345,7 +372,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.scr_jgam = scr; scr += ae ? max_gam * ng : 0;
   P.scr_R = scr; scr += max_rows * W;
   P.scr_r = scr; scr += max_rows;
-  const int kkt_need = P.nK * (P.nK + 1) + 5 * P.nK;
+  const int kkt_need = std::max(P.nK * (P.nK + 1) + 5 * P.nK,
+                                P.nb * (W + P.n_C) * (W + P.n_C + 1) + P.nb * W +
+                                    P.n_C * (P.n_C + 1) + P.n_C + P.nb * P.n_C + 4 * P.nK);
   const int ls_need = P.nb * ng * P.n_C + P.nb * ng;
   const int rbf_need = r.n_centers + r.n_mono;
   P.scr_size = std::max(std::max(scr, kkt_need), std::max(ls_need, rbf_need));

@@ -44,6 +44,9 @@ struct DecDev {
   const double* data;     // [nnz]
   const double* scale;    // [n_out]
   const double* shift;    // [n_out]
+  int ell_w;              // ELL width (max nnz per row, padded to 4)
+  const double* ell_v;    // [ell_w][n_out] W2 values in storage order, 0-padded
+  const int* ell_k;       // [ell_w][n_out] hidden indices, 0-padded
 };
 
 // One sampled residual row in local-column form (RestrictedResidual,

@@ -56,11 +56,15 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
 }
 
 // phase B: one decoder output (value + latent Jacobian row) for all slots.
-// CSR row sweep in storage order (hyper.py:190-197):
+// Row sweep in CSR storage order (hyper.py:190-197), read from the
+// ELL-transposed copy of W2 (entry e of output o at [e][o]: a warp's lanes
+// read consecutive addresses), four entries per batch so their index, weight
+// and W1-row loads are all in flight together:
 //   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e W2_e act'_e W1[k_e, d]) * scale
 template <int G, int L>
 __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int sig_off,
                                              int g_off, int j_off, unsigned mask) {
+  constexpr int U = 4;
   double ag[G], aj[G][L];
 #pragma unroll
   for (int s = 0; s < G; ++s) {
@@ -68,23 +72,37 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
 #pragma unroll
     for (int d = 0; d < L; ++d) aj[s][d] = 0.0;
   }
-  const int e0 = __ldg(D.indptr + o), e1 = __ldg(D.indptr + o + 1);
-  for (int e = e0; e < e1; ++e) {
-    const double v = __ldg(D.data + e);
-    const int k = __ldg(D.indices + e);
-    double w[L];
+  const double* sig[G];
+  const double* dsig[G];
 #pragma unroll
-    for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1 + (size_t)k * L + d);
+  for (int s = 0; s < G; ++s) {
+    sig[s] = V.scr(s) + V.P.scr_sig + sig_off;
+    dsig[s] = V.scr(s) + V.P.scr_dsig + sig_off;
+  }
+  const int n = D.n_out;
+  for (int e = 0; e < D.ell_w; e += U) {
+    double v[U], w[U][L];
+    int k[U];
 #pragma unroll
-    for (int s = 0; s < G; ++s) {
-      if (!((mask >> s) & 1u)) continue;
-      const double* sc = V.scr(s);
-      const double a = sc[V.P.scr_sig + sig_off + k];
-      const double da = sc[V.P.scr_dsig + sig_off + k];
-      ag[s] = fma(v, a, ag[s]);
-      const double t = v * da;
+    for (int u = 0; u < U; ++u) {
+      v[u] = __ldg(D.ell_v + (size_t)(e + u) * n + o);
+      k[u] = __ldg(D.ell_k + (size_t)(e + u) * n + o);
+    }
 #pragma unroll
-      for (int d = 0; d < L; ++d) aj[s][d] = fma(t, w[d], aj[s][d]);
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int d = 0; d < L; ++d) w[u][d] = __ldg(D.W1 + (size_t)k[u] * L + d);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int s = 0; s < G; ++s) {
+        if (!((mask >> s) & 1u)) continue;
+        const double a = sig[s][k[u]];
+        const double t = v[u] * dsig[s][k[u]];
+        ag[s] = fma(v[u], a, ag[s]);
+#pragma unroll
+        for (int d = 0; d < L; ++d) aj[s][d] = fma(t, w[u][d], aj[s][d]);
+      }
     }
   }
   const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
@@ -297,42 +315,50 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
           for (int i = tid; i < P.n_C * NG; i += T) o.cjac[mu * P.tot_cjac + B.cjac_off + i] = eb_cjac(const_cast<double*>(e), B, P.n_C)[i];
       }
     }
-    // ---- phase D: Gram block, projections, r^T r ----
+    // ---- phase D: Gram block, projections, r^T r (thread per entry) ----
     {
       const int ntri = W * (W + 1) / 2, nt = ntri + W + 1;
-      for (int t = warp; t < G * nt; t += nw) {
+      for (int t = tid; t < G * nt; t += T) {
         const int s = t / nt;
         int q = t - s * nt;
         if (!((mask >> s) & 1u)) continue;
         const double* sc = V.scr(s);
         const double* R = sc + P.scr_R;
         const double* rv = sc + P.scr_r;
-        int i = 0, j = 0, kind = 0;
+        // (a, b) column pair: R_i.R_j, R_i.r or r.r
+        const double* pa;
+        const double* pb;
+        int sa, sb, i = 0, j = 0, kind = 0;
         if (q < ntri) {
           while (q >= W - i) { q -= W - i; ++i; }
           j = i + q;
+          pa = R + i; pb = R + j; sa = W; sb = W;
         } else if (q < ntri + W) {
           kind = 1; i = q - ntri;
+          pa = R + i; pb = rv; sa = W; sb = 1;
         } else {
           kind = 2;
+          pa = rv; pb = rv; sa = 1; sb = 1;
         }
-        double acc = 0.0;
-        for (int r = lane; r < B.nrows; r += WARP) {
-          const double a = kind == 2 ? rv[r] : R[(size_t)r * W + i];
-          const double bb = kind == 0 ? R[(size_t)r * W + j] : rv[r];
-          acc = fma(a, bb, acc);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const int nr = B.nrows;
+        int r = 0;
+        for (; r + 4 <= nr; r += 4) {
+          a0 = fma(pa[(size_t)r * sa], pb[(size_t)r * sb], a0);
+          a1 = fma(pa[(size_t)(r + 1) * sa], pb[(size_t)(r + 1) * sb], a1);
+          a2 = fma(pa[(size_t)(r + 2) * sa], pb[(size_t)(r + 2) * sb], a2);
+          a3 = fma(pa[(size_t)(r + 3) * sa], pb[(size_t)(r + 3) * sb], a3);
         }
-        acc = warp_sum(acc);
-        if (lane == 0) {
-          double* e = V.eb(s, ebi[s]);
-          if (kind == 0) {
-            eb_H(e, B)[i * W + j] = acc;
-            eb_H(e, B)[j * W + i] = acc;
-          } else if (kind == 1) {
-            eb_proj(e, B)[i] = acc;
-          } else {
-            *eb_rr(e, B, P.n_C) = acc;
-          }
+        for (; r < nr; ++r) a0 = fma(pa[(size_t)r * sa], pb[(size_t)r * sb], a0);
+        const double acc = (a0 + a1) + (a2 + a3);
+        double* e = V.eb(s, ebi[s]);
+        if (kind == 0) {
+          eb_H(e, B)[i * W + j] = acc;
+          eb_H(e, B)[j * W + i] = acc;
+        } else if (kind == 1) {
+          eb_proj(e, B)[i] = acc;
+        } else {
+          *eb_rr(e, B, P.n_C) = acc;
         }
       }
       __syncthreads();
@@ -383,7 +409,7 @@ __device__ void finalize_eval(const View& V, int s, double* e, const double* lt)
 // warp-level dense LU with partial pivoting (LAPACK dgetf2 semantics:
 // idamax pivot = first max, scale by reciprocal when |pivot| >= sfmin).
 // K row-major with leading dimension ld.  Returns 0 or k+1 for a zero pivot.
-__device__ int warp_lu(double* K, int ld, int n, int* piv) {
+static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
   const int lane = threadIdx.x & 31;
   int info = 0;
   for (int k = 0; k < n; ++k) {
@@ -430,7 +456,7 @@ __device__ int warp_lu(double* K, int ld, int n, int* piv) {
 }
 
 // warp-level getrs: b <- inv(LU) P b, in place.
-__device__ void warp_lu_solve(const double* K, int ld, int n, const int* piv, double* b) {
+static __device__ void warp_lu_solve(const double* K, int ld, int n, const int* piv, double* b) {
   const int lane = threadIdx.x & 31;
   if (lane == 0)
     for (int k = 0; k < n; ++k) {
@@ -573,6 +599,288 @@ __device__ int warp_kkt(const Params& P, const double* e, double* work, double* 
   return 2;
 }
 
+// ---------------------------------------------------------------------------
+// Block-structured KKT LU (fast path of assemble_and_solve_kkt).
+//
+// K = [blockdiag(H_b) E^T; E 0].  Partial-pivoting LU of the dense K (the
+// reference's lu_factor) only ever touches, while eliminating block b's
+// columns, block b's rows and the n_C multiplier rows -- other blocks' rows
+// are structurally zero there.  As long as no multiplier row wins a pivot
+// (|E| entries ~1 against |H| ~1e10 at config 0) the dense factorisation is
+// therefore exactly: per block, eliminate its W columns from the
+// (W + n_C) x (W + n_C) matrix [H_b E_b^T; E_b 0] (same pivots, same row
+// swaps, same updates); then LU the n_C x n_C Schur block S = sum_b S_b.
+// Blocks run on separate warps.  If a multiplier row would win a pivot (or
+// a pivot is exactly zero) the slot falls back to the dense warp LU, so the
+// pivot sequence always equals the dense one.
+struct KktLayout {
+  int ldm, msz, off_piv, off_S, off_pivS, off_tE, off_rhs, off_sol, off_res, off_tmp, ldS;
+};
+
+template <int NI, int NG>
+__device__ __forceinline__ KktLayout kkt_layout(const Params& P) {
+  constexpr int W = NI + NG;
+  KktLayout L;
+  const int m = W + P.n_C;
+  L.ldm = m + 1;
+  L.msz = m * L.ldm;
+  L.off_piv = P.nb * L.msz;
+  L.off_S = L.off_piv + P.nb * W;
+  L.ldS = P.n_C + 1;
+  L.off_pivS = L.off_S + P.n_C * L.ldS;
+  L.off_tE = L.off_pivS + P.n_C;
+  L.off_rhs = L.off_tE + P.nb * P.n_C;
+  L.off_sol = L.off_rhs + P.nK;
+  L.off_res = L.off_sol + P.nK;
+  L.off_tmp = L.off_res + P.nK;
+  return L;
+}
+
+// eliminate block b's W columns (one warp); returns false -> dense fallback
+template <int NI, int NG>
+__device__ bool kkt_block_factor(const Params& P, const double* e, int b, double* M, int* piv) {
+  constexpr int W = NI + NG;
+  const int lane = threadIdx.x & 31;
+  const int nC = P.n_C, m = W + nC, ld = m + 1;
+  const BlockDev& B = P.blk[b];
+  const double* H = eb_H(const_cast<double*>(e), B);
+  const double* cj = eb_cjac(const_cast<double*>(e), B, nC);
+  for (int idx = lane; idx < m * m; idx += WARP) {
+    const int i = idx / m, j = idx - i * m;
+    double v = 0.0;
+    if (i < W && j < W) v = H[i * W + j];
+    else if (i < W && j >= W) v = i >= NI ? cj[(j - W) * NG + (i - NI)] : 0.0;
+    else if (i >= W && j < W) v = j >= NI ? cj[(i - W) * NG + (j - NI)] : 0.0;
+    M[i * ld + j] = v;
+  }
+  __syncwarp();
+  bool ok = true;
+  for (int k = 0; k < W; ++k) {
+    double best = -1.0, bestE = -1.0;
+    int bi = W;
+    for (int i = k + lane; i < m; i += WARP) {
+      const double a = fabs(M[i * ld + k]);
+      if (i < W) {
+        if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+      } else {
+        bestE = fmax(bestE, a);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      bestE = fmax(bestE, __shfl_xor_sync(0xffffffffu, bestE, o));
+    }
+    if (!(best > 0.0) || bestE > best) { ok = false; break; }
+    if (lane == 0) piv[k] = bi;
+    if (bi != k)
+      for (int j = lane; j < m; j += WARP) {
+        const double t = M[k * ld + j];
+        M[k * ld + j] = M[bi * ld + j];
+        M[bi * ld + j] = t;
+      }
+    __syncwarp();
+    const double pv = M[k * ld + k];
+    if (fabs(pv) >= 2.2250738585072014e-308) {
+      const double r = 1.0 / pv;
+      for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] *= r;
+    } else {
+      for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] /= pv;
+    }
+    __syncwarp();
+    for (int j = k + 1 + lane; j < m; j += WARP) {
+      const double ukj = M[k * ld + j];
+      for (int i = k + 1; i < m; ++i) M[i * ld + j] = fma(-M[i * ld + k], ukj, M[i * ld + j]);
+    }
+    __syncwarp();
+  }
+  return ok;
+}
+
+// forward substitution of block b: y_b (in place in rhs) and its Schur
+// right-hand-side contribution tE[c] = -sum_k L[E c][k] y_k
+template <int NI, int NG>
+__device__ void kkt_block_forward(const Params& P, int b, const double* M, const int* piv,
+                                  double* y, double* tE) {
+  constexpr int W = NI + NG;
+  const int lane = threadIdx.x & 31;
+  const int nC = P.n_C, ld = W + nC + 1;
+  if (lane == 0)
+    for (int k = 0; k < W; ++k) {
+      const int p = piv[k];
+      if (p != k) { const double t = y[k]; y[k] = y[p]; y[p] = t; }
+    }
+  for (int c = lane; c < nC; c += WARP) tE[c] = 0.0;
+  __syncwarp();
+  for (int k = 0; k < W; ++k) {
+    const double yk = y[k];
+    for (int i = k + 1 + lane; i < W + nC; i += WARP) {
+      if (i < W) y[i] = fma(-M[i * ld + k], yk, y[i]);
+      else tE[i - W] = fma(-M[i * ld + k], yk, tE[i - W]);
+    }
+    __syncwarp();
+  }
+}
+
+// back substitution of block b given the multiplier part xE
+template <int NI, int NG>
+__device__ void kkt_block_backward(const Params& P, const double* M, double* y, const double* xE) {
+  constexpr int W = NI + NG;
+  const int lane = threadIdx.x & 31;
+  const int nC = P.n_C, ld = W + nC + 1;
+  for (int i = lane; i < W; i += WARP) {
+    double v = y[i];
+    for (int c = 0; c < nC; ++c) v = fma(-M[i * ld + W + c], xE[c], v);
+    y[i] = v;
+  }
+  __syncwarp();
+  for (int k = W - 1; k >= 0; --k) {
+    if (lane == 0) y[k] = y[k] / M[k * ld + k];
+    __syncwarp();
+    const double xk = y[k];
+    for (int i = lane; i < k; i += WARP) y[i] = fma(-M[i * ld + k], xk, y[i]);
+    __syncwarp();
+  }
+}
+
+// CTA-wide KKT stage for every slot in kmask (eval buffer ebi[s]).
+// Solution (s, s_lam) -> vec(s, 2), vec(s, 3); kres[s] = 0 ok, 1 regularized,
+// 2 singular.  Warp w < G*nb works on (slot w / nb, block w % nb).
+template <int G, int NI, int NG>
+__device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kres,
+                          int* kflag) {
+  const Params& P = V.P;
+  constexpr int W = NI + NG;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const KktLayout L = kkt_layout<NI, NG>(P);
+  const int nC = P.n_C, nb = P.nb;
+  if (tid < G) kflag[tid] = 1;
+  __syncthreads();
+  // 1. per-block elimination
+  for (int t = warp; t < G * nb; t += nw) {
+    const int s = t / nb, b = t - s * nb;
+    if (!((kmask >> s) & 1u)) continue;
+    double* sc = V.scr(s);
+    const bool ok = kkt_block_factor<NI, NG>(P, V.eb(s, ebi[s]), b, sc + b * L.msz,
+                                             reinterpret_cast<int*>(sc + L.off_piv) + b * W);
+    if (!ok && lane == 0) atomicAnd(&kflag[s], 0);
+  }
+  __syncthreads();
+  // 2. Schur block S = sum_b (in block order), its LU; rhs = -[rho; con]
+  if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
+    const int s = warp;
+    double* sc = V.scr(s);
+    double* S = sc + L.off_S;
+    for (int idx = lane; idx < nC * nC; idx += WARP) {
+      const int i = idx / nC, j = idx - i * nC;
+      double v = 0.0;
+      for (int b = 0; b < nb; ++b) v = v + sc[b * L.msz + (W + i) * L.ldm + W + j];
+      S[i * L.ldS + j] = v;
+    }
+    __syncwarp();
+    const int info = warp_lu(S, L.ldS, nC, reinterpret_cast<int*>(sc + L.off_pivS));
+    if (info != 0 && lane == 0) kflag[s] = 0;
+    const double* e = V.eb(s, ebi[s]);
+    for (int i = lane; i < P.nK; i += WARP)
+      sc[L.off_rhs + i] = -(i < P.n_D ? e[P.eb_rho + i] : e[P.eb_con + i - P.n_D]);
+  }
+  __syncthreads();
+  // 3. solve, refine once, check (sqp.py:175-189)
+  for (int pass = 0; pass < 2; ++pass) {
+    // right-hand side of this pass -> tmp (copy), solution -> sol (pass 0) / res (pass 1)
+    for (int t = warp; t < G * nb; t += nw) {
+      const int s = t / nb, b = t - s * nb;
+      if (!((kmask >> s) & 1u) || !kflag[s]) continue;
+      double* sc = V.scr(s);
+      double* y = sc + (pass == 0 ? L.off_sol : L.off_res) + b * W;
+      const double* src = sc + (pass == 0 ? L.off_rhs : L.off_res) + b * W;
+      if (pass == 0) for (int i = lane; i < W; i += WARP) y[i] = src[i];
+      __syncwarp();
+      kkt_block_forward<NI, NG>(P, b, sc + b * L.msz,
+                                reinterpret_cast<const int*>(sc + L.off_piv) + b * W, y,
+                                sc + L.off_tE + b * nC);
+    }
+    __syncthreads();
+    if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
+      const int s = warp;
+      double* sc = V.scr(s);
+      double* y = sc + (pass == 0 ? L.off_sol : L.off_res) + P.n_D;
+      const double* src = sc + (pass == 0 ? L.off_rhs : L.off_res) + P.n_D;
+      for (int c = lane; c < nC; c += WARP) {
+        double v = src[c];
+        for (int b = 0; b < nb; ++b) v = v + sc[L.off_tE + b * nC + c];
+        y[c] = v;
+      }
+      __syncwarp();
+      warp_lu_solve(sc + L.off_S, L.ldS, nC, reinterpret_cast<const int*>(sc + L.off_pivS), y);
+    }
+    __syncthreads();
+    for (int t = warp; t < G * nb; t += nw) {
+      const int s = t / nb, b = t - s * nb;
+      if (!((kmask >> s) & 1u) || !kflag[s]) continue;
+      double* sc = V.scr(s);
+      double* y = sc + (pass == 0 ? L.off_sol : L.off_res);
+      kkt_block_backward<NI, NG>(P, sc + b * L.msz, y + b * W, y + P.n_D);
+    }
+    __syncthreads();
+    if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
+      const int s = warp;
+      double* sc = V.scr(s);
+      const double* e = V.eb(s, ebi[s]);
+      double* sol = sc + L.off_sol;
+      double* res = sc + L.off_res;
+      const double* rhs = sc + L.off_rhs;
+      bool finite = true;
+      if (pass == 1)
+        for (int i = lane; i < P.nK; i += WARP) sol[i] += res[i];
+      __syncwarp();
+      for (int i = lane; i < P.nK; i += WARP) finite = finite && isfinite(sol[i]);
+      finite = __all_sync(0xffffffffu, finite);
+      if (!finite) {
+        if (lane == 0) kflag[s] = 0;
+      } else {
+        kkt_matvec<NI, NG>(P, e, 0.0, sol, sc + L.off_tmp);
+        double r2 = 0.0, b2 = 0.0;
+        for (int i = lane; i < P.nK; i += WARP) {
+          const double d = rhs[i] - sc[L.off_tmp + i];
+          res[i] = d;
+          r2 = fma(d, d, r2);
+          b2 = fma(rhs[i], rhs[i], b2);
+        }
+        r2 = warp_sum(r2);
+        b2 = warp_sum(b2);
+        __syncwarp();
+        if (pass == 1) {
+          const double rel = sqrt(r2) / fmax(sqrt(b2), 1e-300);
+          if (!(rel <= 1e-10)) {
+            if (lane == 0) kflag[s] = 0;
+          } else {
+            for (int j = lane; j < P.n_D; j += WARP) V.vec(s, 2)[j] = sol[j];
+            for (int c = lane; c < nC; c += WARP) V.vec(s, 3)[c] = sol[P.n_D + c];
+            if (lane == 0) kres[s] = 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // 4. dense fallback (reference semantics incl. the +delta*I retry)
+  if (warp < G && ((kmask >> warp) & 1u) && !kflag[warp]) {
+    const int s = warp;
+    double* work = V.scr(s);
+    double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
+    const int r = warp_kkt<NI, NG>(P, V.eb(s, ebi[s]), work, sol);
+    if (r != 2) {
+      for (int j = lane; j < P.n_D; j += WARP) V.vec(s, 2)[j] = sol[j];
+      for (int c = lane; c < nC; c += WARP) V.vec(s, 3)[c] = sol[P.n_D + c];
+    }
+    if (lane == 0) kres[s] = r;
+  }
+  __syncthreads();
+}
+
 // multiplier_least_squares (driver.py:461-471) for one slot, one warp:
 // argmin || A lam - rhs ||, A = vstack(cjac_b^T) [sum ng x n_C],
 // rhs = -rho_Gamma(lam = 0).  Householder QR (full column rank; a rank-
@@ -642,7 +950,7 @@ __device__ bool warp_lstsq(const Params& P, const double* e, double* work, doubl
 }
 
 // RBF initializer (driver.py:82-90, thin plate spline + linear tail)
-__device__ void warp_rbf(const Params& P, double a, double lm, double* x0, double* work) {
+static __device__ void warp_rbf(const Params& P, double a, double lm, double* x0, double* work) {
   const int lane = threadIdx.x & 31;
   const double q0 = a, q1 = lm;
   const double sp0 = P.rbf_hi[0] > P.rbf_lo[0] ? P.rbf_hi[0] - P.rbf_lo[0] : 1.0;
@@ -679,7 +987,7 @@ __device__ void warp_rbf(const Params& P, double a, double lm, double* x0, doubl
 
 // boundary values (bx, by, c) of assemble() at every sampled row
 // (burgers.py:188-210): ghost points just outside the edges the node touches.
-__device__ void row_bvals(const Params& P, const StRow& rw, double a, double lm, double* out) {
+static __device__ void row_bvals(const Params& P, const StRow& rw, double a, double lm, double* out) {
   const double hx = P.hx, hy = P.hy, nu = P.nu;
   const bool isv = (rw.bflags >> 4) & 1;
   double exl = 0.0, exr = 0.0, eyb = 0.0, eyt = 0.0, u, v;
@@ -696,7 +1004,7 @@ __device__ void row_bvals(const Params& P, const StRow& rw, double a, double lm,
 // the persistent kernel
 
 template <int G, int NI, int NG>
-__global__ void __launch_bounds__(256) k_solve(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P) {
   extern __shared__ __align__(16) double smem[];
   View V(P, smem);
   SlotState* st = V.st();
@@ -708,6 +1016,7 @@ __global__ void __launch_bounds__(256) k_solve(const __grid_constant__ Params P)
   __shared__ unsigned s_mask;
   __shared__ unsigned s_newmask;
   __shared__ unsigned long long s_evals, s_kkts;
+  __shared__ int s_kres[G], s_kflag[G];
   if (tid < G) { st[tid].mu = -1; st[tid].phase = PH_DONE; s_cur[tid] = 0; }
   if (tid == 0) { s_evals = 0; s_kkts = 0; }
   __syncthreads();
@@ -857,35 +1166,36 @@ __global__ void __launch_bounds__(256) k_solve(const __grid_constant__ Params P)
       __syncwarp();
     }
     __syncthreads();
-    // ---- KKT solves (warp per slot) ----
-    if (warp < G && st[warp].need_kkt) {
-      const int s = warp;
-      SlotState& S = st[s];
-      double* e = V.eb(s, s_cur[s]);
-      double* work = V.scr(s);
-      double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
-      const int r = warp_kkt<NI, NG>(P, e, work, sol);
-      if (lane == 0) { S.need_kkt = 0; atomicAdd(&s_kkts, 1ull); }
-      if (r == 2) {
-        if (lane == 0) { S.status = ST_KKT_SINGULAR; S.phase = PH_DONE; }
-      } else {
-        if (lane == 0) S.n_reg += r;
-        double* sv = V.vec(s, 2);
-        double* sl = V.vec(s, 3);
-        const double* x = V.vec(s, 0);
-        const double* lam = V.vec(s, 1);
-        for (int j = lane; j < P.n_D; j += WARP) sv[j] = sol[j];
-        for (int c = lane; c < P.n_C; c += WARP) sl[c] = sol[P.n_D + c];
-        __syncwarp();
-        double* xt = V.vec(s, 4);
-        double* lt = V.vec(s, 5);
-        for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], sv[j]);
-        for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], sl[c]);
-        if (lane == 0) { S.alpha = 1.0; S.n_trials = 0; S.phase = PH_TRIAL; }
+    // ---- KKT solves (block-structured LU across warps, dense fallback) ----
+    {
+      unsigned kmask = 0;
+      for (int s = 0; s < G; ++s) if (st[s].need_kkt) kmask |= 1u << s;
+      if (kmask) {
+        kkt_stage<G, NI, NG>(V, kmask, s_cur, s_kres, s_kflag);
+        if (warp < G && ((kmask >> warp) & 1u)) {
+          const int s = warp;
+          SlotState& S = st[s];
+          const int r = s_kres[s];
+          if (lane == 0) { S.need_kkt = 0; atomicAdd(&s_kkts, 1ull); }
+          if (r == 2) {
+            if (lane == 0) { S.status = ST_KKT_SINGULAR; S.phase = PH_DONE; }
+          } else {
+            if (lane == 0) S.n_reg += r;
+            const double* sv = V.vec(s, 2);
+            const double* sl = V.vec(s, 3);
+            const double* x = V.vec(s, 0);
+            const double* lam = V.vec(s, 1);
+            double* xt = V.vec(s, 4);
+            double* lt = V.vec(s, 5);
+            for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], sv[j]);
+            for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], sl[c]);
+            if (lane == 0) { S.alpha = 1.0; S.n_trials = 0; S.phase = PH_TRIAL; }
+          }
+          __syncwarp();
+        }
+        __syncthreads();
       }
-      __syncwarp();
     }
-    __syncthreads();
     // ---- write results of finished slots ----
     if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) {
       const int s = warp;
@@ -919,7 +1229,7 @@ namespace ddnm {
 // ddnm_eval_batch: one eval_gradients per mu at a given (x, lam), dumping every
 // intermediate, plus (optionally) the KKT step at that point.  mu = CTA*G + s.
 template <int G, int NI, int NG>
-__global__ void __launch_bounds__(256) k_eval(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(512) k_eval(const __grid_constant__ Params P) {
   extern __shared__ __align__(16) double smem[];
   View V(P, smem);
   SlotState* st = V.st();
@@ -965,18 +1275,23 @@ __global__ void __launch_bounds__(256) k_eval(const __grid_constant__ Params P) 
       if (o.merit) o.merit[mu] = e[P.eb_scal];
       if (o.objective) o.objective[mu] = e[P.eb_scal + 1];
     }
-    if (P.eval_step) {
-      double* work = V.scr(s);
-      double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
-      const int r = warp_kkt<NI, NG>(P, e, work, sol);
-      if (o.step) for (int j = lane; j < P.nK; j += WARP) o.step[mu * P.nK + j] = sol[j];
-      if (lane == 0 && o.kkt_status) o.kkt_status[mu] = r;
+  }
+  if (P.eval_step) {
+    __shared__ int s_kres[G], s_kflag[G];
+    __syncthreads();
+    kkt_stage<G, NI, NG>(V, mask, s_ebi, s_kres, s_kflag);
+    if (warp < G && ((mask >> warp) & 1u)) {
+      const int s = warp;
+      const size_t mu = (size_t)st[s].mu;
+      const EvalOut& o = P.eo;
+      if (o.step) {
+        for (int j = lane; j < P.n_D; j += WARP) o.step[mu * P.nK + j] = V.vec(s, 2)[j];
+        for (int c = lane; c < P.n_C; c += WARP) o.step[mu * P.nK + P.n_D + c] = V.vec(s, 3)[c];
+      }
+      if (lane == 0 && o.kkt_status) o.kkt_status[mu] = s_kres[s];
     }
   }
 }
 
-__global__ void k_fill(double* p, size_t n, double v) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
-}
 
 }  // namespace ddnm

@@ -1,0 +1,12 @@
+// Kernel specialisations for latent dims (n_int, n_gam) = (20, 8).
+#include <vector>
+
+#include "ddnm_registry.h"
+#include "ddnm_solve.cuh"
+
+namespace ddnm {
+void register_20_8(std::vector<KernelEntry>& t) {
+  t.push_back(KernelEntry{20, 8, 1, (const void*)&k_solve<1, 20, 8>,
+                          (const void*)&k_eval<1, 20, 8>});
+}
+}  // namespace ddnm
