@@ -177,7 +177,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     inst = P.RomInstance.load(ARTIFACT)
-    ctx = inst.context(local)
+    ctx = inst.context(local, args.slots)
     info = ctx.info
     cfg = P.SqpConfig()
     B = BATCH
@@ -253,7 +253,7 @@ def run_gpu(args):
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        res = P.solve_rom_batch(inst, mu_h, cfg)
+        res = P.solve_rom_batch(inst, mu_h, cfg, slots=args.slots)
         e2e_vals.append(time.perf_counter() - t0)
     e2e_t = float(np.mean(e2e_vals[1:])) if len(e2e_vals) > 1 else e2e_vals[0]
     if dist:
@@ -319,6 +319,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slots", type=int, default=0, help="mu slots per CTA (0 = largest that fits)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -216,6 +216,12 @@ int ddnm_eval_batch(ddnm_ctx* ctx, int32_t B, const double* mu,
  * evaluations and KKT solves executed. */
 int ddnm_last_counters(const ddnm_ctx* ctx, int64_t* evals, int64_t* kkts);
 
+/* Device-side phase profile of the last solve when the environment variable
+ * DDNM_PROF is set (SM clock cycles summed over CTAs, thread 0 of each CTA):
+ * [0] slot fetch, [1..4] eval phases A-D, [5] slot init, [6] SQP state
+ * machine, [7] KKT, [8..15] reserved.  All zero when profiling is off. */
+int ddnm_last_profile(const ddnm_ctx* ctx, uint64_t* cycles16);
+
 #ifdef __cplusplus
 }
 #endif

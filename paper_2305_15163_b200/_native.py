@@ -116,6 +116,7 @@ def lib():
     L.ddnm_eval_batch.argtypes = [C.c_void_p, C.c_int32, _dp, _dp, _dp, C.c_double,
                                   C.POINTER(EvalOut)]
     L.ddnm_last_counters.argtypes = [C.c_void_p, _lp, _lp]
+    L.ddnm_last_profile.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
     if L.ddnm_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libddnm.so ABI version mismatch; rebuild")
     _lib = L
@@ -124,7 +125,7 @@ def lib():
 
 EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_destroy",
             "ddnm_ctx_info", "ddnm_solve_batch", "ddnm_solve_batch_device",
-            "ddnm_eval_batch", "ddnm_last_counters")
+            "ddnm_eval_batch", "ddnm_last_counters", "ddnm_last_profile")
 
 
 def check(rc: int):

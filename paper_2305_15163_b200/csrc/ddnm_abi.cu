@@ -5,6 +5,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -82,10 +83,12 @@ struct ddnm_ctx {
   cudaStream_t stream = nullptr;
   std::vector<void*> allocs;  // weights, tables
   double* gbv = nullptr;      // boundary values per global slot
+  double* gJ = nullptr;       // interior Jacobian rows per global slot
   size_t gbv_slots = 0;
   int* work = nullptr;
   unsigned long long* counters = nullptr;
   unsigned long long last_counters[2] = {0, 0};
+  unsigned long long* prof = nullptr;   // device-side phase profiler (env DDNM_PROF=1)
   // host-API staging buffers
   std::map<std::string, std::pair<void*, size_t>> io;
 };
@@ -127,8 +130,13 @@ int io_buf(ddnm_ctx* c, const std::string& name, size_t bytes, void** p) {
   return 0;
 }
 
-// RestrictedResidual rows (partition.py:361-425) in local-column form.
-int build_stencil(const ddnm_artifacts* a, const ddnm_block& blk, std::vector<StRow>& out) {
+// RestrictedResidual rows (partition.py:361-425) in local-column form, SoA.
+struct HostRows {
+  std::vector<int> gu, gv, nent, bflags, col;
+  std::vector<double> bxc, byc, cdc, xc, yc;
+};
+
+int build_stencil(const ddnm_artifacts* a, const ddnm_block& blk, HostRows& out) {
   const int nx = a->nx, ny = a->ny;
   const int n = nx * ny;
   const double hx = 2.0 / (nx + 1), hy = 0.05 / (ny + 1), nu = a->nu;
@@ -140,8 +148,13 @@ int build_stencil(const ddnm_artifacts* a, const ddnm_block& blk, std::vector<St
     if (c < 0 || c >= 2 * (int64_t)n) return fail(DDNM_EINVAL, "column index out of range");
     lookup[c] = k;
   }
-  out.resize(blk.n_rows);
-  for (int r = 0; r < blk.n_rows; ++r) {
+  const int nr = blk.n_rows;
+  out.gu.assign(nr, 0); out.gv.assign(nr, 0); out.nent.assign(nr, 0); out.bflags.assign(nr, 0);
+  out.col.assign((size_t)MAXE * nr, 0);
+  out.bxc.assign((size_t)MAXE * nr, 0.0); out.byc.assign((size_t)MAXE * nr, 0.0);
+  out.cdc.assign((size_t)MAXE * nr, 0.0);
+  out.xc.assign(nr, 0.0); out.yc.assign(nr, 0.0);
+  for (int r = 0; r < nr; ++r) {
     const int64_t gr = blk.res_rows[r];
     if (gr < 0 || gr >= 2 * (int64_t)n) return fail(DDNM_EINVAL, "residual row out of range");
     const bool isv = gr >= n;
@@ -162,28 +175,27 @@ int build_stencil(const ddnm_artifacts* a, const ddnm_block& blk, std::vector<St
     if (j < ny - 1) add(off + p + nx, 2, dy * 1.0);
     ent[isv ? p : n + p];  // cross-component diagonal (E_u / E_v)
     if ((int)ent.size() > MAXE) return fail(DDNM_EINVAL, "stencil row wider than 6");
-    StRow& row = out[r];
-    std::memset(&row, 0, sizeof(row));
-    row.gu = lookup[p];
-    row.gv = lookup[n + p];
-    if (row.gu < 0 || row.gv < 0)
+    out.gu[r] = lookup[p];
+    out.gv[r] = lookup[n + p];
+    if (out.gu[r] < 0 || out.gv[r] < 0)
       return fail(DDNM_EINVAL, "diagonal coupling column missing from the provided column set");
     int e = 0;
     for (auto& kv : ent) {
       const int lc = lookup[kv.first];
       if (lc < 0)
         return fail(DDNM_EINVAL, "restricted rows reference columns outside the provided column set");
-      row.col[e] = lc;
-      row.bxc[e] = kv.second[0];
-      row.byc[e] = kv.second[1];
-      row.cdc[e] = kv.second[2];
+      out.col[(size_t)e * nr + r] = lc;
+      out.bxc[(size_t)e * nr + r] = kv.second[0];
+      out.byc[(size_t)e * nr + r] = kv.second[1];
+      out.cdc[(size_t)e * nr + r] = kv.second[2];
       ++e;
     }
-    row.nent = e;
-    row.bflags = (i == 0 ? 1 : 0) | (i == nx - 1 ? 2 : 0) | (j == 0 ? 4 : 0) |
-                 (j == ny - 1 ? 8 : 0) | (isv ? 16 : 0);
-    row.xc = -1.0 + hx * (i + 1);
-    row.yc = hy * (j + 1);
+    for (; e < MAXE; ++e) out.col[(size_t)e * nr + r] = out.gu[r];
+    out.nent[r] = (int)ent.size();
+    out.bflags[r] = (i == 0 ? 1 : 0) | (i == nx - 1 ? 2 : 0) | (j == 0 ? 4 : 0) |
+                    (j == ny - 1 ? 8 : 0) | (isv ? 16 : 0);
+    out.xc[r] = -1.0 + hx * (i + 1);
+    out.yc[r] = hy * (j + 1);
   }
   return 0;
 }
@@ -217,7 +229,11 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
   int rc;
   if (kind == DDNM_MAP_AUTOENCODER) {
     const size_t nnz = (size_t)h.indptr[h.n_out];
-    if ((rc = upload(c, h.W1, (size_t)h.n_hidden * lat, const_cast<double**>(&d.W1)))) return rc;
+    std::vector<double> w1t((size_t)h.n_hidden * lat);
+    for (int k = 0; k < h.n_hidden; ++k)
+      for (int dd = 0; dd < lat; ++dd) w1t[(size_t)dd * h.n_hidden + k] = h.W1[(size_t)k * lat + dd];
+    if ((rc = upload(c, w1t.data(), w1t.size(), const_cast<double**>(&d.W1t)))) return rc;
+    d.W1 = nullptr;
     if ((rc = upload(c, h.b1, (size_t)h.n_hidden, const_cast<double**>(&d.b1)))) return rc;
     if ((rc = upload_i32(c, h.indptr, (size_t)h.n_out + 1, const_cast<int**>(&d.indptr)))) return rc;
     if ((rc = upload_i32(c, h.indices, nnz, const_cast<int**>(&d.indices)))) return rc;
@@ -227,7 +243,7 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
     // ELL-transposed copy of W2 for the sweep (storage order kept per row)
     int64_t wmax = 0;
     for (int o = 0; o < h.n_out; ++o) wmax = std::max<int64_t>(wmax, h.indptr[o + 1] - h.indptr[o]);
-    const int ew = (int)((wmax + 3) / 4 * 4);
+    const int ew = (int)((wmax + 7) / 8 * 8);
     std::vector<double> ev((size_t)ew * h.n_out, 0.0);
     std::vector<int> ek((size_t)ew * h.n_out, 0);
     for (int o = 0; o < h.n_out; ++o)
@@ -237,12 +253,27 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
         ek[slot] = (int)h.indices[e];
       }
     d.ell_w = ew;
+    // contiguous windows (banded masks, autoencoder.py:76-96): index = k0 + e
+    bool contig = true;
+    std::vector<int> k0(h.n_out, 0);
+    for (int o = 0; o < h.n_out && contig; ++o) {
+      if (h.indptr[o + 1] > h.indptr[o]) k0[o] = (int)h.indices[h.indptr[o]];
+      for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e)
+        if (h.indices[e] != k0[o] + (e - h.indptr[o])) { contig = false; break; }
+    }
+    d.ell_k = nullptr;
+    d.ell_k0 = nullptr;
     if (ew > 0) {
       if ((rc = upload(c, ev.data(), ev.size(), const_cast<double**>(&d.ell_v)))) return rc;
-      if ((rc = upload(c, ek.data(), ek.size(), const_cast<int**>(&d.ell_k)))) return rc;
+      if (contig) {
+        if ((rc = upload(c, k0.data(), k0.size(), const_cast<int**>(&d.ell_k0)))) return rc;
+      } else {
+        if ((rc = upload(c, ek.data(), ek.size(), const_cast<int**>(&d.ell_k)))) return rc;
+      }
     }
   } else {
     if ((rc = upload(c, h.W1, (size_t)h.n_out * lat, const_cast<double**>(&d.W1)))) return rc;
+    d.W1t = nullptr;
     d.b1 = nullptr; d.indptr = nullptr; d.indices = nullptr; d.data = nullptr;
     d.scale = nullptr; d.shift = nullptr;
   }
@@ -326,14 +357,25 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     B.cjac_off = cjoff; B.intJ_off = ijoff; B.gamJ_off = gjoff; B.eb_off = eboff;
     if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, B.in))) return bail(rc);
     if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, B.ga))) return bail(rc);
-    std::vector<StRow> rows;
-    if ((rc = build_stencil(a, k, rows))) return bail(rc);
-    if ((rc = upload(c, rows.data(), rows.size(), const_cast<StRow**>(&B.rows)))) return bail(rc);
+    HostRows hr;
+    if ((rc = build_stencil(a, k, hr))) return bail(rc);
+    StRows& R = B.rows;
+    if ((rc = upload(c, hr.gu.data(), hr.gu.size(), const_cast<int**>(&R.gu))) ||
+        (rc = upload(c, hr.gv.data(), hr.gv.size(), const_cast<int**>(&R.gv))) ||
+        (rc = upload(c, hr.nent.data(), hr.nent.size(), const_cast<int**>(&R.nent))) ||
+        (rc = upload(c, hr.bflags.data(), hr.bflags.size(), const_cast<int**>(&R.bflags))) ||
+        (rc = upload(c, hr.col.data(), hr.col.size(), const_cast<int**>(&R.col))) ||
+        (rc = upload(c, hr.bxc.data(), hr.bxc.size(), const_cast<double**>(&R.bxc))) ||
+        (rc = upload(c, hr.byc.data(), hr.byc.size(), const_cast<double**>(&R.byc))) ||
+        (rc = upload(c, hr.cdc.data(), hr.cdc.size(), const_cast<double**>(&R.cdc))) ||
+        (rc = upload(c, hr.xc.data(), hr.xc.size(), const_cast<double**>(&R.xc))) ||
+        (rc = upload(c, hr.yc.data(), hr.yc.size(), const_cast<double**>(&R.yc))))
+      return bail(rc);
     if ((rc = upload_i32(c, k.gio, (size_t)k.n_gio, const_cast<int**>(&B.gio)))) return bail(rc);
     if ((rc = upload(c, k.CA, (size_t)P.n_C * k.interface.n_out, const_cast<double**>(&B.CA)))) return bail(rc);
     xoff += W; row_off += k.n_rows; iout += k.n_io; gout += k.interface.n_out;
     Roff += k.n_rows * W; cjoff += P.n_C * ng; ijoff += k.n_io * ni; gjoff += k.interface.n_out * ng;
-    eboff += W * W + W + P.n_C + P.n_C * ng + 1;
+    eboff += W * (W + 1) / 2 + W + P.n_C + P.n_C * ng + 1;
     max_nh = std::max(max_nh, B.in.n_hidden + B.ga.n_hidden);
     max_io = std::max(max_io, k.n_io);
     max_gam = std::max(max_gam, k.interface.n_out);
@@ -363,15 +405,28 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   }
   // shared-memory plan (doubles)
   const bool ae = a->map_kind == DDNM_MAP_AUTOENCODER;
-  int scr = 0;
-  P.scr_sig = scr; scr += ae ? max_nh : 0;
-  P.scr_dsig = scr; scr += ae ? max_nh : 0;
-  P.scr_gint = scr; scr += max_io;
-  P.scr_jint = scr; scr += ae ? max_io * ni : 0;
-  P.scr_ggam = scr; scr += max_gam;
-  P.scr_jgam = scr; scr += ae ? max_gam * ng : 0;
-  P.scr_R = scr; scr += max_rows * W;
-  P.scr_r = scr; scr += max_rows;
+  // per-slot scratch plan; the interior Jacobian rows stay in shared memory
+  // when they fit, otherwise they go to a per-slot L2 scratch (gJ)
+  auto plan_scratch = [&](bool jint_smem) {
+    int scr = 0;
+    P.scr_sig = scr; scr += ae ? max_nh : 0;
+    P.scr_dsig = scr; scr += ae ? max_nh : 0;
+    P.scr_gint = scr; scr += max_io;
+    if (ae && jint_smem) { P.scr_jint = scr; scr += max_io * ni; } else { P.scr_jint = -1; }
+    P.scr_ggam = scr; scr += max_gam;
+    P.scr_jgam = scr; scr += ae ? max_gam * ng : 0;
+    // R and r are produced after the sweep has consumed sigma/sigma': alias them
+    if (ae && max_rows * (W + 1) <= 2 * max_nh) {
+      P.scr_R = P.scr_sig;
+      P.scr_r = P.scr_sig + max_rows * W;
+    } else {
+      P.scr_R = scr; scr += max_rows * W;
+      P.scr_r = scr; scr += max_rows;
+    }
+    return scr;
+  };
+  int scr = plan_scratch(true);
+  P.gJ_stride = ae ? max_io * ni : 0;
   const int kkt_need = std::max(P.nK * (P.nK + 1) + 5 * P.nK,
                                 P.nb * (W + P.n_C) * (W + P.n_C + 1) + P.nb * W +
                                     P.n_C * (P.n_C + 1) + P.n_C + P.nb * P.n_C + 4 * P.nK);
@@ -383,18 +438,29 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.eb_rho = eboff; P.eb_con = eboff + P.n_D; P.eb_scal = eboff + P.n_D + P.n_C;
   P.eb_size = (P.eb_size + 1) & ~1;
   const int state_d = (int)((sizeof(SlotState) + 7) / 8);
-  // pick G: the largest compiled G whose footprint fits 227 KB
+  // pick G (slots per CTA): the largest compiled G whose footprint fits,
+  // preferring the interior Jacobian rows in shared memory
   const size_t smem_cap = (size_t)prop.sharedMemPerBlockOptin - 1024;
-  auto footprint = [&](int G) {
-    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + P.scr_size)) * 8;
+  const int rbf_need2 = rbf_need;
+  auto scr_total = [&](bool jsm) {
+    int s0 = plan_scratch(jsm);
+    int t = std::max(std::max(s0, kkt_need), std::max(ls_need, rbf_need2));
+    return (t + 1) & ~1;
+  };
+  auto footprint = [&](int G, bool jsm) {
+    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + scr_total(jsm))) * 8;
   };
   const Kernels* kern = nullptr;
-  for (const auto& k : kernel_table()) {
-    if (k.ni != ni || k.ng != ng) continue;
-    if (slots > 0 && k.g != slots) continue;
-    if (footprint(k.g) > smem_cap) continue;
-    if (!kern || k.g > kern->g) kern = &k;
-    if (slots <= 0 && kern->g >= 2) break;
+  bool kern_jsm = true;
+  for (int pass = 0; pass < 2 && !kern; ++pass) {
+    const bool jsm = pass == 0;
+    if (!jsm && !ae) break;
+    for (const auto& k : kernel_table()) {
+      if (k.ni != ni || k.ng != ng) continue;
+      if (slots > 0 && k.g != slots) continue;
+      if (footprint(k.g, jsm) > smem_cap) continue;
+      if (!kern || k.g > kern->g) { kern = &k; kern_jsm = jsm; }
+    }
   }
   if (!kern) {
     char buf[160];
@@ -402,13 +468,14 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
              ni, ng, slots, smem_cap);
     return bail(fail(DDNM_EUNSUPPORTED, buf));
   }
+  P.scr_size = scr_total(kern_jsm);
   c->K = *kern;
   P.G = kern->g;
   P.sm_state = 0;
   P.sm_vec = state_d * P.G;
   P.sm_eb = P.sm_vec + P.G * 8 * P.nK;
   P.sm_scr = P.sm_eb + P.G * 2 * P.eb_size;
-  c->smem = footprint(P.G);
+  c->smem = footprint(P.G, kern_jsm);
   if (cudaFuncSetAttribute(kern->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
       cudaFuncSetAttribute(kern->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cannot reserve dynamic shared memory"));
@@ -430,8 +497,10 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   for (auto& kv : c->io) cudaFree(kv.second.first);
   if (c->gbv) cudaFree(c->gbv);
+  if (c->gJ) cudaFree(c->gJ);
   if (c->work) cudaFree(c->work);
   if (c->counters) cudaFree(c->counters);
+  if (c->prof) cudaFree(c->prof);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -459,8 +528,12 @@ int ddnm_ctx_info(const ddnm_ctx* c, ddnm_info* i) {
 static int ensure_gbv(ddnm_ctx* c, size_t slots) {
   if (c->gbv_slots >= slots) return 0;
   if (c->gbv) cudaFree(c->gbv);
+  if (c->gJ) cudaFree(c->gJ);
   c->gbv = nullptr;
-  CUDA_TRY(cudaMalloc(&c->gbv, std::max<size_t>(slots, 1) * c->tot_rows * 3 * sizeof(double)));
+  c->gJ = nullptr;
+  slots = std::max<size_t>(slots, 1);
+  CUDA_TRY(cudaMalloc(&c->gbv, slots * c->tot_rows * 3 * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&c->gJ, slots * std::max(c->P.gJ_stride, 1) * sizeof(double)));
   c->gbv_slots = slots;
   return 0;
 }
@@ -503,8 +576,15 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
   P.so.x0 = o->x0; P.so.lam0 = o->lam0;
   P.so.n_iter = o->n_iter; P.so.n_evals = o->n_evals; P.so.status = o->status; P.so.n_reg = o->n_reg;
   P.gbv = c->gbv;
+  P.gJ = c->gJ;
   P.work = c->work;
   P.counters = c->counters;
+  P.prof = nullptr;
+  if (getenv("DDNM_PROF")) {
+    if (!c->prof) CUDA_TRY(cudaMalloc(&c->prof, 16 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(c->prof, 0, 16 * sizeof(unsigned long long), s));
+    P.prof = c->prof;
+  }
   if ((rc = fill_nan(s, o->merit_hist, (size_t)B * (cfg->max_iter + 1)))) return rc;
   if ((rc = fill_nan(s, o->obj_hist, (size_t)B * (cfg->max_iter + 1)))) return rc;
   if ((rc = fill_nan(s, o->alpha_hist, (size_t)B * cfg->max_iter))) return rc;
@@ -512,6 +592,13 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(unsigned long long), s));
   void* args[] = {&P};
   CUDA_TRY(cudaLaunchKernel(c->K.solve, dim3(ctas), dim3(c->threads), args, c->smem, s));
+  return 0;
+}
+
+extern "C" int ddnm_last_profile(const ddnm_ctx* c, uint64_t* cycles16) {
+  if (!c || !cycles16) return fail(DDNM_EINVAL, "null argument");
+  if (!c->prof) { for (int i = 0; i < 16; ++i) cycles16[i] = 0; return 0; }
+  CUDA_TRY(cudaMemcpy(cycles16, c->prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   return 0;
 }
 
@@ -627,6 +714,7 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
   P.eval_mode = 1;
   P.eval_step = (o->step || o->kkt_status) ? 1 : 0;
   P.gbv = c->gbv;
+  P.gJ = c->gJ;
   P.work = c->work;
   P.counters = c->counters;
   void* args[] = {&P};

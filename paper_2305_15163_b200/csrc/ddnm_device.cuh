@@ -37,29 +37,36 @@ enum Status { ST_OK = 0, ST_LINE_SEARCH = 1, ST_KKT_SINGULAR = 2, ST_LSTSQ_RANK 
 
 struct DecDev {
   int n_out, n_hidden;
-  const double* W1;       // AE: [n_hidden][lat]; LINEAR: Phi [n_out][lat]
+  const double* W1;       // LINEAR: Phi [n_out][lat]  (AE: unused on device)
+  const double* W1t;      // AE: W1 transposed [lat][n_hidden] (coalesced per latent column)
   const double* b1;       // [n_hidden]
   const int* indptr;      // [n_out+1]
   const int* indices;     // [nnz]
   const double* data;     // [nnz]
   const double* scale;    // [n_out]
   const double* shift;    // [n_out]
-  int ell_w;              // ELL width (max nnz per row, padded to 4)
+  int ell_w;              // ELL width (max nnz per row, padded to 8)
   const double* ell_v;    // [ell_w][n_out] W2 values in storage order, 0-padded
-  const int* ell_k;       // [ell_w][n_out] hidden indices, 0-padded
+  const int* ell_k;       // [ell_w][n_out] hidden indices, 0-padded (null if contiguous)
+  const int* ell_k0;      // [n_out] first hidden index when every row's window is contiguous
 };
 
-// One sampled residual row in local-column form (RestrictedResidual,
-// partition.py:372-425).  Entries are sorted by global column, which is the
-// storage order of the reference's Bx/By/Cdiff rows, so the per-operator sums
-// accumulate in the reference order.
-struct StRow {
-  int gu, gv;             // local positions of u_p and v_p
-  int nent;               // distinct local columns referenced (<= 6)
-  int bflags;             // bit0 left, bit1 right, bit2 bottom, bit3 top, bit4 v-row
-  int col[MAXE];
-  double bxc[MAXE], byc[MAXE], cdc[MAXE];
-  double xc, yc;          // node coordinates (ghost points share one of them)
+// Sampled residual rows in local-column form (RestrictedResidual,
+// partition.py:372-425), structure of arrays so consecutive rows (lanes) read
+// consecutive addresses.  Entry e of row r is at [e * n_rows + r]; entries are
+// sorted by global column, the storage order of the reference's Bx/By/Cdiff
+// rows, so the per-operator sums accumulate in the reference order.
+struct StRows {
+  const int* gu;          // local position of u_p
+  const int* gv;          // local position of v_p
+  const int* nent;        // distinct local columns referenced (<= 6)
+  const int* bflags;      // bit0 left, bit1 right, bit2 bottom, bit3 top, bit4 v-row
+  const int* col;         // [MAXE][n_rows]
+  const double* bxc;      // [MAXE][n_rows]
+  const double* byc;
+  const double* cdc;
+  const double* xc;       // node coordinates (ghost points share one of them)
+  const double* yc;
 };
 
 struct BlockDev {
@@ -70,7 +77,7 @@ struct BlockDev {
   int iout_off, gout_off, R_off, cjac_off, intJ_off, gamJ_off;
   int eb_off;             // offset of this block inside a slot eval buffer
   DecDev in, ga;
-  const StRow* rows;
+  StRows rows;
   const int* gio;
   const double* CA;       // [n_c][ga.n_out]
 };
@@ -126,8 +133,11 @@ struct Params {
   int eval_mode;          // 1: single eval with dumps (ddnm_eval_batch)
   int eval_step;          // eval mode: also solve the KKT
   double* gbv;            // per global slot [total_rows][3] boundary values
+  double* gJ;             // per global slot interior-decoder Jacobian rows [n_io][n_int]
+  int gJ_stride;
   int* work;              // [0]: next mu; [1]: finished CTAs
   unsigned long long* counters;  // [0] block-evals, [1] KKT solves
+  unsigned long long* prof;      // [15] per-phase clock totals (DDNM_PROF=1), or null
 };
 
 struct SlotState {
@@ -139,16 +149,58 @@ struct SlotState {
 // ---------------------------------------------------------------------------
 // scalar helpers
 
-__device__ __forceinline__ double expit_d(double z) {
-  // scipy.special.expit: 1 / (1 + exp(-x))
-  return 1.0 / (1.0 + exp(-z));
+// 2^(j/32), j = 0..31 (correctly rounded)
+static __device__ const double k_exp2_32[32] = {
+    0x1.0000000000000p+0, 0x1.059b0d3158574p+0, 0x1.0b5586cf9890fp+0, 0x1.11301d0125b51p+0,
+    0x1.172b83c7d517bp+0, 0x1.1d4873168b9aap+0, 0x1.2387a6e756238p+0, 0x1.29e9df51fdee1p+0,
+    0x1.306fe0a31b715p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123422p+0, 0x1.44e086061892dp+0,
+    0x1.4bfdad5362a27p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd485429p+0, 0x1.6247eb03a5585p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0,
+    0x1.8ace5422aa0dbp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f090p+0, 0x1.a5503b23e255dp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529cp+0, 0x1.cb720dcef9069p+0,
+    0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0};
+
+// exp(x) for |x| <= 700: x = (32 m + j) ln2/32 + r, |r| <= ln2/64,
+// exp(x) = 2^m 2^(j/32) (1 + p(r)), p degree 6 (truncation < 4e-18).
+// 11 FP64 ops + integer exponent arithmetic (vs ~23 for the libdevice exp).
+__device__ __forceinline__ double exp_fast(double x, const double* tab) {
+  const double t = fma(x, 0x1.71547652b82fep+5, 6755399441055744.0);  // 32/ln2, 1.5*2^52
+  const int n = __double2loint(t);
+  const double nd = t - 6755399441055744.0;
+  double r = fma(nd, -0x1.62e42fee00000p-6, x);                       // ln2/32 (hi, 32 bits)
+  r = fma(nd, -0x1.a39ef35793c76p-38, r);                             // ln2/32 (lo)
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = p * r;                                                          // exp(r) - 1
+  const double T = __ldg(tab + (n & 31));
+  const double y = fma(T, p, T);
+  return __hiloint2double(__double2hiint(y) + ((n >> 5) << 20), __double2loint(y));
 }
 
-__device__ __forceinline__ void act_pair(int act, double z, double& a, double& da) {
-  const double s = expit_d(z);
+__device__ __forceinline__ double rcp_fast(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+
+// scipy.special.expit(z) = 1 / (1 + exp(-z)); |z| clamped at 700 (the
+// results are exactly 1 or below 1e-304 there anyway)
+__device__ __forceinline__ double expit_fast(double z, const double* tab) {
+  const double x = fmin(fmax(-z, -700.0), 700.0);
+  return rcp_fast(1.0 + exp_fast(x, tab));
+}
+
+__device__ __forceinline__ void act_pair(int act, double z, double& a, double& da, const double* tab) {
+  const double s = expit_fast(z, tab);
   if (act == ACT_SWISH) {
-    a = z * s;
-    da = s * (1.0 + z * (1.0 - s));
+    a = z * s;                                   // autoencoder.py:33
+    da = s * fma(z, 1.0 - s, 1.0);               // autoencoder.py:42
   } else {
     a = s;
     da = s * (1.0 - s);

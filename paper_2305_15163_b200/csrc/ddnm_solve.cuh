@@ -10,7 +10,10 @@ namespace ddnm {
 struct View {
   const Params& P;
   double* sm;
-  __device__ View(const Params& p, double* s) : P(p), sm(s) {}
+  int gslot0;  // global index of this CTA's slot 0 (per-slot global scratch)
+  unsigned long long* prof;  // per-phase clock totals (thread 0), or null
+  __device__ View(const Params& p, double* s)
+      : P(p), sm(s), gslot0(blockIdx.x * p.G), prof(nullptr) {}
   __device__ SlotState* st() const { return reinterpret_cast<SlotState*>(sm + P.sm_state); }
   // vectors: 0 x, 1 lam, 2 s, 3 slam, 4 xt, 5 lt, 6 best x, 7 best lam
   __device__ double* vec(int s, int which) const { return sm + P.sm_vec + (s * 8 + which) * P.nK; }
@@ -18,16 +21,33 @@ struct View {
   __device__ double* scr(int s) const { return sm + P.sm_scr + s * P.scr_size; }
 };
 
+// phase timing (device-side profiler, off unless Params::prof is set)
+#define DDNM_MARK(V, i)                                      \
+  do {                                                       \
+    if ((V).prof && threadIdx.x == 0) {                      \
+      const unsigned long long t_ = clock64();               \
+      (V).prof[i] += t_ - (V).prof[15];                      \
+      (V).prof[15] = t_;                                     \
+    }                                                        \
+  } while (0)
+
 // block pieces inside an eval buffer
+__device__ __forceinline__ int tri_n(int w) { return w * (w + 1) / 2; }
 __device__ __forceinline__ double* eb_H(double* e, const BlockDev& B) { return e + B.eb_off; }
-__device__ __forceinline__ double* eb_proj(double* e, const BlockDev& B) { return e + B.eb_off + B.w * B.w; }
-__device__ __forceinline__ double* eb_cval(double* e, const BlockDev& B) { return e + B.eb_off + B.w * B.w + B.w; }
+__device__ __forceinline__ double* eb_proj(double* e, const BlockDev& B) { return e + B.eb_off + tri_n(B.w); }
+__device__ __forceinline__ double* eb_cval(double* e, const BlockDev& B) { return e + B.eb_off + tri_n(B.w) + B.w; }
 __device__ __forceinline__ double* eb_cjac(double* e, const BlockDev& B, int nC) {
-  return e + B.eb_off + B.w * B.w + B.w + nC;
+  return e + B.eb_off + tri_n(B.w) + B.w + nC;
 }
 __device__ __forceinline__ double* eb_rr(double* e, const BlockDev& B, int nC) {
-  return e + B.eb_off + B.w * B.w + B.w + nC + nC * B.ng;
+  return e + B.eb_off + tri_n(B.w) + B.w + nC + nC * B.ng;
 }
+// packed upper triangle of the symmetric Gram block H = R^T R
+__device__ __forceinline__ int tri_idx(int w, int i, int j) {
+  if (i > j) { const int t = i; i = j; j = t; }
+  return i * w - (i * (i - 1)) / 2 + (j - i);
+}
+__device__ __forceinline__ double hval(const double* H, int w, int i, int j) { return H[tri_idx(w, i, j)]; }
 
 // --------------------------------------------------------------------------
 // phase A: one hidden unit for all active slots.
@@ -38,7 +58,7 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
                                             int sig_off, unsigned mask) {
   double w[L];
 #pragma unroll
-  for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1 + (size_t)k * L + d);
+  for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1t + (size_t)d * D.n_hidden + k);
   const double b = __ldg(D.b1 + k);
 #pragma unroll
   for (int s = 0; s < G; ++s) {
@@ -46,9 +66,9 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
     const double* x = V.vec(s, 4) + xo;
     double z = b;
 #pragma unroll
-    for (int d = 0; d < L; ++d) z = __dadd_rn(z, __dmul_rn(w[d], x[d]));
+    for (int d = 0; d < L; ++d) z = fma(w[d], x[d], z);
     double a, da;
-    act_pair(V.P.act, z, a, da);
+    act_pair(V.P.act, z, a, da, k_exp2_32);
     double* sc = V.scr(s);
     sc[V.P.scr_sig + sig_off + k] = a;
     sc[V.P.scr_dsig + sig_off + k] = da;
@@ -63,8 +83,8 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
 //   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e W2_e act'_e W1[k_e, d]) * scale
 template <int G, int L>
 __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int sig_off,
-                                             int g_off, int j_off, unsigned mask) {
-  constexpr int U = 4;
+                                             int g_off, int j_off, unsigned mask, bool jglobal) {
+  constexpr int U = 8;
   double ag[G], aj[G][L];
 #pragma unroll
   for (int s = 0; s < G; ++s) {
@@ -79,29 +99,34 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
     sig[s] = V.scr(s) + V.P.scr_sig + sig_off;
     dsig[s] = V.scr(s) + V.P.scr_dsig + sig_off;
   }
-  const int n = D.n_out;
+  const int n = D.n_out, nh = D.n_hidden;
+  // banded masks give contiguous hidden windows: entry e of output o is hidden
+  // unit k0[o] + e (checked on the host; otherwise explicit indices)
+  const int k0 = D.ell_k0 ? __ldg(D.ell_k0 + o) : 0;
   for (int e = 0; e < D.ell_w; e += U) {
-    double v[U], w[U][L];
+    double v[U], t[U][G];
     int k[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       v[u] = __ldg(D.ell_v + (size_t)(e + u) * n + o);
-      k[u] = __ldg(D.ell_k + (size_t)(e + u) * n + o);
+      k[u] = D.ell_k0 ? min(k0 + e + u, nh - 1) : __ldg(D.ell_k + (size_t)(e + u) * n + o);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int d = 0; d < L; ++d) w[u][d] = __ldg(D.W1 + (size_t)k[u] * L + d);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
       for (int s = 0; s < G; ++s) {
-        if (!((mask >> s) & 1u)) continue;
-        const double a = sig[s][k[u]];
-        const double t = v[u] * dsig[s][k[u]];
-        ag[s] = fma(v[u], a, ag[s]);
+        if (!((mask >> s) & 1u)) { t[u][s] = 0.0; continue; }
+        ag[s] = fma(v[u], sig[s][k[u]], ag[s]);
+        t[u][s] = v[u] * dsig[s][k[u]];
+      }
 #pragma unroll
-        for (int d = 0; d < L; ++d) aj[s][d] = fma(t, w[u][d], aj[s][d]);
+    for (int d = 0; d < L; ++d) {
+      const double* w1 = D.W1t + (size_t)d * nh;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double w = __ldg(w1 + k[u]);
+#pragma unroll
+        for (int s = 0; s < G; ++s) aj[s][d] = fma(t[u][s], w, aj[s][d]);
       }
     }
   }
@@ -111,8 +136,10 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
     if (!((mask >> s) & 1u)) continue;
     double* sc = V.scr(s);
     sc[g_off + o] = __dadd_rn(__dmul_rn(ag[s], scl), sh);
+    double* jr = jglobal ? V.P.gJ + (size_t)(V.gslot0 + s) * V.P.gJ_stride + (size_t)o * L
+                         : sc + j_off + o * L;
 #pragma unroll
-    for (int d = 0; d < L; ++d) sc[j_off + o * L + d] = aj[s][d] * scl;
+    for (int d = 0; d < L; ++d) jr[d] = aj[s][d] * scl;
   }
 }
 
@@ -144,25 +171,37 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
   const double* gint = sc + P.scr_gint;
   const double* ggam = sc + P.scr_ggam;
   const bool lin = P.map_kind == MAP_LINEAR;
-  const double* Jint = lin ? B.in.W1 : sc + P.scr_jint;   // [n_io][NI]
+  const double* Jint = lin ? B.in.W1
+                           : (P.scr_jint < 0 ? P.gJ + (size_t)(V.gslot0 + s) * P.gJ_stride
+                                             : sc + P.scr_jint);  // [n_io][NI]
   const double* Jgam = lin ? B.ga.W1 : sc + P.scr_jgam;   // [N_gam][NG]
-  const StRow& rw = B.rows[row];
+  const StRows& RW = B.rows;
+  const int nr = B.nrows;
   auto val = [&](int c) -> double {
     return c < B.n_io ? gint[c] : ggam[__ldg(B.gio + (c - B.n_io))];
   };
-  const int ne = rw.nent;
-  double xe[MAXE];
+  const int ne = __ldg(RW.nent + row);
+  const int gu = __ldg(RW.gu + row), gv = __ldg(RW.gv + row);
+  int cl[MAXE];
+  double bxc[MAXE], byc[MAXE], cdc[MAXE], xe[MAXE];
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    cl[e] = __ldg(RW.col + e * nr + row);
+    bxc[e] = __ldg(RW.bxc + e * nr + row);
+    byc[e] = __ldg(RW.byc + e * nr + row);
+    cdc[e] = __ldg(RW.cdc + e * nr + row);
+  }
   double sx = 0.0, sy = 0.0, scd = 0.0;
 #pragma unroll
   for (int e = 0; e < MAXE; ++e) {
     if (e < ne) {
-      xe[e] = val(rw.col[e]);
-      if (rw.bxc[e] != 0.0) sx = __dadd_rn(sx, __dmul_rn(rw.bxc[e], xe[e]));
-      if (rw.byc[e] != 0.0) sy = __dadd_rn(sy, __dmul_rn(rw.byc[e], xe[e]));
-      if (rw.cdc[e] != 0.0) scd = __dadd_rn(scd, __dmul_rn(rw.cdc[e], xe[e]));
+      xe[e] = val(cl[e]);
+      if (bxc[e] != 0.0) sx = __dadd_rn(sx, __dmul_rn(bxc[e], xe[e]));
+      if (byc[e] != 0.0) sy = __dadd_rn(sy, __dmul_rn(byc[e], xe[e]));
+      if (cdc[e] != 0.0) scd = __dadd_rn(scd, __dmul_rn(cdc[e], xe[e]));
     }
   }
-  const double xu = val(rw.gu), xv = val(rw.gv);
+  const double xu = val(gu), xv = val(gv);
   const double bx = bv[0], by = bv[1], bc = bv[2];
   const double tx = sx - bx, ty = sy - by;
   // xu*(Bx x - bx) + xv*(By x - by) + Cd x + c  (partition.py:434-441)
@@ -175,14 +214,14 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
 #pragma unroll
   for (int e = 0; e < MAXE; ++e) {
     if (e < ne) {
-      const int c = rw.col[e];
+      const int c = cl[e];
       // diag(Bx x - b)E_u + diag(x_u)Bx + diag(x_v)By + diag(By x - b)E_v + Cd
       double j = 0.0;
-      if (c == rw.gu) j = tx;
-      if (c == rw.gv) j = __dadd_rn(j, ty);
-      if (rw.bxc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xu, rw.bxc[e]));
-      if (rw.byc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xv, rw.byc[e]));
-      if (rw.cdc[e] != 0.0) j = __dadd_rn(j, rw.cdc[e]);
+      if (c == gu) j = tx;
+      if (c == gv) j = __dadd_rn(j, ty);
+      if (bxc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xu, bxc[e]));
+      if (byc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xv, byc[e]));
+      if (cdc[e] != 0.0) j = __dadd_rn(j, cdc[e]);
       if (c < B.n_io) {
         const double* jr = Jint + (size_t)c * NI;
 #pragma unroll
@@ -226,6 +265,7 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
           hidden_unit<G, NG>(V, B.ga, it - nhi, B.xoff + NI, nhi, mask);
       }
       __syncthreads();
+      DDNM_MARK(V, 1);
     }
     // ---- phase B: outputs (+ Jacobian rows) ----
     {
@@ -233,9 +273,9 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       for (int it = tid; it < not_; it += T) {
         if (P.map_kind == MAP_AE) {
           if (it < noi)
-            sweep_output<G, NI>(V, B.in, it, 0, P.scr_gint, P.scr_jint, mask);
+            sweep_output<G, NI>(V, B.in, it, 0, P.scr_gint, P.scr_jint, mask, P.scr_jint < 0);
           else
-            sweep_output<G, NG>(V, B.ga, it - noi, nhi, P.scr_ggam, P.scr_jgam, mask);
+            sweep_output<G, NG>(V, B.ga, it - noi, nhi, P.scr_ggam, P.scr_jgam, mask, false);
         } else {
           if (it < noi)
             linear_output<G, NI>(V, B.in, it, B.xoff, P.scr_gint, mask);
@@ -244,13 +284,18 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         }
       }
       __syncthreads();
+      DDNM_MARK(V, 2);
     }
     // ---- phase C: WFPC constraint (warp tasks) + HR stencil rows ----
     {
       const int ngo = B.ga.n_out;
-      for (int t = warp; t < G * P.n_C; t += nw) {
-        const int s = t / P.n_C, c = t - s * P.n_C;
-        if (!((mask >> s) & 1u)) continue;
+      // 8-lane group per (slot, constraint row): cval = CA g, cjac = CA J
+      // (driver.py:371-373); the remaining threads start on stencil rows
+      const int nct = 8 * G * P.n_C, nct32 = (nct + 31) & ~31;
+      for (int t = tid; t < nct32; t += T) {
+        const int grp = min(t, nct - 1) >> 3, q = t & 7;
+        const int s = grp / P.n_C, c = grp - s * P.n_C;
+        const bool act = t < nct && ((mask >> s) & 1u);
         const double* sc = V.scr(s);
         const double* gg = sc + P.scr_ggam;
         const double* Jg = P.map_kind == MAP_LINEAR ? B.ga.W1 : sc + P.scr_jgam;
@@ -258,29 +303,35 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         double a0 = 0.0, aj[NG];
 #pragma unroll
         for (int d = 0; d < NG; ++d) aj[d] = 0.0;
-        for (int j = lane; j < ngo; j += WARP) {
-          const double cj = __ldg(ca + j);
-          a0 = fma(cj, gg[j], a0);
+        if (act)
+          for (int j = q; j < ngo; j += 8) {
+            const double cj = __ldg(ca + j);
+            a0 = fma(cj, gg[j], a0);
 #pragma unroll
-          for (int d = 0; d < NG; ++d) aj[d] = fma(cj, Jg[(size_t)j * NG + d], aj[d]);
+            for (int d = 0; d < NG; ++d) aj[d] = fma(cj, Jg[(size_t)j * NG + d], aj[d]);
+          }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+#pragma unroll
+          for (int d = 0; d < NG; ++d) aj[d] += __shfl_xor_sync(0xffffffffu, aj[d], o);
         }
-        a0 = warp_sum(a0);
-#pragma unroll
-        for (int d = 0; d < NG; ++d) aj[d] = warp_sum(aj[d]);
-        if (lane == 0) {
+        if (act && q == 0) {
           double* e = V.eb(s, ebi[s]);
           eb_cval(e, B)[c] = a0;
 #pragma unroll
           for (int d = 0; d < NG; ++d) eb_cjac(e, B, P.n_C)[c * NG + d] = aj[d];
         }
       }
-      for (int it = tid; it < G * B.nrows; it += T) {
+      for (int it = tid - nct32; it < G * B.nrows; it += T) {
+        if (it < 0) continue;
         const int s = it / B.nrows, row = it - s * B.nrows;
         if (!((mask >> s) & 1u)) continue;
         const double* bv = P.gbv + ((size_t)(gslot0 + s) * P.total_rows + B.row_off + row) * 3;
         stencil_row<NI, NG>(V, B, s, row, bv);
       }
       __syncthreads();
+      DDNM_MARK(V, 3);
     }
     // ---- optional dumps of every intermediate (ddnm_eval_batch) ----
     if (dump) {
@@ -290,7 +341,9 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         const size_t mu = (size_t)st[s].mu;
         const double* sc = V.scr(s);
         const bool lin = P.map_kind == MAP_LINEAR;
-        const double* Jint = lin ? B.in.W1 : sc + P.scr_jint;
+        const double* Jint = lin ? B.in.W1
+                                 : (P.scr_jint < 0 ? P.gJ + (size_t)(gslot0 + s) * P.gJ_stride
+                                                   : sc + P.scr_jint);
         const double* Jgam = lin ? B.ga.W1 : sc + P.scr_jgam;
         if (o.int_g)
           for (int i = tid; i < B.in.n_out; i += T) o.int_g[mu * P.tot_iout + B.iout_off + i] = sc[P.scr_gint + i];
@@ -353,8 +406,7 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         const double acc = (a0 + a1) + (a2 + a3);
         double* e = V.eb(s, ebi[s]);
         if (kind == 0) {
-          eb_H(e, B)[i * W + j] = acc;
-          eb_H(e, B)[j * W + i] = acc;
+          eb_H(e, B)[tri_idx(W, i, j)] = acc;
         } else if (kind == 1) {
           eb_proj(e, B)[i] = acc;
         } else {
@@ -362,6 +414,7 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         }
       }
       __syncthreads();
+      DDNM_MARK(V, 4);
     }
   }
 }
@@ -489,9 +542,9 @@ __device__ void kkt_matvec(const Params& P, const double* e, double delta, const
     if (i < P.n_D) {
       const int b = i / W, li = i - b * W;
       const BlockDev& B = P.blk[b];
-      const double* H = eb_H(const_cast<double*>(e), B) + li * W;
+      const double* H = eb_H(const_cast<double*>(e), B);
       const double* xb = x + b * W;
-      for (int j = 0; j < W; ++j) v = fma(H[j], xb[j], v);
+      for (int j = 0; j < W; ++j) v = fma(hval(H, W, li, j), xb[j], v);
       if (delta != 0.0) v = fma(delta, x[i], v);
       if (li >= NI) {
         const double* cj = eb_cjac(const_cast<double*>(e), B, P.n_C);
@@ -541,7 +594,7 @@ __device__ int warp_kkt(const Params& P, const double* e, double* work, double* 
       double tr = 0.0;
       if (lane == 0) {
         for (int b = 0; b < P.nb; ++b)
-          for (int i = 0; i < W; ++i) tr = tr + eb_H(const_cast<double*>(e), P.blk[b])[i * W + i];
+          for (int i = 0; i < W; ++i) tr = tr + hval(eb_H(const_cast<double*>(e), P.blk[b]), W, i, i);
       }
       tr = __shfl_sync(0xffffffffu, tr, 0);
       delta = P.cfg.reg_scale * fmax(tr, 1.0);
@@ -552,7 +605,7 @@ __device__ int warp_kkt(const Params& P, const double* e, double* work, double* 
       double v = 0.0;
       if (i < P.n_D && j < P.n_D) {
         const int bi = i / W, bj = j / W;
-        if (bi == bj) v = eb_H(const_cast<double*>(e), P.blk[bi])[(i - bi * W) * W + (j - bj * W)];
+        if (bi == bj) v = hval(eb_H(const_cast<double*>(e), P.blk[bi]), W, i - bi * W, j - bj * W);
         if (i == j) v += delta;
       } else if (i < P.n_D && j >= P.n_D) {
         const int b = i / W, li = i - b * W;
@@ -648,7 +701,7 @@ __device__ bool kkt_block_factor(const Params& P, const double* e, int b, double
   for (int idx = lane; idx < m * m; idx += WARP) {
     const int i = idx / m, j = idx - i * m;
     double v = 0.0;
-    if (i < W && j < W) v = H[i * W + j];
+    if (i < W && j < W) v = hval(H, W, i, j);
     else if (i < W && j >= W) v = i >= NI ? cj[(j - W) * NG + (i - NI)] : 0.0;
     else if (i >= W && j < W) v = j >= NI ? cj[(i - W) * NG + (j - NI)] : 0.0;
     M[i * ld + j] = v;
@@ -690,9 +743,10 @@ __device__ bool kkt_block_factor(const Params& P, const double* e, int b, double
       for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] /= pv;
     }
     __syncwarp();
-    for (int j = k + 1 + lane; j < m; j += WARP) {
-      const double ukj = M[k * ld + j];
-      for (int i = k + 1; i < m; ++i) M[i * ld + j] = fma(-M[i * ld + k], ukj, M[i * ld + j]);
+    const int nt = m - k - 1;
+    for (int idx = lane; idx < nt * nt; idx += WARP) {
+      const int i = k + 1 + idx / nt, j = k + 1 + idx % nt;
+      M[i * ld + j] = fma(-M[i * ld + k], M[k * ld + j], M[i * ld + j]);
     }
     __syncwarp();
   }
@@ -758,6 +812,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   const int nC = P.n_C, nb = P.nb;
   if (tid < G) kflag[tid] = 1;
   __syncthreads();
+  DDNM_MARK(V, 12);
   // 1. per-block elimination
   for (int t = warp; t < G * nb; t += nw) {
     const int s = t / nb, b = t - s * nb;
@@ -768,6 +823,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     if (!ok && lane == 0) atomicAnd(&kflag[s], 0);
   }
   __syncthreads();
+  DDNM_MARK(V, 8);
   // 2. Schur block S = sum_b (in block order), its LU; rhs = -[rho; con]
   if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
     const int s = warp;
@@ -787,6 +843,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
       sc[L.off_rhs + i] = -(i < P.n_D ? e[P.eb_rho + i] : e[P.eb_con + i - P.n_D]);
   }
   __syncthreads();
+  DDNM_MARK(V, 9);
   // 3. solve, refine once, check (sqp.py:175-189)
   for (int pass = 0; pass < 2; ++pass) {
     // right-hand side of this pass -> tmp (copy), solution -> sol (pass 0) / res (pass 1)
@@ -803,6 +860,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
                                 sc + L.off_tE + b * nC);
     }
     __syncthreads();
+    DDNM_MARK(V, 10);
     if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
       const int s = warp;
       double* sc = V.scr(s);
@@ -817,6 +875,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
       warp_lu_solve(sc + L.off_S, L.ldS, nC, reinterpret_cast<const int*>(sc + L.off_pivS), y);
     }
     __syncthreads();
+    DDNM_MARK(V, 10);
     for (int t = warp; t < G * nb; t += nw) {
       const int s = t / nb, b = t - s * nb;
       if (!((kmask >> s) & 1u) || !kflag[s]) continue;
@@ -825,6 +884,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
       kkt_block_backward<NI, NG>(P, sc + b * L.msz, y + b * W, y + P.n_D);
     }
     __syncthreads();
+    DDNM_MARK(V, 10);
     if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
       const int s = warp;
       double* sc = V.scr(s);
@@ -865,6 +925,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
       }
     }
     __syncthreads();
+    DDNM_MARK(V, 11);
   }
   // 4. dense fallback (reference semantics incl. the +delta*I retry)
   if (warp < G && ((kmask >> warp) & 1u) && !kflag[warp]) {
@@ -879,6 +940,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     if (lane == 0) kres[s] = r;
   }
   __syncthreads();
+  DDNM_MARK(V, 13);
 }
 
 // multiplier_least_squares (driver.py:461-471) for one slot, one warp:
@@ -987,14 +1049,16 @@ static __device__ void warp_rbf(const Params& P, double a, double lm, double* x0
 
 // boundary values (bx, by, c) of assemble() at every sampled row
 // (burgers.py:188-210): ghost points just outside the edges the node touches.
-static __device__ void row_bvals(const Params& P, const StRow& rw, double a, double lm, double* out) {
+static __device__ void row_bvals(const Params& P, const StRows& RW, int row, double a, double lm, double* out) {
   const double hx = P.hx, hy = P.hy, nu = P.nu;
-  const bool isv = (rw.bflags >> 4) & 1;
+  const int bflags = RW.bflags[row];
+  const double xc = RW.xc[row], yc = RW.yc[row];
+  const bool isv = (bflags >> 4) & 1;
   double exl = 0.0, exr = 0.0, eyb = 0.0, eyt = 0.0, u, v;
-  if (rw.bflags & 1) { exact_uv(a, lm, -1.0, rw.yc, nu, u, v); exl = isv ? v : u; }
-  if (rw.bflags & 2) { exact_uv(a, lm, 1.0, rw.yc, nu, u, v); exr = isv ? v : u; }
-  if (rw.bflags & 4) { exact_uv(a, lm, rw.xc, 0.0, nu, u, v); eyb = isv ? v : u; }
-  if (rw.bflags & 8) { exact_uv(a, lm, rw.xc, 0.05, nu, u, v); eyt = isv ? v : u; }
+  if (bflags & 1) { exact_uv(a, lm, -1.0, yc, nu, u, v); exl = isv ? v : u; }
+  if (bflags & 2) { exact_uv(a, lm, 1.0, yc, nu, u, v); exr = isv ? v : u; }
+  if (bflags & 4) { exact_uv(a, lm, xc, 0.0, nu, u, v); eyb = isv ? v : u; }
+  if (bflags & 8) { exact_uv(a, lm, xc, 0.05, nu, u, v); eyt = isv ? v : u; }
   out[0] = (-1.0 / (2.0 * hx)) * (exl - exr);
   out[1] = (-1.0 / (2.0 * hy)) * (eyb - eyt);
   out[2] = (nu / (hx * hx)) * (exl + exr) + (nu / (hy * hy)) * (eyb + eyt);
@@ -1017,9 +1081,13 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
   __shared__ unsigned s_newmask;
   __shared__ unsigned long long s_evals, s_kkts;
   __shared__ int s_kres[G], s_kflag[G];
+  __shared__ unsigned long long s_prof[16];
   if (tid < G) { st[tid].mu = -1; st[tid].phase = PH_DONE; s_cur[tid] = 0; }
   if (tid == 0) { s_evals = 0; s_kkts = 0; }
+  if (tid < 16) s_prof[tid] = 0;
+  if (P.prof) V.prof = s_prof;
   __syncthreads();
+  if (tid == 0) s_prof[15] = clock64();
   const SqpCfg& cfg = P.cfg;
   for (;;) {
     // ---- retire finished slots, fetch new mu ----
@@ -1044,6 +1112,7 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
       s_newmask = nm;
     }
     __syncthreads();
+    DDNM_MARK(V, 0);
     const unsigned mask = s_mask, newmask = s_newmask;
     if (mask == 0) break;
     // ---- initialise new slots: boundary values (CTA-wide), x0 / lam0 (warp per slot) ----
@@ -1055,7 +1124,7 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
         double* gb = P.gbv + (size_t)(gslot0 + s) * P.total_rows * 3;
         for (int b = 0; b < P.nb; ++b) {
           const BlockDev& B = P.blk[b];
-          for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows[r], a, lm, gb + (B.row_off + r) * 3);
+          for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows, r, a, lm, gb + (B.row_off + r) * 3);
         }
       }
       if (warp < G && ((newmask >> warp) & 1u)) {
@@ -1073,10 +1142,12 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
         if (P.so.x0) for (int j = lane; j < P.n_D; j += WARP) P.so.x0[(size_t)mu * P.n_D + j] = xt[j];
       }
       __syncthreads();
+      DDNM_MARK(V, 5);
     }
     // ---- one eval_gradients per active slot ----
     if (tid < G) s_ebi[tid] = st[tid].phase == PH_INIT ? s_cur[tid] : 1 - s_cur[tid];
     __syncthreads();
+    DDNM_MARK(V, 0);
     eval_blocks<G, NI, NG>(V, mask, s_ebi, gslot0, false);
     if (tid == 0) s_evals += (unsigned long long)__popc(mask) * P.nb;
     // ---- per-slot state machine (warp s) ----
@@ -1166,6 +1237,7 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
       __syncwarp();
     }
     __syncthreads();
+    DDNM_MARK(V, 6);
     // ---- KKT solves (block-structured LU across warps, dense fallback) ----
     {
       unsigned kmask = 0;
@@ -1196,6 +1268,7 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
         __syncthreads();
       }
     }
+    DDNM_MARK(V, 7);
     // ---- write results of finished slots ----
     if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) {
       const int s = warp;
@@ -1219,6 +1292,8 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
   if (tid == 0) {
     atomicAdd(P.counters, s_evals);
     atomicAdd(P.counters + 1, s_kkts);
+    if (P.prof)
+      for (int i = 0; i < 15; ++i) atomicAdd(P.prof + i, s_prof[i]);
   }
 }
 
@@ -1256,7 +1331,7 @@ __global__ void __launch_bounds__(512) k_eval(const __grid_constant__ Params P) 
     double* gb = P.gbv + (size_t)(gslot0 + s) * P.total_rows * 3;
     for (int b = 0; b < P.nb; ++b) {
       const BlockDev& B = P.blk[b];
-      for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows[r], a, lm, gb + (B.row_off + r) * 3);
+      for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows, r, a, lm, gb + (B.row_off + r) * 3);
     }
     for (int j = tid; j < P.n_D; j += T) V.vec(s, 4)[j] = P.x0_in[(size_t)mu * P.n_D + j];
     for (int c = tid; c < P.n_C; c += T) V.vec(s, 5)[c] = P.lam0_in[(size_t)mu * P.n_C + c];

@@ -172,6 +172,15 @@ class _Context:
             N.lib().ddnm_ctx_destroy(self.h)
             self.h = None
 
+    def profile(self):
+        """Per-phase device cycles of the last solve (set DDNM_PROF=1)."""
+        buf = (C.c_uint64 * 16)()
+        N.check(N.lib().ddnm_last_profile(self.h, buf))
+        names = ["fetch", "A_hidden", "B_sweep", "C_stencil", "D_gram", "init", "sqp_state",
+                 "kkt"]
+        names += ["kkt_factor", "kkt_S", "kkt_solve", "kkt_check", "kkt_setup", "kkt_fallback"]
+        return {n: int(buf[i]) for i, n in enumerate(names)}
+
     def counters(self):
         e, k = C.c_int64(), C.c_int64()
         N.check(N.lib().ddnm_last_counters(self.h, C.byref(e), C.byref(k)))

@@ -15,4 +15,8 @@ inst = P.RomInstance.load(os.path.join(ROOT, "tests", "golden", f"{name}_artifac
 mu = P.seeded_parameters(B, seed=1000)
 for _ in range(2):
     r = P.solve_rom_batch(inst, mu, slots=slots)
+ctx = inst.context(-1, slots)
+prof = ctx.profile()
+tot = sum(prof.values()) or 1
+print({k: f"{100 * v / tot:.1f}%" for k, v in prof.items()})
 print(f"{name} B={B} solve {r.seconds*1e3:.2f} ms, evals {r.counters}, mean n_iter {r.n_iter.mean():.2f}")
