@@ -223,7 +223,13 @@ int check_decoder(const ddnm_decoder& d, int lat, int kind, const char* what) {
   return 0;
 }
 
-int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev& d) {
+struct HostWindows {        // contiguous-window decoders: per-output k0 and width
+  std::vector<int> k0, w;
+  int maxw = 0;
+};
+
+int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev& d,
+                   HostWindows& hw) {
   d.n_out = h.n_out;
   d.n_hidden = kind == DDNM_MAP_AUTOENCODER ? h.n_hidden : 0;
   int rc;
@@ -263,10 +269,37 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
     }
     d.ell_k = nullptr;
     d.ell_k0 = nullptr;
+    d.w1frag = nullptr;
+    d.v_row = nullptr;
+    d.row_w = nullptr;
+    hw.k0.clear();
+    hw.w.clear();
     if (ew > 0) {
       if ((rc = upload(c, ev.data(), ev.size(), const_cast<double**>(&d.ell_v)))) return rc;
       if (contig) {
         if ((rc = upload(c, k0.data(), k0.size(), const_cast<int**>(&d.ell_k0)))) return rc;
+        // tensor-core sweep tables: W1 in A-fragment order, rows contiguous
+        const int nkb = (h.n_hidden + 3) / 4;
+        std::vector<double> fr((size_t)nkb * 32, 0.0);
+        for (int kb = 0; kb < nkb; ++kb)
+          for (int l = 0; l < 32; ++l) {
+            const int k = 4 * kb + (l & 3), dd = l >> 2;
+            if (k < h.n_hidden && dd < lat) fr[(size_t)kb * 32 + l] = h.W1[(size_t)k * lat + dd];
+          }
+        std::vector<double> vr((size_t)h.n_out * ew, 0.0);
+        std::vector<int> rw(h.n_out);
+        for (int o = 0; o < h.n_out; ++o) {
+          rw[o] = (int)(h.indptr[o + 1] - h.indptr[o]);
+          for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e)
+            vr[(size_t)o * ew + (e - h.indptr[o])] = h.data[e];
+        }
+        if ((rc = upload(c, fr.data(), fr.size(), const_cast<double**>(&d.w1frag))) ||
+            (rc = upload(c, vr.data(), vr.size(), const_cast<double**>(&d.v_row))) ||
+            (rc = upload(c, rw.data(), rw.size(), const_cast<int**>(&d.row_w))))
+          return rc;
+        hw.k0 = k0;
+        hw.w = rw;
+        hw.maxw = (int)wmax;
       } else {
         if ((rc = upload(c, ek.data(), ek.size(), const_cast<int**>(&d.ell_k)))) return rc;
       }
@@ -348,6 +381,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   const int W = ni + ng;
   int xoff = 0, row_off = 0, iout = 0, gout = 0, Roff = 0, cjoff = 0, ijoff = 0, gjoff = 0, eboff = 0;
   int max_nh = 0, max_io = 0, max_gam = 0, max_rows = 0;
+  std::vector<HostWindows> hwin(2 * a->n_blocks);
   for (int b = 0; b < P.nb; ++b) {
     const ddnm_block& k = a->blocks[b];
     BlockDev& B = P.blk[b];
@@ -355,8 +389,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     B.nrows = k.n_rows; B.n_io = k.n_io; B.n_gio = k.n_gio;
     B.xoff = xoff; B.row_off = row_off; B.iout_off = iout; B.gout_off = gout; B.R_off = Roff;
     B.cjac_off = cjoff; B.intJ_off = ijoff; B.gamJ_off = gjoff; B.eb_off = eboff;
-    if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, B.in))) return bail(rc);
-    if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, B.ga))) return bail(rc);
+    if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, B.in, hwin[2 * b]))) return bail(rc);
+    if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, B.ga, hwin[2 * b + 1]))) return bail(rc);
     HostRows hr;
     if ((rc = build_stencil(a, k, hr))) return bail(rc);
     StRows& R = B.rows;
@@ -470,6 +504,39 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   }
   P.scr_size = scr_total(kern_jsm);
   c->K = *kern;
+  // tiles of consecutive outputs for the tensor-core sweep (P = 8 / G outputs each)
+  if (getenv("DDNM_DMMA") && ae) {
+    const int Pt = 8 / kern->g;
+    for (int b = 0; b < P.nb; ++b) {
+      if (hwin[2 * b].k0.empty() || hwin[2 * b + 1].k0.empty()) continue;
+      std::vector<TileRec> tiles;
+      for (int which = 0; which < 2; ++which) {
+        const HostWindows& hw = hwin[2 * b + which];
+        const int n = (int)hw.k0.size();
+        int o = 0;
+        while (o < n) {
+          int lo = hw.k0[o], hi = hw.k0[o] + hw.w[o];
+          int cnt = 1;
+          while (cnt < Pt && o + cnt < n) {
+            const int nlo = std::min(lo, hw.k0[o + cnt]);
+            const int nhi = std::max(hi, hw.k0[o + cnt] + hw.w[o + cnt]);
+            if (nhi - nlo > hw.maxw + Pt + 3) break;
+            lo = nlo; hi = nhi; ++cnt;
+          }
+          TileRec t;
+          std::memset(&t, 0, sizeof t);
+          t.o0 = o; t.cnt = cnt | (which << 8); t.kb_lo = lo / 4; t.kb_hi = (hi - 1) / 4;
+          for (int j = 0; j < cnt; ++j) { t.k0[j] = hw.k0[o + j]; t.w[j] = hw.w[o + j]; }
+          if (t.kb_hi - t.kb_lo + 1 > 10) return bail(fail(DDNM_EUNSUPPORTED, "sweep tile wider than 10 k-blocks"));
+          tiles.push_back(t);
+          o += cnt;
+        }
+      }
+      if ((rc = upload(c, tiles.data(), tiles.size(), const_cast<TileRec**>(&P.blk[b].tiles)))) return bail(rc);
+      P.blk[b].n_tiles = (int)tiles.size();
+    }
+  }
+  if (const char* th = getenv("DDNM_THREADS")) c->threads = std::max(128, std::min(512, atoi(th) / 32 * 32));
   P.G = kern->g;
   P.sm_state = 0;
   P.sm_vec = state_d * P.G;

@@ -49,6 +49,19 @@ struct DecDev {
   const double* ell_v;    // [ell_w][n_out] W2 values in storage order, 0-padded
   const int* ell_k;       // [ell_w][n_out] hidden indices, 0-padded (null if contiguous)
   const int* ell_k0;      // [n_out] first hidden index when every row's window is contiguous
+  // DMMA sweep (contiguous windows only): W1 in mma.m8n8k4 A-fragment order,
+  // W2 rows contiguous, and tiles of consecutive outputs with their k-block range
+  const double* w1frag;   // [ceil(n_hidden/4)][32]: lane -> W1[4kb + (lane&3)][lane>>2]
+  const double* v_row;    // [n_out][ell_w] W2 values, row-contiguous, 0-padded
+  const int* row_w;       // [n_out] stored entries per row
+};
+
+// A tensor-core sweep tile: up to 8/G consecutive outputs of one decoder with
+// everything its B operand needs, so a warp issues no dependent loads.
+struct TileRec {
+  int o0, cnt, kb_lo, kb_hi;    // cnt | which << 8 (0 interior, 1 interface)
+  int k0[8];                    // first hidden unit of each output's window
+  int w[8];                     // stored entries of each output
 };
 
 // Sampled residual rows in local-column form (RestrictedResidual,
@@ -70,6 +83,7 @@ struct StRows {
 };
 
 struct BlockDev {
+  // (tiles depend on G; the host builds them for the kernel's G)
   int ni, ng, w;          // latent dims, w = ni + ng
   int nrows, n_io, n_gio;
   int xoff;               // offset of (x_int, x_gam) in the stacked latent
@@ -77,6 +91,8 @@ struct BlockDev {
   int iout_off, gout_off, R_off, cjac_off, intJ_off, gamJ_off;
   int eb_off;             // offset of this block inside a slot eval buffer
   DecDev in, ga;
+  const TileRec* tiles;   // tensor-core sweep tiles of both decoders (or null)
+  int n_tiles;
   StRows rows;
   const int* gio;
   const double* CA;       // [n_c][ga.n_out]

@@ -2,10 +2,19 @@
 #pragma once
 #include "ddnm_device.cuh"
 
+#ifndef DDNM_MAX_THREADS
+#define DDNM_MAX_THREADS 512
+#endif
+
 namespace ddnm {
 
 // --------------------------------------------------------------------------
 // shared-memory views
+
+// Dynamic shared memory of the kernels.  Every slot view is formed from this
+// symbol (not from a pointer member) so the compiler keeps the shared address
+// space and emits LDS/STS instead of generic loads.
+extern __shared__ __align__(16) double ddnm_smem[];
 
 struct View {
   const Params& P;
@@ -14,11 +23,11 @@ struct View {
   unsigned long long* prof;  // per-phase clock totals (thread 0), or null
   __device__ View(const Params& p, double* s)
       : P(p), sm(s), gslot0(blockIdx.x * p.G), prof(nullptr) {}
-  __device__ SlotState* st() const { return reinterpret_cast<SlotState*>(sm + P.sm_state); }
+  __device__ SlotState* st() const { return reinterpret_cast<SlotState*>(ddnm_smem + P.sm_state); }
   // vectors: 0 x, 1 lam, 2 s, 3 slam, 4 xt, 5 lt, 6 best x, 7 best lam
-  __device__ double* vec(int s, int which) const { return sm + P.sm_vec + (s * 8 + which) * P.nK; }
-  __device__ double* eb(int s, int which) const { return sm + P.sm_eb + (s * 2 + which) * P.eb_size; }
-  __device__ double* scr(int s) const { return sm + P.sm_scr + s * P.scr_size; }
+  __device__ double* vec(int s, int which) const { return ddnm_smem + P.sm_vec + (s * 8 + which) * P.nK; }
+  __device__ double* eb(int s, int which) const { return ddnm_smem + P.sm_eb + (s * 2 + which) * P.eb_size; }
+  __device__ double* scr(int s) const { return ddnm_smem + P.sm_scr + s * P.scr_size; }
 };
 
 // phase timing (device-side profiler, off unless Params::prof is set)
@@ -140,6 +149,106 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
                          : sc + j_off + o * L;
 #pragma unroll
     for (int d = 0; d < L; ++d) jr[d] = aj[s][d] * scl;
+  }
+}
+
+// phase B on the FP64 tensor cores (mma.sync m8n8k4): for a tile of P = 8/G
+// consecutive outputs and all G slots,
+//   J[d][(mu, o)] = sum_k W1[k][d] * (W2[o][k] * sigma'[mu][k])      (A = W1, shared)
+// M = latent dim d, N = 8 columns (slot mu = col % G, output o = col / G),
+// K = 4 hidden units per mma, over the tile's k-block range; g = W2 sigma
+// accumulates on the FP64 pipe from the same B-operand loads.  Same sums as
+// hyper.py:190-197 in a different association order.
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ TileRec load_tile(const TileRec* t) {
+  TileRec r;
+  const int4* p = reinterpret_cast<const int4*>(t);
+  const int4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3), e = __ldg(p + 4);
+  r.o0 = a.x; r.cnt = a.y; r.kb_lo = a.z; r.kb_hi = a.w;
+  r.k0[0] = b.x; r.k0[1] = b.y; r.k0[2] = b.z; r.k0[3] = b.w;
+  r.k0[4] = c.x; r.k0[5] = c.y; r.k0[6] = c.z; r.k0[7] = c.w;
+  r.w[0] = d.x; r.w[1] = d.y; r.w[2] = d.z; r.w[3] = d.w;
+  r.w[4] = e.x; r.w[5] = e.y; r.w[6] = e.z; r.w[7] = e.w;
+  return r;
+}
+
+template <int G, int L>
+__device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const TileRec& tile,
+                                           int sig_off, int g_off, int j_off, unsigned mask,
+                                           bool jglobal) {
+  constexpr int P = 8 / G;
+  const int lane = threadIdx.x & 31, tig = lane & 3, grp = lane >> 2;
+  const int o0 = tile.o0, cnt = tile.cnt & 0xff;
+  // B-operand column of this lane: col = grp -> (slot, output)
+  const int bmu = grp % G, bo = grp / G;
+  const bool bval = bo < cnt && ((mask >> bmu) & 1u);
+  int bk0 = tile.k0[0], bw = tile.w[0];
+#pragma unroll
+  for (int j = 1; j < P; ++j)
+    if (bo == j) { bk0 = tile.k0[j]; bw = tile.w[j]; }
+  const int bout = o0 + min(bo, cnt - 1);
+  const double* vrow = D.v_row + (size_t)bout * D.ell_w;
+  const double* sg = V.scr(bmu) + V.P.scr_sig + sig_off;
+  const double* dsg = V.scr(bmu) + V.P.scr_dsig + sig_off;
+  // all fragment loads of the tile first (independent), then the MMAs on
+  // three independent accumulator chains
+  constexpr int KB = 10;                        // window <= 24 + P + 3 -> <= 10 k-blocks
+  double a[KB], b[KB];
+  double gacc = 0.0;
+  const int nh1 = D.n_hidden - 1, ew1 = D.ell_w - 1;
+  // branch-free: every load has a valid (clamped) address, values are masked
+#pragma unroll
+  for (int i = 0; i < KB; ++i) {
+    const bool kin = tile.kb_lo + i <= tile.kb_hi;
+    const int kb = min(tile.kb_lo + i, tile.kb_hi);
+    const double af = __ldg(D.w1frag + (size_t)kb * 32 + lane);
+    const int k = 4 * kb + tig;
+    const int e = k - bk0;
+    const bool ok = kin && bval && e >= 0 && e < bw;
+    const double vr = __ldg(vrow + min(max(e, 0), ew1));
+    const int kk = min(k, nh1);
+    const double sp = dsg[kk], s0 = sg[kk];
+    const double v = ok ? vr : 0.0;
+    a[i] = kin ? af : 0.0;
+    b[i] = v * sp;
+    gacc = fma(v, s0, gacc);
+  }
+  double c[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < KB; ++i) {
+    if (tile.kb_lo + i <= tile.kb_hi) {
+      if (i % 3 == 0) dmma_884(c, a[i], b[i]);
+      else if (i % 3 == 1) dmma_884(c1, a[i], b[i]);
+      else dmma_884(c2, a[i], b[i]);
+    }
+  }
+  c[0] = (c[0] + c1[0]) + c2[0];
+  c[1] = (c[1] + c1[1]) + c2[1];
+  // g: reduce the 4 k-lanes of each column
+  gacc += __shfl_xor_sync(0xffffffffu, gacc, 1);
+  gacc += __shfl_xor_sync(0xffffffffu, gacc, 2);
+  if (tig == 0 && bval) {
+    const double scl = __ldg(D.scale + bout), sh = __ldg(D.shift + bout);
+    V.scr(bmu)[g_off + bout] = __dadd_rn(__dmul_rn(gacc, scl), sh);
+  }
+  // J: lane holds C[d = grp][cols 2 tig, 2 tig + 1]
+  if (grp < L) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = 2 * tig + h;
+      const int mu = col % G, oo = col / G;
+      if (oo < cnt && ((mask >> mu) & 1u)) {
+        const int o = o0 + oo;
+        const double scl = __ldg(D.scale + o);
+        double* jr = jglobal ? V.P.gJ + (size_t)(V.gslot0 + mu) * V.P.gJ_stride + (size_t)o * L
+                             : V.scr(mu) + j_off + o * L;
+        jr[grp] = c[h] * scl;
+      }
+    }
   }
 }
 
@@ -268,7 +377,24 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       DDNM_MARK(V, 1);
     }
     // ---- phase B: outputs (+ Jacobian rows) ----
-    {
+    if (P.map_kind == MAP_AE && B.tiles) {
+      // tensor-core sweep: warp per tile, next tile record prefetched
+      const int ntt = B.n_tiles;
+      int t = warp;
+      TileRec cur;
+      if (t < ntt) cur = load_tile(B.tiles + t);
+      for (; t < ntt; t += nw) {
+        TileRec nxt;
+        if (t + nw < ntt) nxt = load_tile(B.tiles + t + nw);
+        if ((cur.cnt >> 8) == 0)
+          sweep_tile<G, NI>(V, B.in, cur, 0, P.scr_gint, P.scr_jint, mask, P.scr_jint < 0);
+        else
+          sweep_tile<G, NG>(V, B.ga, cur, nhi, P.scr_ggam, P.scr_jgam, mask, false);
+        cur = nxt;
+      }
+      __syncthreads();
+      DDNM_MARK(V, 2);
+    } else {
       const int noi = B.in.n_out, not_ = noi + B.ga.n_out;
       for (int it = tid; it < not_; it += T) {
         if (P.map_kind == MAP_AE) {
@@ -1068,9 +1194,8 @@ static __device__ void row_bvals(const Params& P, const StRows& RW, int row, dou
 // the persistent kernel
 
 template <int G, int NI, int NG>
-__global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P) {
-  extern __shared__ __align__(16) double smem[];
-  View V(P, smem);
+__global__ void __launch_bounds__(DDNM_MAX_THREADS) k_solve(const __grid_constant__ Params P) {
+  View V(P, ddnm_smem);
   SlotState* st = V.st();
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
   constexpr int W = NI + NG;
@@ -1299,14 +1424,17 @@ __global__ void __launch_bounds__(512) k_solve(const __grid_constant__ Params P)
 
 }  // namespace ddnm
 
+#ifndef DDNM_MAX_THREADS
+#define DDNM_MAX_THREADS 512
+#endif
+
 namespace ddnm {
 
 // ddnm_eval_batch: one eval_gradients per mu at a given (x, lam), dumping every
 // intermediate, plus (optionally) the KKT step at that point.  mu = CTA*G + s.
 template <int G, int NI, int NG>
-__global__ void __launch_bounds__(512) k_eval(const __grid_constant__ Params P) {
-  extern __shared__ __align__(16) double smem[];
-  View V(P, smem);
+__global__ void __launch_bounds__(DDNM_MAX_THREADS) k_eval(const __grid_constant__ Params P) {
+  View V(P, ddnm_smem);
   SlotState* st = V.st();
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int gslot0 = blockIdx.x * G;
