@@ -443,8 +443,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // when they fit, otherwise they go to a per-slot L2 scratch (gJ)
   auto plan_scratch = [&](bool jint_smem) {
     int scr = 0;
-    P.scr_sig = scr; scr += ae ? max_nh : 0;
-    P.scr_dsig = scr; scr += ae ? max_nh : 0;
+    P.scr_sig = scr; scr += ae ? max_nh + 8 : 0;     // +8: zero padding read by the
+    P.scr_dsig = scr; scr += ae ? max_nh + 8 : 0;    // tensor-core sweep past n_hidden
     P.scr_gint = scr; scr += max_io;
     if (ae && jint_smem) { P.scr_jint = scr; scr += max_io * ni; } else { P.scr_jint = -1; }
     P.scr_ggam = scr; scr += max_gam;
@@ -510,7 +510,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     for (int b = 0; b < P.nb; ++b) {
       if (hwin[2 * b].k0.empty() || hwin[2 * b + 1].k0.empty()) continue;
       std::vector<TileRec> tiles;
+      int n_in = 0;
       for (int which = 0; which < 2; ++which) {
+        if (which == 1) n_in = (int)tiles.size();
         const HostWindows& hw = hwin[2 * b + which];
         const int n = (int)hw.k0.size();
         int o = 0;
@@ -532,8 +534,27 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
           o += cnt;
         }
       }
-      if ((rc = upload(c, tiles.data(), tiles.size(), const_cast<TileRec**>(&P.blk[b].tiles)))) return bail(rc);
+      // B-operand W2 values per tile in fragment order (mu-independent)
+      std::vector<double> tv(tiles.size() * 10 * 32, 0.0);
+      const int Gk = kern->g;
+      for (size_t t = 0; t < tiles.size(); ++t) {
+        const TileRec& T = tiles[t];
+        const int which = T.cnt >> 8, cnt = T.cnt & 0xff;
+        const ddnm_decoder& h = which == 0 ? a->blocks[b].interior : a->blocks[b].interface;
+        for (int i = 0; i <= T.kb_hi - T.kb_lo; ++i)
+          for (int l = 0; l < 32; ++l) {
+            const int tig = l & 3, oo = (l >> 2) / Gk;
+            if (oo >= cnt) continue;
+            const int o = T.o0 + oo;
+            const int e = 4 * (T.kb_lo + i) + tig - T.k0[oo];
+            if (e >= 0 && e < T.w[oo]) tv[(t * 10 + i) * 32 + l] = h.data[h.indptr[o] + e];
+          }
+      }
+      if ((rc = upload(c, tiles.data(), tiles.size(), const_cast<TileRec**>(&P.blk[b].tiles))) ||
+          (rc = upload(c, tv.data(), tv.size(), const_cast<double**>(&P.blk[b].tile_v))))
+        return bail(rc);
       P.blk[b].n_tiles = (int)tiles.size();
+      P.blk[b].n_tiles_in = n_in;
     }
   }
   if (const char* th = getenv("DDNM_THREADS")) c->threads = std::max(128, std::min(512, atoi(th) / 32 * 32));

@@ -92,7 +92,8 @@ struct BlockDev {
   int eb_off;             // offset of this block inside a slot eval buffer
   DecDev in, ga;
   const TileRec* tiles;   // tensor-core sweep tiles of both decoders (or null)
-  int n_tiles;
+  int n_tiles, n_tiles_in;  // total, interior (stored first)
+  const double* tile_v;   // [n_tiles][10][32] B-operand W2 values per tile
   StRows rows;
   const int* gio;
   const double* CA;       // [n_c][ga.n_out]

@@ -91,9 +91,12 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
 // and W1-row loads are all in flight together:
 //   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e W2_e act'_e W1[k_e, d]) * scale
 template <int G, int L>
-__device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int sig_off,
-                                             int g_off, int j_off, unsigned mask, bool jglobal) {
-  constexpr int U = 8;
+__device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int half,
+                                             bool valid, int sig_off, int g_off, int j_off,
+                                             unsigned mask, bool jglobal) {
+  // each output's row is split in two halves on adjacent lanes (o, half 0/1),
+  // combined by one shuffle: 2 x outputs work items balance the CTA
+  constexpr int U = 4;
   double ag[G], aj[G][L];
 #pragma unroll
   for (int s = 0; s < G; ++s) {
@@ -109,10 +112,12 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
     dsig[s] = V.scr(s) + V.P.scr_dsig + sig_off;
   }
   const int n = D.n_out, nh = D.n_hidden;
+  const int hw = D.ell_w >> 1;
   // banded masks give contiguous hidden windows: entry e of output o is hidden
   // unit k0[o] + e (checked on the host; otherwise explicit indices)
-  const int k0 = D.ell_k0 ? __ldg(D.ell_k0 + o) : 0;
-  for (int e = 0; e < D.ell_w; e += U) {
+  const int k0 = valid && D.ell_k0 ? __ldg(D.ell_k0 + o) : 0;
+  const int e_lo = half * hw, e_hi = valid ? e_lo + hw : e_lo;
+  for (int e = e_lo; e < e_hi; e += U) {
     double v[U], t[U][G];
     int k[U];
 #pragma unroll
@@ -139,6 +144,14 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
       }
     }
   }
+  // combine the two halves (lanes 2j, 2j+1); half 0 writes
+#pragma unroll
+  for (int s = 0; s < G; ++s) {
+    ag[s] += __shfl_xor_sync(0xffffffffu, ag[s], 1);
+#pragma unroll
+    for (int d = 0; d < L; ++d) aj[s][d] += __shfl_xor_sync(0xffffffffu, aj[s][d], 1);
+  }
+  if (!valid || half) return;
   const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
 #pragma unroll
   for (int s = 0; s < G; ++s) {
@@ -164,78 +177,42 @@ __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ TileRec load_tile(const TileRec* t) {
-  TileRec r;
-  const int4* p = reinterpret_cast<const int4*>(t);
-  const int4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3), e = __ldg(p + 4);
-  r.o0 = a.x; r.cnt = a.y; r.kb_lo = a.z; r.kb_hi = a.w;
-  r.k0[0] = b.x; r.k0[1] = b.y; r.k0[2] = b.z; r.k0[3] = b.w;
-  r.k0[4] = c.x; r.k0[5] = c.y; r.k0[6] = c.z; r.k0[7] = c.w;
-  r.w[0] = d.x; r.w[1] = d.y; r.w[2] = d.z; r.w[3] = d.w;
-  r.w[4] = e.x; r.w[5] = e.y; r.w[6] = e.z; r.w[7] = e.w;
-  return r;
-}
-
+// Lean tensor-core tile: the host expands each tile's B-operand W2 values in
+// fragment order (vt[i][lane] = W2[o(lane)][4(kb_lo+i)+tig-k0(o)] or 0), the
+// sigma arrays are zero-padded past n_hidden, so the k-block loop is fully
+// unrolled with unconditional, coalesced loads at immediate offsets.
 template <int G, int L>
-__device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const TileRec& tile,
-                                           int sig_off, int g_off, int j_off, unsigned mask,
-                                           bool jglobal) {
-  constexpr int P = 8 / G;
+__device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const TileRec* tr,
+                                           const double* vt, int sig_off, int g_off, int j_off,
+                                           unsigned mask, bool jglobal) {
+  constexpr int KB = 10;
   const int lane = threadIdx.x & 31, tig = lane & 3, grp = lane >> 2;
-  const int o0 = tile.o0, cnt = tile.cnt & 0xff;
-  // B-operand column of this lane: col = grp -> (slot, output)
+  const int o0 = __ldg(&tr->o0), cnt = __ldg(&tr->cnt) & 0xff;
+  const int kb_lo = __ldg(&tr->kb_lo), nkb = __ldg(&tr->kb_hi) - kb_lo + 1;
   const int bmu = grp % G, bo = grp / G;
-  const bool bval = bo < cnt && ((mask >> bmu) & 1u);
-  int bk0 = tile.k0[0], bw = tile.w[0];
-#pragma unroll
-  for (int j = 1; j < P; ++j)
-    if (bo == j) { bk0 = tile.k0[j]; bw = tile.w[j]; }
-  const int bout = o0 + min(bo, cnt - 1);
-  const double* vrow = D.v_row + (size_t)bout * D.ell_w;
-  const double* sg = V.scr(bmu) + V.P.scr_sig + sig_off;
-  const double* dsg = V.scr(bmu) + V.P.scr_dsig + sig_off;
-  // all fragment loads of the tile first (independent), then the MMAs on
-  // three independent accumulator chains
-  constexpr int KB = 10;                        // window <= 24 + P + 3 -> <= 10 k-blocks
-  double a[KB], b[KB];
+  const double* ps = V.scr(bmu) + V.P.scr_dsig + sig_off + 4 * kb_lo + tig;
+  const double* ps0 = V.scr(bmu) + V.P.scr_sig + sig_off + 4 * kb_lo + tig;
+  const double* pa = D.w1frag + (size_t)kb_lo * 32 + lane;
+  const double* pv = vt + lane;
+  double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
   double gacc = 0.0;
-  const int nh1 = D.n_hidden - 1, ew1 = D.ell_w - 1;
-  // branch-free: every load has a valid (clamped) address, values are masked
 #pragma unroll
   for (int i = 0; i < KB; ++i) {
-    const bool kin = tile.kb_lo + i <= tile.kb_hi;
-    const int kb = min(tile.kb_lo + i, tile.kb_hi);
-    const double af = __ldg(D.w1frag + (size_t)kb * 32 + lane);
-    const int k = 4 * kb + tig;
-    const int e = k - bk0;
-    const bool ok = kin && bval && e >= 0 && e < bw;
-    const double vr = __ldg(vrow + min(max(e, 0), ew1));
-    const int kk = min(k, nh1);
-    const double sp = dsg[kk], s0 = sg[kk];
-    const double v = ok ? vr : 0.0;
-    a[i] = kin ? af : 0.0;
-    b[i] = v * sp;
-    gacc = fma(v, s0, gacc);
-  }
-  double c[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
-#pragma unroll
-  for (int i = 0; i < KB; ++i) {
-    if (tile.kb_lo + i <= tile.kb_hi) {
-      if (i % 3 == 0) dmma_884(c, a[i], b[i]);
-      else if (i % 3 == 1) dmma_884(c1, a[i], b[i]);
-      else dmma_884(c2, a[i], b[i]);
+    if (i < nkb) {
+      const double a = __ldg(pa + 32 * i);
+      const double v = __ldg(pv + 32 * i);
+      const double b = v * ps[4 * i];
+      gacc = fma(v, ps0[4 * i], gacc);
+      if (i & 1) dmma_884(c1, a, b); else dmma_884(c0, a, b);
     }
   }
-  c[0] = (c[0] + c1[0]) + c2[0];
-  c[1] = (c[1] + c1[1]) + c2[1];
-  // g: reduce the 4 k-lanes of each column
+  const double cc[2] = {c0[0] + c1[0], c0[1] + c1[1]};
   gacc += __shfl_xor_sync(0xffffffffu, gacc, 1);
   gacc += __shfl_xor_sync(0xffffffffu, gacc, 2);
-  if (tig == 0 && bval) {
-    const double scl = __ldg(D.scale + bout), sh = __ldg(D.shift + bout);
-    V.scr(bmu)[g_off + bout] = __dadd_rn(__dmul_rn(gacc, scl), sh);
+  if (tig == 0 && bo < cnt && ((mask >> bmu) & 1u)) {
+    const int o = o0 + bo;
+    V.scr(bmu)[g_off + o] = __dadd_rn(__dmul_rn(gacc, __ldg(D.scale + o)), __ldg(D.shift + o));
   }
-  // J: lane holds C[d = grp][cols 2 tig, 2 tig + 1]
   if (grp < L) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -243,10 +220,9 @@ __device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const
       const int mu = col % G, oo = col / G;
       if (oo < cnt && ((mask >> mu) & 1u)) {
         const int o = o0 + oo;
-        const double scl = __ldg(D.scale + o);
         double* jr = jglobal ? V.P.gJ + (size_t)(V.gslot0 + mu) * V.P.gJ_stride + (size_t)o * L
                              : V.scr(mu) + j_off + o * L;
-        jr[grp] = c[h] * scl;
+        jr[grp] = cc[h] * __ldg(D.scale + o);
       }
     }
   }
@@ -378,31 +354,39 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
     }
     // ---- phase B: outputs (+ Jacobian rows) ----
     if (P.map_kind == MAP_AE && B.tiles) {
-      // tensor-core sweep: warp per tile, next tile record prefetched
-      const int ntt = B.n_tiles;
-      int t = warp;
-      TileRec cur;
-      if (t < ntt) cur = load_tile(B.tiles + t);
-      for (; t < ntt; t += nw) {
-        TileRec nxt;
-        if (t + nw < ntt) nxt = load_tile(B.tiles + t + nw);
-        if ((cur.cnt >> 8) == 0)
-          sweep_tile<G, NI>(V, B.in, cur, 0, P.scr_gint, P.scr_jint, mask, P.scr_jint < 0);
+      // tensor-core sweep: warp per tile (interior tiles first, then interface)
+      const int ntt = B.n_tiles, nti = B.n_tiles_in;
+      for (int t = warp; t < ntt; t += nw) {
+        const double* vt = B.tile_v + (size_t)t * 10 * 32;
+        if (t < nti)
+          sweep_tile<G, NI>(V, B.in, B.tiles + t, vt, 0, P.scr_gint, P.scr_jint, mask,
+                            P.scr_jint < 0);
         else
-          sweep_tile<G, NG>(V, B.ga, cur, nhi, P.scr_ggam, P.scr_jgam, mask, false);
-        cur = nxt;
+          sweep_tile<G, NG>(V, B.ga, B.tiles + t, vt, nhi, P.scr_ggam, P.scr_jgam, mask, false);
       }
       __syncthreads();
       DDNM_MARK(V, 2);
     } else {
       const int noi = B.in.n_out, not_ = noi + B.ga.n_out;
-      for (int it = tid; it < not_; it += T) {
-        if (P.map_kind == MAP_AE) {
-          if (it < noi)
-            sweep_output<G, NI>(V, B.in, it, 0, P.scr_gint, P.scr_jint, mask, P.scr_jint < 0);
-          else
-            sweep_output<G, NG>(V, B.ga, it - noi, nhi, P.scr_ggam, P.scr_jgam, mask, false);
-        } else {
+      if (P.map_kind == MAP_AE) {
+        // half-row items on lane pairs; each decoder's item range is padded to
+        // whole warps so every warp runs one decoder (uniform shuffles)
+        const int ni2 = 2 * noi, ng2 = 2 * B.ga.n_out;
+        const int A = (ni2 + 31) & ~31, nit32 = A + ((ng2 + 31) & ~31);
+        for (int it = tid; it < nit32; it += T) {
+          if (it < A) {
+            const bool valid = it < ni2;
+            sweep_output<G, NI>(V, B.in, valid ? it >> 1 : 0, it & 1, valid, 0, P.scr_gint,
+                                P.scr_jint, mask, P.scr_jint < 0);
+          } else {
+            const int j = it - A;
+            const bool valid = j < ng2;
+            sweep_output<G, NG>(V, B.ga, valid ? j >> 1 : 0, j & 1, valid, nhi, P.scr_ggam,
+                                P.scr_jgam, mask, false);
+          }
+        }
+      } else for (int it = tid; it < not_; it += T) {
+        {
           if (it < noi)
             linear_output<G, NI>(V, B.in, it, B.xoff, P.scr_gint, mask);
           else
@@ -624,10 +608,11 @@ static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
       info = k + 1;
     }
     __syncwarp();
-    // rank-1 update of the trailing block, lanes over columns
-    for (int j = k + 1 + lane; j < n; j += WARP) {
-      const double ukj = K[k * ld + j];
-      for (int i = k + 1; i < n; ++i) K[i * ld + j] = fma(-K[i * ld + k], ukj, K[i * ld + j]);
+    // rank-1 update of the trailing block, lanes over (i, j) pairs
+    const int nt = n - k - 1;
+    for (int idx = lane; idx < nt * nt; idx += WARP) {
+      const int i = k + 1 + idx / nt, j = k + 1 + idx % nt;
+      K[i * ld + j] = fma(-K[i * ld + k], K[k * ld + j], K[i * ld + j]);
     }
     __syncwarp();
   }
@@ -637,6 +622,28 @@ static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
 // warp-level getrs: b <- inv(LU) P b, in place.
 static __device__ void warp_lu_solve(const double* K, int ld, int n, const int* piv, double* b) {
   const int lane = threadIdx.x & 31;
+  if (n <= WARP) {
+    // register version: lane i holds b_i
+    if (lane == 0)
+      for (int k = 0; k < n; ++k) {
+        const int p = piv[k];
+        if (p != k) { const double t = b[k]; b[k] = b[p]; b[p] = t; }
+      }
+    __syncwarp();
+    double bl = lane < n ? b[lane] : 0.0;
+    for (int k = 0; k < n; ++k) {
+      const double bk = __shfl_sync(0xffffffffu, bl, k);
+      if (lane > k && lane < n) bl = fma(-K[lane * ld + k], bk, bl);
+    }
+    for (int k = n - 1; k >= 0; --k) {
+      const double xk = __shfl_sync(0xffffffffu, bl, k) / K[k * ld + k];
+      if (lane == k) bl = xk;
+      if (lane < k) bl = fma(-K[lane * ld + k], xk, bl);
+    }
+    if (lane < n) b[lane] = bl;
+    __syncwarp();
+    return;
+  }
   if (lane == 0)
     for (int k = 0; k < n; ++k) {
       const int p = piv[k];
@@ -892,16 +899,17 @@ __device__ void kkt_block_forward(const Params& P, int b, const double* M, const
       const int p = piv[k];
       if (p != k) { const double t = y[k]; y[k] = y[p]; y[p] = t; }
     }
-  for (int c = lane; c < nC; c += WARP) tE[c] = 0.0;
   __syncwarp();
+  // lane i holds row i of [y_b; tE] (W + nC <= 32) across the steps
+  const int m = W + nC;
+  double yl = lane < W ? y[lane] : 0.0;
   for (int k = 0; k < W; ++k) {
-    const double yk = y[k];
-    for (int i = k + 1 + lane; i < W + nC; i += WARP) {
-      if (i < W) y[i] = fma(-M[i * ld + k], yk, y[i]);
-      else tE[i - W] = fma(-M[i * ld + k], yk, tE[i - W]);
-    }
-    __syncwarp();
+    const double yk = __shfl_sync(0xffffffffu, yl, k);
+    if (lane > k && lane < m) yl = fma(-M[lane * ld + k], yk, yl);
   }
+  if (lane < W) y[lane] = yl;
+  else if (lane < m) tE[lane - W] = yl;
+  __syncwarp();
 }
 
 // back substitution of block b given the multiplier part xE
@@ -916,13 +924,16 @@ __device__ void kkt_block_backward(const Params& P, const double* M, double* y, 
     y[i] = v;
   }
   __syncwarp();
+  // column-oriented back substitution; the diagonal division is done by every
+  // lane from registers (no lane-0 round trip through shared memory)
+  double yl = lane < W ? y[lane] : 0.0;
   for (int k = W - 1; k >= 0; --k) {
-    if (lane == 0) y[k] = y[k] / M[k * ld + k];
-    __syncwarp();
-    const double xk = y[k];
-    for (int i = lane; i < k; i += WARP) y[i] = fma(-M[i * ld + k], xk, y[i]);
-    __syncwarp();
+    const double xk = __shfl_sync(0xffffffffu, yl, k) / M[k * ld + k];
+    if (lane == k) yl = xk;
+    if (lane < k) yl = fma(-M[lane * ld + k], xk, yl);
   }
+  if (lane < W) y[lane] = yl;
+  __syncwarp();
 }
 
 // CTA-wide KKT stage for every slot in kmask (eval buffer ebi[s]).
@@ -936,13 +947,14 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const KktLayout L = kkt_layout<NI, NG>(P);
   const int nC = P.n_C, nb = P.nb;
-  if (tid < G) kflag[tid] = 1;
+  // the register-resident substitutions need one lane per block-system row
+  if (tid < G) kflag[tid] = (W + nC <= WARP) ? 1 : 0;
   __syncthreads();
   DDNM_MARK(V, 12);
   // 1. per-block elimination
   for (int t = warp; t < G * nb; t += nw) {
     const int s = t / nb, b = t - s * nb;
-    if (!((kmask >> s) & 1u)) continue;
+    if (!((kmask >> s) & 1u) || !kflag[s]) continue;
     double* sc = V.scr(s);
     const bool ok = kkt_block_factor<NI, NG>(P, V.eb(s, ebi[s]), b, sc + b * L.msz,
                                              reinterpret_cast<int*>(sc + L.off_piv) + b * W);
@@ -1211,6 +1223,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS) k_solve(const __grid_constan
   if (tid == 0) { s_evals = 0; s_kkts = 0; }
   if (tid < 16) s_prof[tid] = 0;
   if (P.prof) V.prof = s_prof;
+  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
   __syncthreads();
   if (tid == 0) s_prof[15] = clock64();
   const SqpCfg& cfg = P.cfg;
