@@ -84,6 +84,7 @@ struct ddnm_ctx {
   std::vector<void*> allocs;  // weights, tables
   double* gbv = nullptr;      // boundary values per global slot
   double* gJ = nullptr;       // interior Jacobian rows per global slot
+  double* gJg = nullptr;      // interface Jacobian rows per global slot
   size_t gbv_slots = 0;
   int* work = nullptr;
   unsigned long long* counters = nullptr;
@@ -235,9 +236,10 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
   int rc;
   if (kind == DDNM_MAP_AUTOENCODER) {
     const size_t nnz = (size_t)h.indptr[h.n_out];
-    std::vector<double> w1t((size_t)h.n_hidden * lat);
+    d.ldw = h.n_hidden + 32;
+    std::vector<double> w1t((size_t)d.ldw * lat, 0.0);
     for (int k = 0; k < h.n_hidden; ++k)
-      for (int dd = 0; dd < lat; ++dd) w1t[(size_t)dd * h.n_hidden + k] = h.W1[(size_t)k * lat + dd];
+      for (int dd = 0; dd < lat; ++dd) w1t[(size_t)dd * d.ldw + k] = h.W1[(size_t)k * lat + dd];
     if ((rc = upload(c, w1t.data(), w1t.size(), const_cast<double**>(&d.W1t)))) return rc;
     d.W1 = nullptr;
     if ((rc = upload(c, h.b1, (size_t)h.n_hidden, const_cast<double**>(&d.b1)))) return rc;
@@ -441,14 +443,16 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   const bool ae = a->map_kind == DDNM_MAP_AUTOENCODER;
   // per-slot scratch plan; the interior Jacobian rows stay in shared memory
   // when they fit, otherwise they go to a per-slot L2 scratch (gJ)
-  auto plan_scratch = [&](bool jint_smem) {
+  // level 0: both Jacobian row sets in shared memory; 1: interface rows in L2;
+  // 2: both in L2 (per-slot global scratch)
+  auto plan_scratch = [&](int level) {
     int scr = 0;
-    P.scr_sig = scr; scr += ae ? max_nh + 8 : 0;     // +8: zero padding read by the
-    P.scr_dsig = scr; scr += ae ? max_nh + 8 : 0;    // tensor-core sweep past n_hidden
+    P.scr_sig = scr; scr += ae ? max_nh + 32 : 0;    // +32: zero padding read past
+    P.scr_dsig = scr; scr += ae ? max_nh + 32 : 0;   // n_hidden by the sweeps
     P.scr_gint = scr; scr += max_io;
-    if (ae && jint_smem) { P.scr_jint = scr; scr += max_io * ni; } else { P.scr_jint = -1; }
+    if (ae && level < 2) { P.scr_jint = scr; scr += max_io * ni; } else { P.scr_jint = -1; }
     P.scr_ggam = scr; scr += max_gam;
-    P.scr_jgam = scr; scr += ae ? max_gam * ng : 0;
+    if (ae && level < 1) { P.scr_jgam = scr; scr += max_gam * ng; } else { P.scr_jgam = -1; }
     // R and r are produced after the sweep has consumed sigma/sigma': alias them
     if (ae && max_rows * (W + 1) <= 2 * max_nh) {
       P.scr_R = P.scr_sig;
@@ -459,9 +463,10 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     }
     return scr;
   };
-  int scr = plan_scratch(true);
+  int scr = plan_scratch(0);
   P.gJ_stride = ae ? max_io * ni : 0;
-  const int kkt_need = std::max(P.nK * (P.nK + 1) + 5 * P.nK,
+  P.gJg_stride = ae ? max_gam * ng : 0;
+  const int kkt_need = std::max(P.nK * (P.nK + 1) + 6 * P.nK,
                                 P.nb * (W + P.n_C) * (W + P.n_C + 1) + P.nb * W +
                                     P.n_C * (P.n_C + 1) + P.n_C + P.nb * P.n_C + 4 * P.nK);
   const int ls_need = P.nb * ng * P.n_C + P.nb * ng;
@@ -476,24 +481,24 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // preferring the interior Jacobian rows in shared memory
   const size_t smem_cap = (size_t)prop.sharedMemPerBlockOptin - 1024;
   const int rbf_need2 = rbf_need;
-  auto scr_total = [&](bool jsm) {
-    int s0 = plan_scratch(jsm);
+  auto scr_total = [&](int level) {
+    int s0 = plan_scratch(level);
     int t = std::max(std::max(s0, kkt_need), std::max(ls_need, rbf_need2));
     return (t + 1) & ~1;
   };
-  auto footprint = [&](int G, bool jsm) {
-    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + scr_total(jsm))) * 8;
+  auto footprint = [&](int G, int level) {
+    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + scr_total(level))) * 8;
   };
   const Kernels* kern = nullptr;
-  bool kern_jsm = true;
-  for (int pass = 0; pass < 2 && !kern; ++pass) {
-    const bool jsm = pass == 0;
-    if (!jsm && !ae) break;
+  int kern_level = 0;
+  const char* jl = getenv("DDNM_JLEVEL");
+  const int lvl_lo = jl ? atoi(jl) : 0, lvl_hi = jl ? atoi(jl) : (ae ? 2 : 0);
+  for (int level = lvl_lo; level <= lvl_hi; ++level) {
     for (const auto& k : kernel_table()) {
       if (k.ni != ni || k.ng != ng) continue;
       if (slots > 0 && k.g != slots) continue;
-      if (footprint(k.g, jsm) > smem_cap) continue;
-      if (!kern || k.g > kern->g) { kern = &k; kern_jsm = jsm; }
+      if (footprint(k.g, level) > smem_cap) continue;
+      if (!kern || k.g > kern->g) { kern = &k; kern_level = level; }
     }
   }
   if (!kern) {
@@ -502,10 +507,10 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
              ni, ng, slots, smem_cap);
     return bail(fail(DDNM_EUNSUPPORTED, buf));
   }
-  P.scr_size = scr_total(kern_jsm);
+  P.scr_size = scr_total(kern_level);
   c->K = *kern;
   // tiles of consecutive outputs for the tensor-core sweep (P = 8 / G outputs each)
-  if (getenv("DDNM_DMMA") && ae) {
+  if (getenv("DDNM_DMMA") && ae && 8 % kern->g == 0) {
     const int Pt = 8 / kern->g;
     for (int b = 0; b < P.nb; ++b) {
       if (hwin[2 * b].k0.empty() || hwin[2 * b + 1].k0.empty()) continue;
@@ -563,7 +568,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.sm_vec = state_d * P.G;
   P.sm_eb = P.sm_vec + P.G * 8 * P.nK;
   P.sm_scr = P.sm_eb + P.G * 2 * P.eb_size;
-  c->smem = footprint(P.G, kern_jsm);
+  c->smem = footprint(P.G, kern_level);
   if (cudaFuncSetAttribute(kern->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
       cudaFuncSetAttribute(kern->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cannot reserve dynamic shared memory"));
@@ -586,6 +591,7 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   for (auto& kv : c->io) cudaFree(kv.second.first);
   if (c->gbv) cudaFree(c->gbv);
   if (c->gJ) cudaFree(c->gJ);
+  if (c->gJg) cudaFree(c->gJg);
   if (c->work) cudaFree(c->work);
   if (c->counters) cudaFree(c->counters);
   if (c->prof) cudaFree(c->prof);
@@ -622,6 +628,9 @@ static int ensure_gbv(ddnm_ctx* c, size_t slots) {
   slots = std::max<size_t>(slots, 1);
   CUDA_TRY(cudaMalloc(&c->gbv, slots * c->tot_rows * 3 * sizeof(double)));
   CUDA_TRY(cudaMalloc(&c->gJ, slots * std::max(c->P.gJ_stride, 1) * sizeof(double)));
+  if (c->gJg) cudaFree(c->gJg);
+  c->gJg = nullptr;
+  CUDA_TRY(cudaMalloc(&c->gJg, slots * std::max(c->P.gJg_stride, 1) * sizeof(double)));
   c->gbv_slots = slots;
   return 0;
 }
@@ -665,6 +674,7 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
   P.so.n_iter = o->n_iter; P.so.n_evals = o->n_evals; P.so.status = o->status; P.so.n_reg = o->n_reg;
   P.gbv = c->gbv;
   P.gJ = c->gJ;
+  P.gJg = c->gJg;
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
@@ -803,6 +813,7 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
   P.eval_step = (o->step || o->kkt_status) ? 1 : 0;
   P.gbv = c->gbv;
   P.gJ = c->gJ;
+  P.gJg = c->gJg;
   P.work = c->work;
   P.counters = c->counters;
   void* args[] = {&P};

@@ -38,7 +38,8 @@ enum Status { ST_OK = 0, ST_LINE_SEARCH = 1, ST_KKT_SINGULAR = 2, ST_LSTSQ_RANK 
 struct DecDev {
   int n_out, n_hidden;
   const double* W1;       // LINEAR: Phi [n_out][lat]  (AE: unused on device)
-  const double* W1t;      // AE: W1 transposed [lat][n_hidden] (coalesced per latent column)
+  const double* W1t;      // AE: W1 transposed [lat][ldw] (coalesced per latent column),
+  int ldw;                //     ldw = n_hidden + 32, zero padded
   const double* b1;       // [n_hidden]
   const int* indptr;      // [n_out+1]
   const int* indices;     // [nnz]
@@ -152,6 +153,8 @@ struct Params {
   double* gbv;            // per global slot [total_rows][3] boundary values
   double* gJ;             // per global slot interior-decoder Jacobian rows [n_io][n_int]
   int gJ_stride;
+  double* gJg;            // per global slot interface-decoder Jacobian rows [N_gam][n_gam]
+  int gJg_stride;
   int* work;              // [0]: next mu; [1]: finished CTAs
   unsigned long long* counters;  // [0] block-evals, [1] KKT solves
   unsigned long long* prof;      // [15] per-phase clock totals (DDNM_PROF=1), or null

@@ -28,6 +28,13 @@ struct View {
   __device__ double* vec(int s, int which) const { return ddnm_smem + P.sm_vec + (s * 8 + which) * P.nK; }
   __device__ double* eb(int s, int which) const { return ddnm_smem + P.sm_eb + (s * 2 + which) * P.eb_size; }
   __device__ double* scr(int s) const { return ddnm_smem + P.sm_scr + s * P.scr_size; }
+  // decoder Jacobian rows: shared memory when they fit, else per-slot L2 scratch
+  __device__ double* jint(int s) const {
+    return P.scr_jint >= 0 ? scr(s) + P.scr_jint : P.gJ + (size_t)(gslot0 + s) * P.gJ_stride;
+  }
+  __device__ double* jgam(int s) const {
+    return P.scr_jgam >= 0 ? scr(s) + P.scr_jgam : P.gJg + (size_t)(gslot0 + s) * P.gJg_stride;
+  }
 };
 
 // phase timing (device-side profiler, off unless Params::prof is set)
@@ -67,7 +74,7 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
                                             int sig_off, unsigned mask) {
   double w[L];
 #pragma unroll
-  for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1t + (size_t)d * D.n_hidden + k);
+  for (int d = 0; d < L; ++d) w[d] = __ldg(D.W1t + (size_t)d * D.ldw + k);
   const double b = __ldg(D.b1 + k);
 #pragma unroll
   for (int s = 0; s < G; ++s) {
@@ -90,20 +97,20 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
 // read consecutive addresses), four entries per batch so their index, weight
 // and W1-row loads are all in flight together:
 //   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e W2_e act'_e W1[k_e, d]) * scale
-template <int G, int L>
-__device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int half,
-                                             bool valid, int sig_off, int g_off, int j_off,
-                                             unsigned mask, bool jglobal) {
-  // each output's row is split in two halves on adjacent lanes (o, half 0/1),
-  // combined by one shuffle: 2 x outputs work items balance the CTA
-  constexpr int U = 4;
-  double ag[G], aj[G][L];
+template <int G, int L, int NQ>
+__device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int q,
+                                             bool valid, int sig_off, int g_off, bool gam,
+                                             unsigned mask) {
+  // NQ lanes per output (q = lane % NQ) take the row's entries interleaved
+  // (e = NQ i + q): a warp covers 32/NQ consecutive outputs, so its W1 /
+  // sigma reads fall in few hidden windows per instruction.  The NQ partial
+  // sums are combined by a reduce-scatter (each lane finishes 1/NQ of them).
+  static_assert(NQ == 2 || NQ == 4, "2 or 4 lanes per output");
+  constexpr int NV = G * (L + 1);            // values per output: per slot g, J_0..J_{L-1}
+  constexpr int NV4 = (NV + NQ - 1) / NQ * NQ;
+  double val[NV4];
 #pragma unroll
-  for (int s = 0; s < G; ++s) {
-    ag[s] = 0.0;
-#pragma unroll
-    for (int d = 0; d < L; ++d) aj[s][d] = 0.0;
-  }
+  for (int j = 0; j < NV4; ++j) val[j] = 0.0;
   const double* sig[G];
   const double* dsig[G];
 #pragma unroll
@@ -112,56 +119,115 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
     dsig[s] = V.scr(s) + V.P.scr_dsig + sig_off;
   }
   const int n = D.n_out, nh = D.n_hidden;
-  const int hw = D.ell_w >> 1;
-  // banded masks give contiguous hidden windows: entry e of output o is hidden
-  // unit k0[o] + e (checked on the host; otherwise explicit indices)
   const int k0 = valid && D.ell_k0 ? __ldg(D.ell_k0 + o) : 0;
-  const int e_lo = half * hw, e_hi = valid ? e_lo + hw : e_lo;
-  for (int e = e_lo; e < e_hi; e += U) {
-    double v[U], t[U][G];
-    int k[U];
+  if (NQ == 2 && D.ell_k0 && D.ell_w == 24) {
+    // fast path (banded rows of <= 24 entries): fully unrolled, hoisted base
+    // pointers, no clamps (W1^T and sigma are zero-padded past n_hidden and
+    // padded W2 entries are 0); inactive slots compute on stale finite data
+    // and are never written back
+    const double* pv = D.ell_v + (size_t)q * n + o;
+    const double* pw = D.W1t + k0 + q;
+    const int ldw = D.ldw;
+    const double* ps[G];
+    const double* pd[G];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      v[u] = __ldg(D.ell_v + (size_t)(e + u) * n + o);
-      k[u] = D.ell_k0 ? min(k0 + e + u, nh - 1) : __ldg(D.ell_k + (size_t)(e + u) * n + o);
-    }
+    for (int s = 0; s < G; ++s) { ps[s] = sig[s] + k0 + q; pd[s] = dsig[s] + k0 + q; }
+    const size_t n2 = 2 * (size_t)n;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int i = 0; i < 12; ++i) {
+      const double v = valid ? __ldg(pv + i * n2) : 0.0;
+      double t[G];
 #pragma unroll
       for (int s = 0; s < G; ++s) {
-        if (!((mask >> s) & 1u)) { t[u][s] = 0.0; continue; }
-        ag[s] = fma(v[u], sig[s][k[u]], ag[s]);
-        t[u][s] = v[u] * dsig[s][k[u]];
+        val[s * (L + 1)] = fma(v, ps[s][2 * i], val[s * (L + 1)]);
+        t[s] = v * pd[s][2 * i];
       }
 #pragma unroll
-    for (int d = 0; d < L; ++d) {
-      const double* w1 = D.W1t + (size_t)d * nh;
+      for (int d = 0; d < L; ++d) {
+        const double w = __ldg(pw + d * ldw + 2 * i);
+#pragma unroll
+        for (int s = 0; s < G; ++s) val[s * (L + 1) + 1 + d] = fma(t[s], w, val[s * (L + 1) + 1 + d]);
+      }
+    }
+  } else {
+    constexpr int U = NQ == 2 ? 4 : 3;
+    const int i_hi = valid ? D.ell_w / NQ : 0;      // ell_w is a multiple of 8
+    for (int i0 = 0; i0 < i_hi; i0 += U) {
+      double v[U], t[U][G];
+      int k[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const double w = __ldg(w1 + k[u]);
+        const int e = min(NQ * (i0 + u) + q, D.ell_w - 1);
+        const bool ok = i0 + u < i_hi;
+        v[u] = ok ? __ldg(D.ell_v + (size_t)e * n + o) : 0.0;
+        k[u] = D.ell_k0 ? min(k0 + e, nh - 1) : __ldg(D.ell_k + (size_t)e * n + o);
+      }
 #pragma unroll
-        for (int s = 0; s < G; ++s) aj[s][d] = fma(t[u][s], w, aj[s][d]);
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < G; ++s) {
+          if (!((mask >> s) & 1u)) { t[u][s] = 0.0; continue; }
+          val[s * (L + 1)] = fma(v[u], sig[s][k[u]], val[s * (L + 1)]);
+          t[u][s] = v[u] * dsig[s][k[u]];
+        }
+#pragma unroll
+      for (int d = 0; d < L; ++d) {
+        const double* w1 = D.W1t + (size_t)d * D.ldw;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double w = __ldg(w1 + k[u]);
+#pragma unroll
+          for (int s = 0; s < G; ++s) val[s * (L + 1) + 1 + d] = fma(t[u][s], w, val[s * (L + 1) + 1 + d]);
+        }
       }
     }
   }
-  // combine the two halves (lanes 2j, 2j+1); half 0 writes
+  // reduce-scatter over the NQ lanes of an output
+  double r2[NV4 / NQ];
+  const bool hi1 = (q & 1) != 0;
+  int base;
+  if constexpr (NQ == 4) {
+    constexpr int H = NV4 / 2, Q = NV4 / 4;
+    const bool hi2 = (q & 2) != 0;
+    double r1[H];
 #pragma unroll
-  for (int s = 0; s < G; ++s) {
-    ag[s] += __shfl_xor_sync(0xffffffffu, ag[s], 1);
+    for (int j = 0; j < H; ++j) {
+      const double send = hi2 ? val[j] : val[H + j];
+      const double mine = hi2 ? val[H + j] : val[j];
+      r1[j] = mine + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
 #pragma unroll
-    for (int d = 0; d < L; ++d) aj[s][d] += __shfl_xor_sync(0xffffffffu, aj[s][d], 1);
+    for (int j = 0; j < Q; ++j) {
+      const double send = hi1 ? r1[j] : r1[Q + j];
+      const double mine = hi1 ? r1[Q + j] : r1[j];
+      r2[j] = mine + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    base = (hi2 ? H : 0) + (hi1 ? Q : 0);
+  } else {
+    constexpr int H = NV4 / 2;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const double send = hi1 ? val[j] : val[H + j];
+      const double mine = hi1 ? val[H + j] : val[j];
+      r2[j] = mine + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    base = hi1 ? H : 0;
   }
-  if (!valid || half) return;
-  const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
+  if (!valid) return;
+  // lane q now holds values [base, base + NV4 / NQ)
+  const double scl = __ldg(D.scale + o);
 #pragma unroll
-  for (int s = 0; s < G; ++s) {
+  for (int j = 0; j < NV4 / NQ; ++j) {
+    const int idx = base + j;
+    if (idx >= NV) continue;
+    const int s = idx / (L + 1), r = idx - s * (L + 1);
     if (!((mask >> s) & 1u)) continue;
-    double* sc = V.scr(s);
-    sc[g_off + o] = __dadd_rn(__dmul_rn(ag[s], scl), sh);
-    double* jr = jglobal ? V.P.gJ + (size_t)(V.gslot0 + s) * V.P.gJ_stride + (size_t)o * L
-                         : sc + j_off + o * L;
-#pragma unroll
-    for (int d = 0; d < L; ++d) jr[d] = aj[s][d] * scl;
+    if (r == 0) {
+      V.scr(s)[g_off + o] = __dadd_rn(__dmul_rn(r2[j], scl), __ldg(D.shift + o));
+    } else {
+      double* jr = (gam ? V.jgam(s) : V.jint(s)) + (size_t)o * L;
+      jr[r - 1] = r2[j] * scl;
+    }
   }
 }
 
@@ -183,8 +249,8 @@ __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
 // unrolled with unconditional, coalesced loads at immediate offsets.
 template <int G, int L>
 __device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const TileRec* tr,
-                                           const double* vt, int sig_off, int g_off, int j_off,
-                                           unsigned mask, bool jglobal) {
+                                           const double* vt, int sig_off, int g_off, bool gam,
+                                           unsigned mask) {
   constexpr int KB = 10;
   const int lane = threadIdx.x & 31, tig = lane & 3, grp = lane >> 2;
   const int o0 = __ldg(&tr->o0), cnt = __ldg(&tr->cnt) & 0xff;
@@ -220,8 +286,7 @@ __device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const
       const int mu = col % G, oo = col / G;
       if (oo < cnt && ((mask >> mu) & 1u)) {
         const int o = o0 + oo;
-        double* jr = jglobal ? V.P.gJ + (size_t)(V.gslot0 + mu) * V.P.gJ_stride + (size_t)o * L
-                             : V.scr(mu) + j_off + o * L;
+        double* jr = (gam ? V.jgam(mu) : V.jint(mu)) + (size_t)o * L;
         jr[grp] = cc[h] * __ldg(D.scale + o);
       }
     }
@@ -256,10 +321,8 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
   const double* gint = sc + P.scr_gint;
   const double* ggam = sc + P.scr_ggam;
   const bool lin = P.map_kind == MAP_LINEAR;
-  const double* Jint = lin ? B.in.W1
-                           : (P.scr_jint < 0 ? P.gJ + (size_t)(V.gslot0 + s) * P.gJ_stride
-                                             : sc + P.scr_jint);  // [n_io][NI]
-  const double* Jgam = lin ? B.ga.W1 : sc + P.scr_jgam;   // [N_gam][NG]
+  const double* Jint = lin ? B.in.W1 : V.jint(s);   // [n_io][NI]
+  const double* Jgam = lin ? B.ga.W1 : V.jgam(s);   // [N_gam][NG]
   const StRows& RW = B.rows;
   const int nr = B.nrows;
   auto val = [&](int c) -> double {
@@ -359,30 +422,30 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       for (int t = warp; t < ntt; t += nw) {
         const double* vt = B.tile_v + (size_t)t * 10 * 32;
         if (t < nti)
-          sweep_tile<G, NI>(V, B.in, B.tiles + t, vt, 0, P.scr_gint, P.scr_jint, mask,
-                            P.scr_jint < 0);
+          sweep_tile<G, NI>(V, B.in, B.tiles + t, vt, 0, P.scr_gint, false, mask);
         else
-          sweep_tile<G, NG>(V, B.ga, B.tiles + t, vt, nhi, P.scr_ggam, P.scr_jgam, mask, false);
+          sweep_tile<G, NG>(V, B.ga, B.tiles + t, vt, nhi, P.scr_ggam, true, mask);
       }
       __syncthreads();
       DDNM_MARK(V, 2);
     } else {
       const int noi = B.in.n_out, not_ = noi + B.ga.n_out;
       if (P.map_kind == MAP_AE) {
-        // half-row items on lane pairs; each decoder's item range is padded to
-        // whole warps so every warp runs one decoder (uniform shuffles)
-        const int ni2 = 2 * noi, ng2 = 2 * B.ga.n_out;
-        const int A = (ni2 + 31) & ~31, nit32 = A + ((ng2 + 31) & ~31);
+        // NQ lanes per output; each decoder's item range is padded to whole
+        // warps so every warp runs one decoder (uniform shuffles)
+        constexpr int NQ = 2;
+        const int niq = NQ * noi, ngq = NQ * B.ga.n_out;
+        const int A = (niq + 31) & ~31, nit32 = A + ((ngq + 31) & ~31);
         for (int it = tid; it < nit32; it += T) {
           if (it < A) {
-            const bool valid = it < ni2;
-            sweep_output<G, NI>(V, B.in, valid ? it >> 1 : 0, it & 1, valid, 0, P.scr_gint,
-                                P.scr_jint, mask, P.scr_jint < 0);
+            const bool valid = it < niq;
+            sweep_output<G, NI, NQ>(V, B.in, valid ? it / NQ : 0, it % NQ, valid, 0, P.scr_gint,
+                                    false, mask);
           } else {
             const int j = it - A;
-            const bool valid = j < ng2;
-            sweep_output<G, NG>(V, B.ga, valid ? j >> 1 : 0, j & 1, valid, nhi, P.scr_ggam,
-                                P.scr_jgam, mask, false);
+            const bool valid = j < ngq;
+            sweep_output<G, NG, NQ>(V, B.ga, valid ? j / NQ : 0, j % NQ, valid, nhi, P.scr_ggam,
+                                    true, mask);
           }
         }
       } else for (int it = tid; it < not_; it += T) {
@@ -408,7 +471,7 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         const bool act = t < nct && ((mask >> s) & 1u);
         const double* sc = V.scr(s);
         const double* gg = sc + P.scr_ggam;
-        const double* Jg = P.map_kind == MAP_LINEAR ? B.ga.W1 : sc + P.scr_jgam;
+        const double* Jg = P.map_kind == MAP_LINEAR ? B.ga.W1 : V.jgam(s);
         const double* ca = B.CA + (size_t)c * ngo;
         double a0 = 0.0, aj[NG];
 #pragma unroll
@@ -451,10 +514,8 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         const size_t mu = (size_t)st[s].mu;
         const double* sc = V.scr(s);
         const bool lin = P.map_kind == MAP_LINEAR;
-        const double* Jint = lin ? B.in.W1
-                                 : (P.scr_jint < 0 ? P.gJ + (size_t)(gslot0 + s) * P.gJ_stride
-                                                   : sc + P.scr_jint);
-        const double* Jgam = lin ? B.ga.W1 : sc + P.scr_jgam;
+        const double* Jint = lin ? B.in.W1 : V.jint(s);
+        const double* Jgam = lin ? B.ga.W1 : V.jgam(s);
         if (o.int_g)
           for (int i = tid; i < B.in.n_out; i += T) o.int_g[mu * P.tot_iout + B.iout_off + i] = sc[P.scr_gint + i];
         if (o.int_J)
@@ -609,10 +670,9 @@ static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
     }
     __syncwarp();
     // rank-1 update of the trailing block, lanes over (i, j) pairs
-    const int nt = n - k - 1;
-    for (int idx = lane; idx < nt * nt; idx += WARP) {
-      const int i = k + 1 + idx / nt, j = k + 1 + idx % nt;
-      K[i * ld + j] = fma(-K[i * ld + k], K[k * ld + j], K[i * ld + j]);
+    for (int j = k + 1 + lane; j < n; j += WARP) {
+      const double ukj = K[k * ld + j];
+      for (int i = k + 1; i < n; ++i) K[i * ld + j] = fma(-K[i * ld + k], ukj, K[i * ld + j]);
     }
     __syncwarp();
   }
@@ -785,6 +845,156 @@ __device__ int warp_kkt(const Params& P, const double* e, double* work, double* 
   return 2;
 }
 
+// CTA-cooperative assemble_and_solve_kkt (sqp.py:162-208) for one slot: dense
+// K, LU with partial pivoting (getf2 semantics: first-max pivot, scaling by
+// the reciprocal), one refinement step, the 1e-10 back-substitution check and
+// the +delta*I retry.  Pivot search and triangular solves on warp 0; swaps,
+// multipliers and rank-1 updates on all threads (3 barriers per column).
+// Returns 0 ok, 1 ok after regularization, 2 singular.  Used when the block-
+// structured path does not apply (e.g. LS-ROM, where multiplier rows win
+// pivots).
+template <int NI, int NG>
+__device__ int cta_kkt(const Params& P, const double* e, double* work, double* sol) {
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int W = NI + NG;
+  const int n = P.nK, ld = n + 1;
+  double* K = work;
+  int* piv = reinterpret_cast<int*>(work + (size_t)n * ld);
+  double* rhs = work + (size_t)n * ld + n;
+  double* res = rhs + n;
+  double* tmp = res + n;
+  double* lbuf = tmp + 2 * n;  // multipliers of the current column (sol is at tmp + n)
+  __shared__ double s_pval, s_kk, s_rp, s_rhsn, s_delta;
+  __shared__ int s_p, s_ret, s_fin;
+  for (int i = tid; i < n; i += T) rhs[i] = -(i < P.n_D ? e[P.eb_rho + i] : e[P.eb_con + i - P.n_D]);
+  __syncthreads();
+  if (warp == 0) {
+    double ss = 0.0;
+    for (int i = lane; i < n; i += WARP) ss = fma(rhs[i], rhs[i], ss);
+    ss = warp_sum(ss);
+    if (lane == 0) {
+      s_rhsn = fmax(sqrt(ss), 1e-300);
+      double tr = 0.0;
+      for (int b = 0; b < P.nb; ++b)
+        for (int i = 0; i < W; ++i) tr = tr + hval(eb_H(const_cast<double*>(e), P.blk[b]), W, i, i);
+      s_delta = P.cfg.reg_scale * fmax(tr, 1.0);
+      s_ret = 2;
+    }
+  }
+  __syncthreads();
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const double delta = attempt == 0 ? 0.0 : s_delta;
+    for (int i = warp; i < n; i += (T >> 5))
+    for (int j = lane; j < n; j += WARP) {
+      double v = 0.0;
+      if (i < P.n_D && j < P.n_D) {
+        const int bi = i / W, bj = j / W;
+        if (bi == bj) v = hval(eb_H(const_cast<double*>(e), P.blk[bi]), W, i - bi * W, j - bj * W);
+        if (i == j) v += delta;
+      } else if (i < P.n_D && j >= P.n_D) {
+        const int b = i / W, li = i - b * W;
+        if (li >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(j - P.n_D) * NG + (li - NI)];
+      } else if (i >= P.n_D && j < P.n_D) {
+        const int b = j / W, lj = j - b * W;
+        if (lj >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(i - P.n_D) * NG + (lj - NI)];
+      }
+      K[i * ld + j] = v;
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = n;
+        for (int i = k + lane; i < n; i += WARP) {
+          const double a = fabs(K[i * ld + k]);
+          if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) {
+          piv[k] = bi;
+          s_p = bi;
+          const double pv = K[bi * ld + k];
+          s_pval = pv;
+          s_kk = K[k * ld + k];
+          s_rp = pv != 0.0 && fabs(pv) >= 2.2250738585072014e-308 ? 1.0 / pv : 0.0;
+        }
+      }
+      __syncthreads();
+      const int p = s_p;
+      const double pv = s_pval, rp = s_rp;
+      // swap rows k and p (all columns but k), column k: pivot + multipliers
+      if (p != k)
+        for (int j = tid; j < n; j += T) {
+          if (j == k) continue;
+          const double t = K[k * ld + j];
+          K[k * ld + j] = K[p * ld + j];
+          K[p * ld + j] = t;
+        }
+      for (int i = k + tid; i < n; i += T) {
+        double v = i == p ? s_kk : K[i * ld + k];
+        if (i == k) v = pv;
+        if (i > k && pv != 0.0) v = rp != 0.0 ? v * rp : v / pv;
+        K[i * ld + k] = v;
+        lbuf[i] = v;
+      }
+      __syncthreads();
+      if (pv != 0.0) {
+        // rows over warps, columns over lanes (no index division)
+        const int nw = T >> 5;
+        for (int j = k + 1 + lane; j < n; j += WARP) {
+          const double ukj = K[k * ld + j];
+          for (int i = k + 1 + warp; i < n; i += nw) K[i * ld + j] = fma(-lbuf[i], ukj, K[i * ld + j]);
+        }
+      }
+      __syncthreads();
+    }
+    // solve, one refinement, check (warp 0)
+    if (warp == 0) {
+      for (int i = lane; i < n; i += WARP) sol[i] = rhs[i];
+      __syncwarp();
+      warp_lu_solve(K, ld, n, piv, sol);
+      bool finite = true;
+      for (int i = lane; i < n; i += WARP) finite = finite && isfinite(sol[i]);
+      finite = __all_sync(0xffffffffu, finite);
+      double rel = INFINITY;
+      if (finite) {
+        kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
+        for (int i = lane; i < n; i += WARP) res[i] = rhs[i] - tmp[i];
+        __syncwarp();
+        warp_lu_solve(K, ld, n, piv, res);
+        for (int i = lane; i < n; i += WARP) sol[i] += res[i];
+        __syncwarp();
+        finite = true;
+        for (int i = lane; i < n; i += WARP) finite = finite && isfinite(sol[i]);
+        finite = __all_sync(0xffffffffu, finite);
+        if (finite) {
+          kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
+          double r2 = 0.0;
+          for (int i = lane; i < n; i += WARP) {
+            const double d = rhs[i] - tmp[i];
+            r2 = fma(d, d, r2);
+          }
+          r2 = warp_sum(r2);
+          rel = sqrt(r2) / s_rhsn;
+        }
+      }
+      if (lane == 0) s_fin = rel <= 1e-10 ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_fin) {
+      const int r = attempt;
+      __syncthreads();
+      return r;
+    }
+  }
+  return 2;
+}
+
 // ---------------------------------------------------------------------------
 // Block-structured KKT LU (fast path of assemble_and_solve_kkt).
 //
@@ -876,10 +1086,10 @@ __device__ bool kkt_block_factor(const Params& P, const double* e, int b, double
       for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] /= pv;
     }
     __syncwarp();
-    const int nt = m - k - 1;
-    for (int idx = lane; idx < nt * nt; idx += WARP) {
-      const int i = k + 1 + idx / nt, j = k + 1 + idx % nt;
-      M[i * ld + j] = fma(-M[i * ld + k], M[k * ld + j], M[i * ld + j]);
+    // lanes over columns; the column-k multipliers are read before any write
+    for (int j = k + 1 + lane; j < m; j += WARP) {
+      const double ukj = M[k * ld + j];
+      for (int i = k + 1; i < m; ++i) M[i * ld + j] = fma(-M[i * ld + k], ukj, M[i * ld + j]);
     }
     __syncwarp();
   }
@@ -1065,19 +1275,22 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     __syncthreads();
     DDNM_MARK(V, 11);
   }
-  // 4. dense fallback (reference semantics incl. the +delta*I retry)
-  if (warp < G && ((kmask >> warp) & 1u) && !kflag[warp]) {
-    const int s = warp;
-    double* work = V.scr(s);
+  // 4. dense fallback (reference semantics incl. the +delta*I retry), one
+  // slot at a time with the whole CTA
+  for (int ss = 0; ss < G; ++ss) {
+    if (!((kmask >> ss) & 1u) || kflag[ss]) continue;   // uniform (shared flags)
+    double* work = V.scr(ss);
     double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
-    const int r = warp_kkt<NI, NG>(P, V.eb(s, ebi[s]), work, sol);
-    if (r != 2) {
-      for (int j = lane; j < P.n_D; j += WARP) V.vec(s, 2)[j] = sol[j];
-      for (int c = lane; c < nC; c += WARP) V.vec(s, 3)[c] = sol[P.n_D + c];
+    const int r = cta_kkt<NI, NG>(P, V.eb(ss, ebi[ss]), work, sol);
+    if (warp == 0) {
+      if (r != 2) {
+        for (int j = lane; j < P.n_D; j += WARP) V.vec(ss, 2)[j] = sol[j];
+        for (int c = lane; c < nC; c += WARP) V.vec(ss, 3)[c] = sol[P.n_D + c];
+      }
+      if (lane == 0) kres[ss] = r;
     }
-    if (lane == 0) kres[s] = r;
+    __syncthreads();
   }
-  __syncthreads();
   DDNM_MARK(V, 13);
 }
 

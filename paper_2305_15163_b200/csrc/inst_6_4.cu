@@ -10,6 +10,8 @@ void register_6_4(std::vector<KernelEntry>& t) {
                           (const void*)&k_eval<1, 6, 4>});
   t.push_back(KernelEntry{6, 4, 2, (const void*)&k_solve<2, 6, 4>,
                           (const void*)&k_eval<2, 6, 4>});
+  t.push_back(KernelEntry{6, 4, 3, (const void*)&k_solve<3, 6, 4>,
+                          (const void*)&k_eval<3, 6, 4>});
   t.push_back(KernelEntry{6, 4, 4, (const void*)&k_solve<4, 6, 4>,
                           (const void*)&k_eval<4, 6, 4>});
 }

@@ -16,6 +16,7 @@ mu = P.seeded_parameters(B, seed=1000)
 for _ in range(2):
     r = P.solve_rom_batch(inst, mu, slots=slots)
 ctx = inst.context(-1, slots)
+print(f"slots/CTA {ctx.info.slots_per_cta}, CTAs {ctx.info.ctas}, smem {ctx.info.smem_bytes} B")
 prof = ctx.profile()
 tot = sum(prof.values()) or 1
 print({k: f"{100 * v / tot:.1f}%" for k, v in prof.items()})
