@@ -133,7 +133,7 @@ int io_buf(ddnm_ctx* c, const std::string& name, size_t bytes, void** p) {
 
 // RestrictedResidual rows (partition.py:361-425) in local-column form, SoA.
 struct HostRows {
-  std::vector<int> gu, gv, nent, bflags, col;
+  std::vector<int> gu, gv, nent, bflags, col, src, sgu, sgv;
   std::vector<double> bxc, byc, cdc, xc, yc;
 };
 
@@ -198,6 +198,14 @@ int build_stencil(const ddnm_artifacts* a, const ddnm_block& blk, HostRows& out)
     out.xc[r] = -1.0 + hx * (i + 1);
     out.yc[r] = hy * (j + 1);
   }
+  // source codes: interior outputs keep their index, interface outputs map
+  // through gio to -1 - position
+  auto code = [&](int c) { return c < blk.n_io ? c : -1 - (int)blk.gio[c - blk.n_io]; };
+  out.src.resize(out.col.size());
+  for (size_t q = 0; q < out.col.size(); ++q) out.src[q] = code(out.col[q]);
+  out.sgu.resize(nr);
+  out.sgv.resize(nr);
+  for (int r = 0; r < nr; ++r) { out.sgu[r] = code(out.gu[r]); out.sgv[r] = code(out.gv[r]); }
   return 0;
 }
 
@@ -401,6 +409,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
         (rc = upload(c, hr.nent.data(), hr.nent.size(), const_cast<int**>(&R.nent))) ||
         (rc = upload(c, hr.bflags.data(), hr.bflags.size(), const_cast<int**>(&R.bflags))) ||
         (rc = upload(c, hr.col.data(), hr.col.size(), const_cast<int**>(&R.col))) ||
+        (rc = upload(c, hr.src.data(), hr.src.size(), const_cast<int**>(&R.src))) ||
+        (rc = upload(c, hr.sgu.data(), hr.sgu.size(), const_cast<int**>(&R.src_gu))) ||
+        (rc = upload(c, hr.sgv.data(), hr.sgv.size(), const_cast<int**>(&R.src_gv))) ||
         (rc = upload(c, hr.bxc.data(), hr.bxc.size(), const_cast<double**>(&R.bxc))) ||
         (rc = upload(c, hr.byc.data(), hr.byc.size(), const_cast<double**>(&R.byc))) ||
         (rc = upload(c, hr.cdc.data(), hr.cdc.size(), const_cast<double**>(&R.cdc))) ||

@@ -75,7 +75,10 @@ struct StRows {
   const int* gv;          // local position of v_p
   const int* nent;        // distinct local columns referenced (<= 6)
   const int* bflags;      // bit0 left, bit1 right, bit2 bottom, bit3 top, bit4 v-row
-  const int* col;         // [MAXE][n_rows]
+  const int* col;         // [MAXE][n_rows] local columns
+  const int* src;         // [MAXE][n_rows] source codes: >= 0 interior output, < 0: -1 - interface output
+  const int* src_gu;      // source codes of u_p and v_p
+  const int* src_gv;
   const double* bxc;      // [MAXE][n_rows]
   const double* byc;
   const double* cdc;

@@ -325,16 +325,16 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
   const double* Jgam = lin ? B.ga.W1 : V.jgam(s);   // [N_gam][NG]
   const StRows& RW = B.rows;
   const int nr = B.nrows;
-  auto val = [&](int c) -> double {
-    return c < B.n_io ? gint[c] : ggam[__ldg(B.gio + (c - B.n_io))];
-  };
+  // source codes (host-precomputed): c >= 0 -> interior output c,
+  // c < 0 -> interface output -1 - c (no gio lookups on the device)
+  auto val = [&](int c) -> double { return c >= 0 ? gint[c] : ggam[-1 - c]; };
   const int ne = __ldg(RW.nent + row);
-  const int gu = __ldg(RW.gu + row), gv = __ldg(RW.gv + row);
+  const int gu = __ldg(RW.src_gu + row), gv = __ldg(RW.src_gv + row);
   int cl[MAXE];
   double bxc[MAXE], byc[MAXE], cdc[MAXE], xe[MAXE];
 #pragma unroll
   for (int e = 0; e < MAXE; ++e) {
-    cl[e] = __ldg(RW.col + e * nr + row);
+    cl[e] = __ldg(RW.src + e * nr + row);
     bxc[e] = __ldg(RW.bxc + e * nr + row);
     byc[e] = __ldg(RW.byc + e * nr + row);
     cdc[e] = __ldg(RW.cdc + e * nr + row);
@@ -370,12 +370,12 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
       if (bxc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xu, bxc[e]));
       if (byc[e] != 0.0) j = __dadd_rn(j, __dmul_rn(xv, byc[e]));
       if (cdc[e] != 0.0) j = __dadd_rn(j, cdc[e]);
-      if (c < B.n_io) {
+      if (c >= 0) {
         const double* jr = Jint + (size_t)c * NI;
 #pragma unroll
         for (int d = 0; d < NI; ++d) Ri[d] = fma(j, jr[d], Ri[d]);
       } else {
-        const double* jr = Jgam + (size_t)__ldg(B.gio + (c - B.n_io)) * NG;
+        const double* jr = Jgam + (size_t)(-1 - c) * NG;
 #pragma unroll
         for (int d = 0; d < NG; ++d) Rg[d] = fma(j, jr[d], Rg[d]);
       }
@@ -1666,6 +1666,8 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS) k_eval(const __grid_constant
   const int gslot0 = blockIdx.x * G;
   __shared__ int s_ebi[G];
   __shared__ unsigned s_mask;
+  // finite (zero) padding past n_hidden for the sweeps
+  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
   if (tid == 0) {
     unsigned m = 0;
     for (int s = 0; s < G; ++s) {
