@@ -660,7 +660,7 @@ static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
         }
       __syncwarp();
       if (fabs(pv) >= 2.2250738585072014e-308) {
-        const double r = 1.0 / pv;
+        const double r = rcp_fast(pv);
         for (int i = k + 1 + lane; i < n; i += WARP) K[i * ld + k] *= r;
       } else {
         for (int i = k + 1 + lane; i < n; i += WARP) K[i * ld + k] /= pv;
@@ -696,7 +696,7 @@ static __device__ void warp_lu_solve(const double* K, int ld, int n, const int* 
       if (lane > k && lane < n) bl = fma(-K[lane * ld + k], bk, bl);
     }
     for (int k = n - 1; k >= 0; --k) {
-      const double xk = __shfl_sync(0xffffffffu, bl, k) / K[k * ld + k];
+      const double xk = __shfl_sync(0xffffffffu, bl, k) * rcp_fast(K[k * ld + k]);
       if (lane == k) bl = xk;
       if (lane < k) bl = fma(-K[lane * ld + k], xk, bl);
     }
@@ -1080,7 +1080,7 @@ __device__ bool kkt_block_factor(const Params& P, const double* e, int b, double
     __syncwarp();
     const double pv = M[k * ld + k];
     if (fabs(pv) >= 2.2250738585072014e-308) {
-      const double r = 1.0 / pv;
+      const double r = rcp_fast(pv);
       for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] *= r;
     } else {
       for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] /= pv;
@@ -1138,7 +1138,7 @@ __device__ void kkt_block_backward(const Params& P, const double* M, double* y, 
   // lane from registers (no lane-0 round trip through shared memory)
   double yl = lane < W ? y[lane] : 0.0;
   for (int k = W - 1; k >= 0; --k) {
-    const double xk = __shfl_sync(0xffffffffu, yl, k) / M[k * ld + k];
+    const double xk = __shfl_sync(0xffffffffu, yl, k) * rcp_fast(M[k * ld + k]);
     if (lane == k) yl = xk;
     if (lane < k) yl = fma(-M[lane * ld + k], xk, yl);
   }
