@@ -285,7 +285,9 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev
     hw.k0.clear();
     hw.w.clear();
     if (ew > 0) {
-      if ((rc = upload(c, ev.data(), ev.size(), const_cast<double**>(&d.ell_v)))) return rc;
+      ev.push_back(0.0);   // spare zero for masked-out lanes
+    if ((rc = upload(c, ev.data(), ev.size(), const_cast<double**>(&d.ell_v)))) return rc;
+    d.ell_zero = d.ell_v + ev.size() - 1;
       if (contig) {
         if ((rc = upload(c, k0.data(), k0.size(), const_cast<int**>(&d.ell_k0)))) return rc;
         // tensor-core sweep tables: W1 in A-fragment order, rows contiguous

@@ -48,6 +48,7 @@ struct DecDev {
   const double* shift;    // [n_out]
   int ell_w;              // ELL width (max nnz per row, padded to 8)
   const double* ell_v;    // [ell_w][n_out] W2 values in storage order, 0-padded
+  const double* ell_zero; // 1 zero double (target of masked-out lanes)
   const int* ell_k;       // [ell_w][n_out] hidden indices, 0-padded (null if contiguous)
   const int* ell_k0;      // [n_out] first hidden index when every row's window is contiguous
   // DMMA sweep (contiguous windows only): W1 in mma.m8n8k4 A-fragment order,

@@ -125,26 +125,30 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
     // pointers, no clamps (W1^T and sigma are zero-padded past n_hidden and
     // padded W2 entries are 0); inactive slots compute on stale finite data
     // and are never written back
-    const double* pv = D.ell_v + (size_t)q * n + o;
+    // invalid lanes read the all-zero padding row (ell_v has one spare row)
+    const double* pv = valid ? D.ell_v + (size_t)q * n + o : D.ell_zero;
+    const int vstep = valid ? 2 * n : 0;
     const double* pw = D.W1t + k0 + q;
     const int ldw = D.ldw;
     const double* ps[G];
     const double* pd[G];
 #pragma unroll
     for (int s = 0; s < G; ++s) { ps[s] = sig[s] + k0 + q; pd[s] = dsig[s] + k0 + q; }
-    const size_t n2 = 2 * (size_t)n;
 #pragma unroll
     for (int i = 0; i < 12; ++i) {
-      const double v = valid ? __ldg(pv + i * n2) : 0.0;
+      const double v = __ldg(pv);
+      pv += vstep;
       double t[G];
 #pragma unroll
       for (int s = 0; s < G; ++s) {
         val[s * (L + 1)] = fma(v, ps[s][2 * i], val[s * (L + 1)]);
         t[s] = v * pd[s][2 * i];
       }
+      const double* pwi = pw + 2 * i;
 #pragma unroll
       for (int d = 0; d < L; ++d) {
-        const double w = __ldg(pw + d * ldw + 2 * i);
+        const double w = __ldg(pwi);
+        pwi += ldw;
 #pragma unroll
         for (int s = 0; s < G; ++s) val[s * (L + 1) + 1 + d] = fma(t[s], w, val[s * (L + 1) + 1 + d]);
       }
