@@ -857,9 +857,105 @@ __device__ int warp_kkt(const Params& P, const double* e, double* work, double* 
 // Returns 0 ok, 1 ok after regularization, 2 singular.  Used when the block-
 // structured path does not apply (e.g. LS-ROM, where multiplier rows win
 // pivots).
+// CTA-wide getrs with LU factors in K (ld) and pivots piv: b <- inv(LU) P b.
+// Blocks of 32 rows: warp 0 solves the diagonal block in registers, every
+// warp then applies its off-diagonal update (one thread per remaining row).
+static __device__ void cta_lu_solve(const double* K, int ld, int n, const int* piv, double* b) {
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0)
+    for (int k = 0; k < n; ++k) {
+      const int p = piv[k];
+      if (p != k) { const double t = b[k]; b[k] = b[p]; b[p] = t; }
+    }
+  __syncthreads();
+  for (int b0 = 0; b0 < n; b0 += WARP) {           // unit lower
+    const int nb = min(WARP, n - b0);
+    if (warp == 0) {
+      double y = lane < nb ? b[b0 + lane] : 0.0;
+      for (int k = 0; k < nb; ++k) {
+        const double yk = __shfl_sync(0xffffffffu, y, k);
+        if (lane > k && lane < nb) y = fma(-K[(b0 + lane) * ld + b0 + k], yk, y);
+      }
+      if (lane < nb) b[b0 + lane] = y;
+    }
+    __syncthreads();
+    for (int i = b0 + nb + tid; i < n; i += T) {
+      const double* Lr = K + i * ld + b0;
+      double a0 = 0.0, a1 = 0.0;
+      int k = 0;
+      for (; k + 1 < nb; k += 2) { a0 = fma(Lr[k], b[b0 + k], a0); a1 = fma(Lr[k + 1], b[b0 + k + 1], a1); }
+      if (k < nb) a0 = fma(Lr[k], b[b0 + k], a0);
+      b[i] -= a0 + a1;
+    }
+    __syncthreads();
+  }
+  for (int b1 = n; b1 > 0; b1 -= WARP) {           // upper
+    const int b0 = max(0, b1 - WARP), nb = b1 - b0;
+    if (warp == 0) {
+      double z = lane < nb ? b[b0 + lane] : 0.0;
+      for (int k = nb - 1; k >= 0; --k) {
+        const double xk = __shfl_sync(0xffffffffu, z, k) * rcp_fast(K[(b0 + k) * ld + b0 + k]);
+        if (lane == k) z = xk;
+        if (lane < k) z = fma(-K[(b0 + lane) * ld + b0 + k], xk, z);
+      }
+      if (lane < nb) b[b0 + lane] = z;
+    }
+    __syncthreads();
+    for (int i = tid; i < b0; i += T) {
+      const double* Ur = K + i * ld + b0;
+      double a0 = 0.0, a1 = 0.0;
+      int k = 0;
+      for (; k + 1 < nb; k += 2) { a0 = fma(Ur[k], b[b0 + k], a0); a1 = fma(Ur[k + 1], b[b0 + k + 1], a1); }
+      if (k < nb) a0 = fma(Ur[k], b[b0 + k], a0);
+      b[i] -= a0 + a1;
+    }
+    __syncthreads();
+  }
+}
+
+// y = K x (compact blockdiag H + delta I, E, E^T), one thread per row
+template <int NI, int NG>
+__device__ void cta_kkt_matvec(const Params& P, const double* e, double delta, const double* x,
+                               double* y) {
+  constexpr int W = NI + NG;
+  for (int i = threadIdx.x; i < P.nK; i += blockDim.x) {
+    double v = 0.0;
+    if (i < P.n_D) {
+      const int b = i / W, li = i - b * W;
+      const BlockDev& B = P.blk[b];
+      const double* H = eb_H(const_cast<double*>(e), B);
+      const double* xb = x + b * W;
+      for (int j = 0; j < W; ++j) v = fma(hval(H, W, li, j), xb[j], v);
+      if (delta != 0.0) v = fma(delta, x[i], v);
+      if (li >= NI) {
+        const double* cj = eb_cjac(const_cast<double*>(e), B, P.n_C);
+        for (int c = 0; c < P.n_C; ++c) v = fma(cj[c * NG + (li - NI)], x[P.n_D + c], v);
+      }
+    } else {
+      const int c = i - P.n_D;
+      for (int b = 0; b < P.nb; ++b) {
+        const double* cj = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C) + c * NG;
+        const double* xb = x + b * W + NI;
+        for (int d = 0; d < NG; ++d) v = fma(cj[d], xb[d], v);
+      }
+    }
+    y[i] = v;
+  }
+}
+
+// CTA-cooperative assemble_and_solve_kkt (sqp.py:162-208) for one slot: dense
+// K, LU with partial pivoting (getf2 semantics: first-max pivot, scaling by
+// the reciprocal), one refinement step, the 1e-10 back-substitution check and
+// the +delta*I retry.  Per column: the pivot of column k+1 is reduced from
+// per-warp partial maxima gathered during column k's rank-1 update; swaps,
+// multipliers and updates use all threads; solves are blocked (cta_lu_solve).
+// Returns 0 ok, 1 ok after regularization, 2 singular.  Used when the block-
+// structured path does not apply (e.g. LS-ROM, where multiplier rows win
+// pivots).
 template <int NI, int NG>
 __device__ int cta_kkt(const Params& P, const double* e, double* work, double* sol) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = T >> 5;
   constexpr int W = NI + NG;
   const int n = P.nK, ld = n + 1;
   double* K = work;
@@ -868,8 +964,8 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
   double* res = rhs + n;
   double* tmp = res + n;
   double* lbuf = tmp + 2 * n;  // multipliers of the current column (sol is at tmp + n)
-  __shared__ double s_pval, s_kk, s_rp, s_rhsn, s_delta;
-  __shared__ int s_p, s_ret, s_fin;
+  __shared__ double s_pval, s_kk, s_rp, s_rhsn, s_delta, s_wmax[32], s_red[32];
+  __shared__ int s_p, s_fin, s_widx[32];
   for (int i = tid; i < n; i += T) rhs[i] = -(i < P.n_D ? e[P.eb_rho + i] : e[P.eb_con + i - P.n_D]);
   __syncthreads();
   if (warp == 0) {
@@ -882,37 +978,45 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
       for (int b = 0; b < P.nb; ++b)
         for (int i = 0; i < W; ++i) tr = tr + hval(eb_H(const_cast<double*>(e), P.blk[b]), W, i, i);
       s_delta = P.cfg.reg_scale * fmax(tr, 1.0);
-      s_ret = 2;
     }
   }
   __syncthreads();
   for (int attempt = 0; attempt < 2; ++attempt) {
     const double delta = attempt == 0 ? 0.0 : s_delta;
-    for (int i = warp; i < n; i += (T >> 5))
-    for (int j = lane; j < n; j += WARP) {
-      double v = 0.0;
-      if (i < P.n_D && j < P.n_D) {
-        const int bi = i / W, bj = j / W;
-        if (bi == bj) v = hval(eb_H(const_cast<double*>(e), P.blk[bi]), W, i - bi * W, j - bj * W);
-        if (i == j) v += delta;
-      } else if (i < P.n_D && j >= P.n_D) {
-        const int b = i / W, li = i - b * W;
-        if (li >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(j - P.n_D) * NG + (li - NI)];
-      } else if (i >= P.n_D && j < P.n_D) {
-        const int b = j / W, lj = j - b * W;
-        if (lj >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(i - P.n_D) * NG + (lj - NI)];
+    for (int i = warp; i < n; i += nw)
+      for (int j = lane; j < n; j += WARP) {
+        double v = 0.0;
+        if (i < P.n_D && j < P.n_D) {
+          const int bi = i / W, bj = j / W;
+          if (bi == bj) v = hval(eb_H(const_cast<double*>(e), P.blk[bi]), W, i - bi * W, j - bj * W);
+          if (i == j) v += delta;
+        } else if (i < P.n_D && j >= P.n_D) {
+          const int b = i / W, li = i - b * W;
+          if (li >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(j - P.n_D) * NG + (li - NI)];
+        } else if (i >= P.n_D && j < P.n_D) {
+          const int b = j / W, lj = j - b * W;
+          if (lj >= NI) v = eb_cjac(const_cast<double*>(e), P.blk[b], P.n_C)[(i - P.n_D) * NG + (lj - NI)];
+        }
+        K[i * ld + j] = v;
       }
-      K[i * ld + j] = v;
+    __syncthreads();
+    // column-0 pivot candidates: per-warp partial maxima
+    {
+      double best = -1.0;
+      int bi = n;
+      for (int i = warp; i < n; i += nw) {     // lane 0 of each warp scans its rows
+        if (lane == 0) {
+          const double a = fabs(K[i * ld]);
+          if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+        }
+      }
+      if (lane == 0) { s_wmax[warp] = best; s_widx[warp] = bi; }
     }
     __syncthreads();
     for (int k = 0; k < n; ++k) {
       if (warp == 0) {
-        double best = -1.0;
-        int bi = n;
-        for (int i = k + lane; i < n; i += WARP) {
-          const double a = fabs(K[i * ld + k]);
-          if (a > best || (a == best && i < bi)) { best = a; bi = i; }
-        }
+        double best = lane < nw ? s_wmax[lane] : -1.0;
+        int bi = lane < nw ? s_widx[lane] : n;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -925,7 +1029,7 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
           const double pv = K[bi * ld + k];
           s_pval = pv;
           s_kk = K[k * ld + k];
-          s_rp = pv != 0.0 && fabs(pv) >= 2.2250738585072014e-308 ? 1.0 / pv : 0.0;
+          s_rp = pv != 0.0 && fabs(pv) >= 2.2250738585072014e-308 ? rcp_fast(pv) : 0.0;
         }
       }
       __syncthreads();
@@ -947,54 +1051,72 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
         lbuf[i] = v;
       }
       __syncthreads();
+      // rank-1 update; lane 0 of each warp owns column k+1 and tracks its
+      // pivot candidates (first max over its rows)
+      double best = -1.0;
+      int bi = n;
       if (pv != 0.0) {
-        // rows over warps, columns over lanes (no index division)
-        const int nw = T >> 5;
         for (int j = k + 1 + lane; j < n; j += WARP) {
           const double ukj = K[k * ld + j];
-          for (int i = k + 1 + warp; i < n; i += nw) K[i * ld + j] = fma(-lbuf[i], ukj, K[i * ld + j]);
-        }
-      }
-      __syncthreads();
-    }
-    // solve, one refinement, check (warp 0)
-    if (warp == 0) {
-      for (int i = lane; i < n; i += WARP) sol[i] = rhs[i];
-      __syncwarp();
-      warp_lu_solve(K, ld, n, piv, sol);
-      bool finite = true;
-      for (int i = lane; i < n; i += WARP) finite = finite && isfinite(sol[i]);
-      finite = __all_sync(0xffffffffu, finite);
-      double rel = INFINITY;
-      if (finite) {
-        kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
-        for (int i = lane; i < n; i += WARP) res[i] = rhs[i] - tmp[i];
-        __syncwarp();
-        warp_lu_solve(K, ld, n, piv, res);
-        for (int i = lane; i < n; i += WARP) sol[i] += res[i];
-        __syncwarp();
-        finite = true;
-        for (int i = lane; i < n; i += WARP) finite = finite && isfinite(sol[i]);
-        finite = __all_sync(0xffffffffu, finite);
-        if (finite) {
-          kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
-          double r2 = 0.0;
-          for (int i = lane; i < n; i += WARP) {
-            const double d = rhs[i] - tmp[i];
-            r2 = fma(d, d, r2);
+          for (int i = k + 1 + warp; i < n; i += nw) {
+            const double v = fma(-lbuf[i], ukj, K[i * ld + j]);
+            K[i * ld + j] = v;
+            if (j == k + 1) {
+              const double a = fabs(v);
+              if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+            }
           }
-          r2 = warp_sum(r2);
-          rel = sqrt(r2) / s_rhsn;
+        }
+      } else if (lane == 0) {
+        for (int i = k + 1 + warp; i < n; i += nw) {
+          const double a = fabs(K[i * ld + k + 1]);
+          if (a > best || (a == best && i < bi)) { best = a; bi = i; }
         }
       }
-      if (lane == 0) s_fin = rel <= 1e-10 ? 1 : 0;
-    }
-    __syncthreads();
-    if (s_fin) {
-      const int r = attempt;
+      if (lane == 0) { s_wmax[warp] = best; s_widx[warp] = bi; }
       __syncthreads();
-      return r;
     }
+    // solve, one refinement, check (sqp.py:175-189)
+    for (int i = tid; i < n; i += T) sol[i] = rhs[i];
+    __syncthreads();
+    cta_lu_solve(K, ld, n, piv, sol);
+    int fin = 1;
+    for (int i = tid; i < n; i += T) fin &= isfinite(sol[i]) ? 1 : 0;
+    fin = __syncthreads_and(fin);
+    double rel = INFINITY;
+    if (fin) {
+      cta_kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
+      __syncthreads();
+      for (int i = tid; i < n; i += T) res[i] = rhs[i] - tmp[i];
+      __syncthreads();
+      cta_lu_solve(K, ld, n, piv, res);
+      for (int i = tid; i < n; i += T) sol[i] += res[i];
+      __syncthreads();
+      fin = 1;
+      for (int i = tid; i < n; i += T) fin &= isfinite(sol[i]) ? 1 : 0;
+      fin = __syncthreads_and(fin);
+      if (fin) {
+        cta_kkt_matvec<NI, NG>(P, e, delta, sol, tmp);
+        __syncthreads();
+        double r2 = 0.0;
+        for (int i = tid; i < n; i += T) {
+          const double d = rhs[i] - tmp[i];
+          r2 = fma(d, d, r2);
+        }
+        r2 = warp_sum(r2);
+        if (lane == 0) s_red[warp] = r2;
+        __syncthreads();
+        if (tid == 0) {
+          double t = 0.0;
+          for (int w = 0; w < nw; ++w) t += s_red[w];
+          s_fin = sqrt(t) / s_rhsn <= 1e-10 ? 1 : 0;
+        }
+        __syncthreads();
+        rel = s_fin ? 0.0 : INFINITY;
+      }
+    }
+    if (rel <= 1e-10) return attempt;
+    __syncthreads();
   }
   return 2;
 }
