@@ -410,6 +410,12 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
     // ---- phase A: hidden layer of both decoders ----
     if (P.map_kind == MAP_AE) {
       const int nht = nhi + B.ga.n_hidden;
+      // the sweeps read up to 32 entries past the last hidden unit: keep that
+      // padding zero (the region is reused by R / KKT scratch between rounds)
+      for (int it = tid; it < G * 64; it += T) {
+        const int s = it >> 6, z = it & 63;
+        if ((mask >> s) & 1u) V.scr(s)[(z < 32 ? P.scr_sig : P.scr_dsig) + nht + (z & 31)] = 0.0;
+      }
       for (int it = tid; it < nht; it += T) {
         if (it < nhi)
           hidden_unit<G, NI>(V, B.in, it, B.xoff, 0, mask);
