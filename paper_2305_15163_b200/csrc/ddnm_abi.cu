@@ -506,7 +506,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   int kern_level = 0;
   const char* jl = getenv("DDNM_JLEVEL");
   const int lvl_lo = jl ? atoi(jl) : 0, lvl_hi = jl ? atoi(jl) : (ae ? 2 : 0);
-  for (int level = lvl_lo; level <= lvl_hi; ++level) {
+  // lowest level that fits wins (measured: 2 slots with both Jacobian row sets
+  // in shared memory beat 3-4 slots with rows in L2), largest G within it
+  for (int level = lvl_lo; level <= lvl_hi && !kern; ++level) {
     for (const auto& k : kernel_table()) {
       if (k.ni != ni || k.ng != ng) continue;
       if (slots > 0 && k.g != slots) continue;

@@ -682,7 +682,18 @@ static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
     // rank-1 update of the trailing block, lanes over (i, j) pairs
     for (int j = k + 1 + lane; j < n; j += WARP) {
       const double ukj = K[k * ld + j];
-      for (int i = k + 1; i < n; ++i) K[i * ld + j] = fma(-K[i * ld + k], ukj, K[i * ld + j]);
+      int i = k + 1;
+      for (; i + 4 <= n; i += 4) {
+        const double l0 = K[i * ld + k], l1 = K[(i + 1) * ld + k];
+        const double l2 = K[(i + 2) * ld + k], l3 = K[(i + 3) * ld + k];
+        const double a0 = K[i * ld + j], a1 = K[(i + 1) * ld + j];
+        const double a2 = K[(i + 2) * ld + j], a3 = K[(i + 3) * ld + j];
+        K[i * ld + j] = fma(-l0, ukj, a0);
+        K[(i + 1) * ld + j] = fma(-l1, ukj, a1);
+        K[(i + 2) * ld + j] = fma(-l2, ukj, a2);
+        K[(i + 3) * ld + j] = fma(-l3, ukj, a3);
+      }
+      for (; i < n; ++i) K[i * ld + j] = fma(-K[i * ld + k], ukj, K[i * ld + j]);
     }
     __syncwarp();
   }
@@ -1218,10 +1229,22 @@ __device__ bool kkt_block_factor(const Params& P, const double* e, int b, double
       for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] /= pv;
     }
     __syncwarp();
-    // lanes over columns; the column-k multipliers are read before any write
+    // lanes over columns; each lane loads its column's rows and the column-k
+    // multipliers 4 at a time before storing (no load-after-store stalls)
     for (int j = k + 1 + lane; j < m; j += WARP) {
       const double ukj = M[k * ld + j];
-      for (int i = k + 1; i < m; ++i) M[i * ld + j] = fma(-M[i * ld + k], ukj, M[i * ld + j]);
+      int i = k + 1;
+      for (; i + 4 <= m; i += 4) {
+        const double l0 = M[i * ld + k], l1 = M[(i + 1) * ld + k];
+        const double l2 = M[(i + 2) * ld + k], l3 = M[(i + 3) * ld + k];
+        const double a0 = M[i * ld + j], a1 = M[(i + 1) * ld + j];
+        const double a2 = M[(i + 2) * ld + j], a3 = M[(i + 3) * ld + j];
+        M[i * ld + j] = fma(-l0, ukj, a0);
+        M[(i + 1) * ld + j] = fma(-l1, ukj, a1);
+        M[(i + 2) * ld + j] = fma(-l2, ukj, a2);
+        M[(i + 3) * ld + j] = fma(-l3, ukj, a3);
+      }
+      for (; i < m; ++i) M[i * ld + j] = fma(-M[i * ld + k], ukj, M[i * ld + j]);
     }
     __syncwarp();
   }
