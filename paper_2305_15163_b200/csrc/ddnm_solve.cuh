@@ -186,6 +186,23 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
       }
     }
   }
+  if constexpr (NQ == 2 && G % 2 == 0) {
+    // all-reduce over the lane pair; lane q writes the slots s with s % 2 == q
+    // (static register indices, no per-value index arithmetic)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) val[j] += __shfl_xor_sync(0xffffffffu, val[j], 1);
+    if (!valid) return;
+    const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
+#pragma unroll
+    for (int s = 0; s < G; ++s) {
+      if ((s & 1) != q || !((mask >> s) & 1u)) continue;
+      V.scr(s)[g_off + o] = __dadd_rn(__dmul_rn(val[s * (L + 1)], scl), sh);
+      double* jr = (gam ? V.jgam(s) : V.jint(s)) + (size_t)o * L;
+#pragma unroll
+      for (int d = 0; d < L; ++d) jr[d] = val[s * (L + 1) + 1 + d] * scl;
+    }
+    return;
+  }
   // reduce-scatter over the NQ lanes of an output
   double r2[NV4 / NQ];
   const bool hi1 = (q & 1) != 0;
