@@ -222,6 +222,33 @@ int ddnm_last_counters(const ddnm_ctx* ctx, int64_t* evals, int64_t* kkts);
  * machine, [7] KKT, [8..15] reserved.  All zero when profiling is off. */
 int ddnm_last_profile(const ddnm_ctx* ctx, uint64_t* cycles16);
 
+/* ---- full decode (RomInstance.decode, driver.py:148-152) ---------------- */
+
+/* Register the full interior maps: interior[b] is block b's whole interior
+ * decoder (n_out = all interior dofs; the ddnm_block carries only its HR
+ * restriction), same latent dim, map kind and activation as the artifacts.
+ * The interface map of block b is the block's `interface` decoder. */
+int ddnm_ctx_set_full_decoders(ddnm_ctx* ctx, const ddnm_decoder* interior);
+
+/* Length of one decoded state: sum over blocks of (interior n_out + N_Gamma),
+ * laid out [blk0 interior | blk0 interface | blk1 interior | ...] -- the
+ * flattened list of (x_int, x_gam) pairs RomInstance.decode returns. */
+int ddnm_ctx_state_len(const ddnm_ctx* ctx, int64_t* len);
+
+/* Decode B latent solutions x[B][n_D] into states[B][state_len] (NULL: not
+ * stored).  fom (NULL allowed) holds restrict_blocks (driver.py:477-480) of a
+ * FOM state per mu in the same layout; then err[B] = relative_error
+ * (driver.py:496-507), NaN where a reference block has zero norm (the
+ * reference raises ValueError there).  fom and err are both NULL or both set.
+ * Host pointers, synchronous. */
+int ddnm_decode_batch(ddnm_ctx* ctx, int32_t B, const double* x,
+                      const double* fom, double* states, double* err);
+
+/* Same with device pointers, asynchronous on `stream` (NULL: context stream). */
+int ddnm_decode_batch_device(ddnm_ctx* ctx, int32_t B, const double* d_x,
+                             const double* d_fom, double* d_states,
+                             double* d_err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

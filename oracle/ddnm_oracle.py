@@ -363,6 +363,33 @@ class Instance:
                                         for b in self.blocks])[:-1]
         self.n_primal = int(sum(b.n_int + b.n_gam for b in self.blocks))
         self.rbf = {k[4:]: d[k] for k in d if k.startswith("rbf_")}
+        # full interior maps + dof columns for decode / restrict (optional keys)
+        self.full_interior = []
+        self.cols = []
+        for b in range(m["nblocks"]):
+            p = f"b{b}_"
+            if p + "int_cols" not in d:
+                self.full_interior = None
+                break
+            if self.kind == "nm":
+                self.full_interior.append(SparseDecoder(
+                    d[p + "intf_W1"], d[p + "intf_b1"], d[p + "intf_W2_indptr"],
+                    d[p + "intf_W2_indices"], d[p + "intf_W2_data"], d[p + "intf_scale"],
+                    d[p + "intf_shift"], m["activation"]))
+            else:
+                self.full_interior.append(LinearDecoder(d[p + "intf_Phi"]))
+            self.cols.append((d[p + "int_cols"], d[p + "gam_cols"]))
+
+    def decode(self, x):
+        """RomInstance.decode (driver.py:148-152): [(x_int, x_gam), ...]."""
+        if self.full_interior is None:
+            raise ValueError("artifacts carry no full interior maps")
+        return [(fm.decode(xi), b.gam_map.decode(xg))
+                for fm, b, (xi, xg) in zip(self.full_interior, self.blocks, self.split(x))]
+
+    def restrict_blocks(self, state):
+        """driver.py:477-480 / Partition.restrict (partition.py:232-235)."""
+        return [(state[ci], state[cg]) for ci, cg in self.cols]
 
     def split(self, x):
         return [(x[o:o + b.n_int], x[o + b.n_int:o + b.n_int + b.n_gam])
@@ -371,6 +398,20 @@ class Instance:
     def boundary(self, a, lam):
         bvec = boundary_values(self.nx, self.ny, self.nu, a, lam)
         return [b.stencil.boundary(bvec) for b in self.blocks]
+
+
+def relative_error(fom_blocks, rom_blocks):
+    """driver.py:496-507: root mean over blocks of the squared blockwise
+    relative error."""
+    if len(fom_blocks) != len(rom_blocks):
+        raise ValueError("block counts differ")
+    total = 0.0
+    for (fi, fg), (ri, rg) in zip(fom_blocks, rom_blocks):
+        denom = float(fi @ fi + fg @ fg)
+        if denom == 0.0:
+            raise ValueError("zero-norm reference block")
+        total += float((fi - ri) @ (fi - ri) + (fg - rg) @ (fg - rg)) / denom
+    return float(np.sqrt(total / len(fom_blocks)))
 
 
 # -- SQP --------------------------------------------------------------------------

@@ -8,8 +8,9 @@ ABI in ``include/ddnm.h`` (``libddnm.so``).  There is no CPU fallback.
 """
 
 from .burgers import A_RANGE, LAM_RANGE, Grid2D, ParameterPoint, seeded_parameters
-from .driver import (BatchResult, EvalBatch, RomInstance, RomSolution, build_problem,
-                     eval_gradients_batch, init_guess, solve_rom, solve_rom_batch)
+from .driver import (BatchResult, DecodeBatch, EvalBatch, RomInstance, RomSolution,
+                     build_problem, decode_batch, eval_gradients_batch, init_guess,
+                     solve_rom, solve_rom_batch)
 from .errors import ConvergenceError, FormatError, SingularityError
 from .sqp import SqpBlock, SqpConfig, SqpProblem, SqpResult, iterate
 
@@ -17,7 +18,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "A_RANGE", "LAM_RANGE", "Grid2D", "ParameterPoint", "seeded_parameters",
-    "BatchResult", "EvalBatch", "RomInstance", "RomSolution", "build_problem",
+    "BatchResult", "DecodeBatch", "EvalBatch", "RomInstance", "RomSolution",
+    "build_problem", "decode_batch",
     "eval_gradients_batch", "init_guess", "solve_rom", "solve_rom_batch",
     "ConvergenceError", "FormatError", "SingularityError",
     "SqpBlock", "SqpConfig", "SqpProblem", "SqpResult", "iterate",

@@ -117,6 +117,11 @@ def lib():
                                   C.POINTER(EvalOut)]
     L.ddnm_last_counters.argtypes = [C.c_void_p, _lp, _lp]
     L.ddnm_last_profile.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    L.ddnm_ctx_set_full_decoders.argtypes = [C.c_void_p, C.POINTER(Decoder)]
+    L.ddnm_ctx_state_len.argtypes = [C.c_void_p, _lp]
+    L.ddnm_decode_batch.argtypes = [C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp]
+    L.ddnm_decode_batch_device.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]
     if L.ddnm_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libddnm.so ABI version mismatch; rebuild")
     _lib = L
@@ -125,7 +130,9 @@ def lib():
 
 EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_destroy",
             "ddnm_ctx_info", "ddnm_solve_batch", "ddnm_solve_batch_device",
-            "ddnm_eval_batch", "ddnm_last_counters", "ddnm_last_profile")
+            "ddnm_eval_batch", "ddnm_last_counters", "ddnm_last_profile",
+            "ddnm_ctx_set_full_decoders", "ddnm_ctx_state_len", "ddnm_decode_batch",
+            "ddnm_decode_batch_device")
 
 
 def check(rc: int):

@@ -92,7 +92,17 @@ struct ddnm_ctx {
   unsigned long long* prof = nullptr;   // device-side phase profiler (env DDNM_PROF=1)
   // host-API staging buffers
   std::map<std::string, std::pair<void*, size_t>> io;
+  // full decode (ddnm_ctx_set_full_decoders)
+  int map_kind = 0;
+  DecodeJob* d_jobs = nullptr;
+  int state_len = 0, dec_max_hidden = 0, dec_mu_tile = 0;
 };
+
+namespace ddnm {
+size_t decode_smem(int mu, int max_hidden);
+int decode_mu_tile(int max_hidden, size_t smem_cap);
+cudaError_t launch_decode(const DecodeParams& p, cudaStream_t s);
+}  // namespace ddnm
 
 namespace {
 
@@ -384,6 +394,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.nb = a->n_blocks;
   P.n_C = a->n_c;
   P.map_kind = a->map_kind;
+  c->map_kind = a->map_kind;
   P.act = a->activation;
   P.nx = a->nx;
   P.ny = a->ny;
@@ -610,6 +621,7 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   if (c->work) cudaFree(c->work);
   if (c->counters) cudaFree(c->counters);
   if (c->prof) cudaFree(c->prof);
+  if (c->d_jobs) cudaFree(c->d_jobs);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -835,6 +847,107 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
   CUDA_TRY(cudaLaunchKernel(c->K.eval, dim3(ctas), dim3(c->threads), args, c->smem, s));
   for (int i = 0; i < NF; ++i)
     if (f[i].host) CUDA_TRY(cudaMemcpyAsync(f[i].host, dp[i], f[i].bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int ddnm_ctx_set_full_decoders(ddnm_ctx* c, const ddnm_decoder* interior) {
+  if (!c || !interior) return fail(DDNM_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc;
+  const int nb = c->nb;
+  for (int b = 0; b < nb; ++b)
+    if ((rc = check_decoder(interior[b], c->P.blk[b].ni, c->map_kind, "full interior"))) return rc;
+  std::vector<DecodeJob> jobs(2 * nb);
+  int off = 0, max_h = 0;
+  for (int b = 0; b < nb; ++b) {
+    const BlockDev& B = c->P.blk[b];
+    HostWindows hw;
+    DecodeJob& ji = jobs[2 * b];
+    if ((rc = upload_decoder(c, interior[b], B.ni, c->map_kind, ji.D, hw))) return rc;
+    ji.x_off = B.xoff; ji.lat = B.ni; ji.out_off = off;
+    off += ji.D.n_out;
+    DecodeJob& jg = jobs[2 * b + 1];
+    jg.D = B.ga;
+    jg.x_off = B.xoff + B.ni; jg.lat = B.ng; jg.out_off = off;
+    off += jg.D.n_out;
+    max_h = std::max({max_h, ji.D.n_hidden, jg.D.n_hidden});
+  }
+  const int mu = c->map_kind == DDNM_MAP_LINEAR ? 8 : decode_mu_tile(max_h, 200 * 1024);
+  if (mu == 0) return fail(DDNM_EUNSUPPORTED, "decoder hidden layer too wide for shared memory");
+  if (c->d_jobs) cudaFree(c->d_jobs);
+  c->d_jobs = nullptr;
+  CUDA_TRY(cudaMalloc(&c->d_jobs, jobs.size() * sizeof(DecodeJob)));
+  CUDA_TRY(cudaMemcpy(c->d_jobs, jobs.data(), jobs.size() * sizeof(DecodeJob), cudaMemcpyHostToDevice));
+  c->state_len = off;
+  c->dec_max_hidden = max_h;
+  c->dec_mu_tile = mu;
+  return 0;
+}
+
+int ddnm_ctx_state_len(const ddnm_ctx* c, int64_t* len) {
+  if (!c || !len) return fail(DDNM_EINVAL, "null argument");
+  *len = c->state_len;
+  return 0;
+}
+
+int ddnm_decode_batch_device(ddnm_ctx* c, int32_t B, const double* d_x, const double* d_fom,
+                             double* d_states, double* d_err, void* stream) {
+  if (!c || !d_x) return fail(DDNM_EINVAL, "null argument");
+  if (B < 0) return fail(DDNM_EINVAL, "negative batch");
+  if (!c->d_jobs) return fail(DDNM_EINVAL, "no full decoders (ddnm_ctx_set_full_decoders)");
+  if ((d_fom == nullptr) != (d_err == nullptr)) return fail(DDNM_EINVAL, "fom and err go together");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if (B == 0) return 0;
+  DecodeParams p{};
+  p.jobs = c->d_jobs;
+  p.n_jobs = 2 * c->nb;
+  p.nb = c->nb;
+  p.B = B;
+  p.n_D = c->n_D;
+  p.state_len = c->state_len;
+  p.act = c->P.act;
+  p.linear = c->map_kind == DDNM_MAP_LINEAR;
+  p.mu_tile = c->dec_mu_tile;
+  p.max_hidden = c->dec_max_hidden;
+  p.x = d_x;
+  p.fom = d_fom;
+  p.states = d_states;
+  p.err = d_err;
+  int rc;
+  if (d_fom) {
+    void* part = nullptr;
+    if ((rc = io_buf(c, "dec_part", (size_t)B * p.n_jobs * 2 * 8, &part))) return rc;
+    p.part = (double*)part;
+  }
+  CUDA_TRY(launch_decode(p, s));
+  return 0;
+}
+
+int ddnm_decode_batch(ddnm_ctx* c, int32_t B, const double* x, const double* fom, double* states,
+                      double* err) {
+  if (!c || !x) return fail(DDNM_EINVAL, "null argument");
+  if (B <= 0) return B == 0 ? 0 : fail(DDNM_EINVAL, "negative batch");
+  if (!c->d_jobs) return fail(DDNM_EINVAL, "no full decoders (ddnm_ctx_set_full_decoders)");
+  if ((fom == nullptr) != (err == nullptr)) return fail(DDNM_EINVAL, "fom and err go together");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t L = (size_t)c->state_len * B * 8;
+  void *dx, *df = nullptr, *ds = nullptr, *de = nullptr;
+  int rc;
+  if ((rc = io_buf(c, "dec_x", (size_t)B * c->n_D * 8, &dx))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dx, x, (size_t)B * c->n_D * 8, cudaMemcpyHostToDevice, s));
+  if (fom) {
+    if ((rc = io_buf(c, "dec_fom", L, &df)) || (rc = io_buf(c, "dec_err", (size_t)B * 8, &de))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(df, fom, L, cudaMemcpyHostToDevice, s));
+  }
+  if (states && (rc = io_buf(c, "dec_states", L, &ds))) return rc;
+  if ((rc = ddnm_decode_batch_device(c, B, (double*)dx, (double*)df, (double*)ds, (double*)de, s)))
+    return rc;
+  if (states) CUDA_TRY(cudaMemcpyAsync(states, ds, L, cudaMemcpyDeviceToHost, s));
+  if (err) CUDA_TRY(cudaMemcpyAsync(err, de, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
   return 0;

@@ -164,6 +164,23 @@ struct Params {
   unsigned long long* prof;      // [15] per-phase clock totals (DDNM_PROF=1), or null
 };
 
+// RomInstance.decode (driver.py:148-152): one full decoder of one block.
+struct DecodeJob {
+  DecDev D;               // full interior map (job 2b) or the interface map (2b+1)
+  int x_off, lat;         // latent slice of the stacked x
+  int out_off;            // offset in the flattened per-mu state
+};
+
+struct DecodeParams {
+  const DecodeJob* jobs;  // [n_jobs] (device)
+  int n_jobs, nb, B, n_D, state_len, act, linear, mu_tile, max_hidden;
+  const double* x;        // [B][n_D]
+  const double* fom;      // [B][state_len] restrict_blocks of a FOM state, or null
+  double* states;         // [B][state_len] or null
+  double* part;           // [B][n_jobs][2] (sum (f-r)^2, sum f^2) when fom
+  double* err;            // [B] relative_error (driver.py:496-507) when fom
+};
+
 struct SlotState {
   int mu, phase, n_iter, n_trials, n_evals, n_reg, status, need_kkt;
   int lam_given, pad;

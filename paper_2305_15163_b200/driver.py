@@ -80,28 +80,13 @@ class RomInstance:
             return N.ptr(x, C.c_double if kind == "f" else C.c_int64)
 
         blocks = (N.Block * self.n_blocks)()
-        ae = self.kind == "nm"
         for b in range(self.n_blocks):
             p = f"b{b}_"
             blk = blocks[b]
             blk.n_int, blk.n_gam = self.latent_layout[b]
             io, gio = a[p + "io"], a[p + "gio"]
-            for dec, pre in ((blk.interior, "int_"), (blk.interface, "gam_")):
-                if ae:
-                    dec.n_out = a[p + pre + "scale"].size
-                    dec.n_hidden = a[p + pre + "b1"].size
-                    dec.W1 = arr(a[p + pre + "W1"])
-                    dec.b1 = arr(a[p + pre + "b1"])
-                    dec.indptr = arr(a[p + pre + "W2_indptr"], "i")
-                    dec.indices = arr(a[p + pre + "W2_indices"], "i")
-                    dec.data = arr(a[p + pre + "W2_data"])
-                    dec.scale = arr(a[p + pre + "scale"])
-                    dec.shift = arr(a[p + pre + "shift"])
-                else:
-                    Phi = a[p + pre + "Phi"]
-                    dec.n_out = Phi.shape[0]
-                    dec.n_hidden = 0
-                    dec.W1 = arr(Phi)
+            self._fill_decoder(blk.interior, p + "int_", arr)
+            self._fill_decoder(blk.interface, p + "gam_", arr)
             blk.n_rows = a[p + "res_rows"].size
             blk.res_rows = arr(a[p + "res_rows"], "i")
             blk.n_cols = a[p + "cols"].size
@@ -112,7 +97,7 @@ class RomInstance:
             blk.CA = arr(a[p + "CA"])
         art = N.Artifacts()
         art.abi_version = N.ABI_VERSION
-        art.map_kind = N.MAP_AUTOENCODER if ae else N.MAP_LINEAR
+        art.map_kind = N.MAP_AUTOENCODER if self.kind == "nm" else N.MAP_LINEAR
         act = m.get("activation", "swish")
         art.activation = N.ACT_SIGMOID if act == "sigmoid" else N.ACT_SWISH
         art.nx, art.ny, art.nu = m["nx"], m["ny"], m["nu"]
@@ -136,6 +121,75 @@ class RomInstance:
         keep.append(blocks)
         return art, keep
 
+    def _fill_decoder(self, dec, pre, arr):
+        a = self.arrays
+        if self.kind == "nm":
+            dec.n_out = a[pre + "scale"].size
+            dec.n_hidden = a[pre + "b1"].size
+            dec.W1 = arr(a[pre + "W1"])
+            dec.b1 = arr(a[pre + "b1"])
+            dec.indptr = arr(a[pre + "W2_indptr"], "i")
+            dec.indices = arr(a[pre + "W2_indices"], "i")
+            dec.data = arr(a[pre + "W2_data"])
+            dec.scale = arr(a[pre + "scale"])
+            dec.shift = arr(a[pre + "shift"])
+        else:
+            Phi = a[pre + "Phi"]
+            dec.n_out = Phi.shape[0]
+            dec.n_hidden = 0
+            dec.W1 = arr(Phi)
+
+    @property
+    def has_full_decoders(self) -> bool:
+        """Whether the artifacts carry the full interior maps (decode)."""
+        return "b0_int_cols" in self.arrays
+
+    @property
+    def state_layout(self):
+        """[(n_interior_dofs, n_interface_dofs), ...] of RomInstance.decode."""
+        a = self.arrays
+        return [(int(a[f"b{b}_int_cols"].size), int(a[f"b{b}_gam_cols"].size))
+                for b in range(self.n_blocks)]
+
+    def _set_full_decoders(self, h):
+        keep = []
+
+        def arr(x, kind="f"):
+            x = N.f64(x) if kind == "f" else N.i64(x)
+            keep.append(x)
+            return N.ptr(x, C.c_double if kind == "f" else C.c_int64)
+
+        decs = (N.Decoder * self.n_blocks)()
+        for b in range(self.n_blocks):
+            self._fill_decoder(decs[b], f"b{b}_intf_", arr)
+        N.check(N.lib().ddnm_ctx_set_full_decoders(h, decs))
+
+    def decode(self, x, device: int = -1):
+        """RomInstance.decode (driver.py:148-152) on the device:
+        [(x_int, x_gam), ...] of one latent vector."""
+        return decode_batch(self, np.asarray(x, float)[None, :], device=device).blocks(0)
+
+    def restrict_blocks(self, state):
+        """driver.py:477-480 (Partition.restrict, partition.py:232-235):
+        a global FOM state split into [(x_int, x_gam), ...] per block."""
+        state = np.asarray(state, float)
+        if state.shape != (self.meta["ndof"],):
+            raise ValueError("state has wrong length")
+        return [(state[self.arrays[f"b{b}_int_cols"]], state[self.arrays[f"b{b}_gam_cols"]])
+                for b in range(self.n_blocks)]
+
+    def assemble_global(self, states):
+        """driver.py:483-493: merge per-block states; shared interface entries
+        are averaged over the blocks holding them."""
+        n = self.meta["ndof"]
+        acc, cnt = np.zeros(n), np.zeros(n)
+        for b, (xi, xg) in enumerate(states):
+            for cols, v in ((self.arrays[f"b{b}_int_cols"], xi),
+                            (self.arrays[f"b{b}_gam_cols"], xg)):
+                acc[cols] += v
+                cnt[cols] += 1
+        return acc / np.maximum(cnt, 1)
+
     def context(self, device: int = -1, slots: int = 0):
         """The libddnm context of this instance on ``device`` (created once)."""
         key = (device, slots)
@@ -145,7 +199,14 @@ class RomInstance:
                 art, keep = self._artifacts_struct()
                 h = C.c_void_p()
                 N.check(L.ddnm_ctx_create(device, C.byref(art), slots, C.byref(h)))
-                self._ctx[key] = _Context(h, self)
+                ctx = _Context(h, self)
+                if self.has_full_decoders:
+                    try:
+                        self._set_full_decoders(h)
+                    except Exception:
+                        ctx.close()
+                        raise
+                self._ctx[key] = ctx
             return self._ctx[key]
 
     def close(self):
@@ -301,9 +362,60 @@ def solve_rom_batch(instance: RomInstance, mus, cfg: SqpConfig = SqpConfig(), *,
 
 
 @dataclass(eq=False)
+class DecodeBatch:
+    """Decoded states of a batch (row k = mu k), flattened per mu as
+    [blk0 interior | blk0 interface | blk1 interior | ...]."""
+
+    states: np.ndarray
+    layout: list
+    error: np.ndarray = None
+
+    def blocks(self, k: int):
+        """RomInstance.decode's list of (x_int, x_gam) for mu k."""
+        out, off = [], 0
+        for ni, ng in self.layout:
+            out.append((self.states[k, off:off + ni], self.states[k, off + ni:off + ni + ng]))
+            off += ni + ng
+        return out
+
+
+def decode_batch(instance: RomInstance, x, *, fom_states=None, device: int = -1,
+                 keep_states: bool = True) -> DecodeBatch:
+    """RomInstance.decode (driver.py:148-152) of every latent row of ``x`` on
+    the device; with ``fom_states`` ((B, ndof) global FOM states) also
+    relative_error (driver.py:496-507) of each row against
+    restrict_blocks(fom_states[k]) (driver.py:477-480)."""
+    if not instance.has_full_decoders:
+        raise ValueError("the artifacts carry no full interior maps (regenerate them with "
+                         "tools/make_golden.py)")
+    x = N.f64(x)
+    if x.ndim != 2 or x.shape[1] != instance.n_primal:
+        raise ValueError("latents must have shape (B, n_primal)")
+    B = x.shape[0]
+    layout = instance.state_layout
+    L = sum(a + b for a, b in layout)
+    ctx = instance.context(device)
+    states = np.empty((B, L)) if keep_states else None
+    fom = err = None
+    if fom_states is not None:
+        fs = np.asarray(fom_states, float)
+        if fs.shape != (B, instance.meta["ndof"]):
+            raise ValueError("fom_states must have shape (B, ndof)")
+        cols = np.concatenate([np.concatenate([instance.arrays[f"b{b}_int_cols"],
+                                               instance.arrays[f"b{b}_gam_cols"]])
+                               for b in range(instance.n_blocks)])
+        fom = N.f64(fs[:, cols])
+        err = np.empty(B)
+    N.check(N.lib().ddnm_decode_batch(ctx.h, B, N.ptr(x), N.ptr(fom), N.ptr(states),
+                                      N.ptr(err)))
+    if err is not None and np.isnan(err).any():
+        raise ValueError("zero-norm reference block")
+    return DecodeBatch(states=states, layout=layout, error=err)
+
+
+@dataclass(eq=False)
 class RomSolution:
-    """driver.py:513-519.  ``states`` (the full decode) is not produced by
-    the online kernel; see DESIGN.md (out of scope this round)."""
+    """driver.py:513-519."""
 
     x_latent: np.ndarray
     lam: np.ndarray
@@ -313,24 +425,35 @@ class RomSolution:
 
 
 def solve_rom(instance: RomInstance, p: ParameterPoint, cfg: SqpConfig = SqpConfig(), *,
-              x0=None, lam0=None, compute_error: bool = False, label: str = ""):
+              x0=None, lam0=None, fom_state=None, compute_error: bool = False,
+              label: str = ""):
     """Solve the ROM at ``p`` (driver.py:554-597) on the GPU.
 
-    Returns ``(RomSolution, record_dict)``.  ``compute_error`` needs the FOM
-    (out of scope for the online kernel) and is rejected."""
-    if compute_error:
+    Returns ``(RomSolution, record_dict)``.  ``states`` is the device decode
+    of the solution (driver.py:589) when the artifacts carry the full maps.
+    ``fom_state`` (a global FOM state) gives ``error`` = relative_error
+    (driver.py:590-592); computing the FOM itself (``compute_error`` without
+    ``fom_state``) is outside the online GPU path and is rejected."""
+    if compute_error and fom_state is None:
         raise NotImplementedError("compute_error needs the full-order solve, which is "
-                                  "not part of the online GPU path")
+                                  "not part of the online GPU path; pass fom_state")
     mu = np.array([[p.a, p.lam]], dtype=float)
     res = solve_rom_batch(instance, mu, cfg,
                           x0=None if x0 is None else np.asarray(x0, float)[None, :],
                           lam0=None if lam0 is None else np.asarray(lam0, float)[None, :])
     r = res.result(0, cfg)
+    states, error = None, np.nan
+    if instance.has_full_decoders:
+        dec = decode_batch(instance, r.x[None, :],
+                           fom_states=None if fom_state is None else np.asarray(fom_state)[None])
+        states = dec.blocks(0)
+        if dec.error is not None:
+            error = float(dec.error[0])
     rec = {"label": label or instance.provenance.get("rom", "rom"), "a": p.a, "lam": p.lam,
-           "rom_seconds": res.seconds, "n_iter": r.n_iter, "converged": r.converged,
-           "final_merit": r.final_merit,
+           "error": error, "rom_seconds": res.seconds, "n_iter": r.n_iter,
+           "converged": r.converged, "final_merit": r.final_merit,
            "status": "ok" if r.failure_reason is None else r.failure_reason}
-    return RomSolution(x_latent=r.x, lam=r.lam, sqp=r), rec
+    return RomSolution(x_latent=r.x, lam=r.lam, states=states, sqp=r, error=error), rec
 
 
 def init_guess(instance: RomInstance, p: ParameterPoint):

@@ -66,7 +66,22 @@ def extract(inst) -> dict:
         out[p + "n_interior"] = np.int64(sub.n_interior)
         out[p + "n_interface"] = np.int64(sub.n_interface)
         out[p + "CA"] = inst.wfpc_C @ inst.fom_constraints.blocks[i].toarray()
+        # global dof columns of the block (Partition.restrict, partition.py:232-235)
+        out[p + "int_cols"] = sub.interior_cols.astype(np.int64)
+        out[p + "gam_cols"] = sub.interface_cols.astype(np.int64)
         im, gm = inst.interior_maps[i], inst.interface_maps[i]
+        # the full interior map for RomInstance.decode (driver.py:148-152)
+        if kind == "nm":
+            W2f = im.W2g.tocsr()
+            out[p + "intf_W1"] = np.ascontiguousarray(im.W1g)
+            out[p + "intf_b1"] = im.b1g.copy()
+            out[p + "intf_W2_indptr"] = W2f.indptr.astype(np.int64)
+            out[p + "intf_W2_indices"] = W2f.indices.astype(np.int64)
+            out[p + "intf_W2_data"] = W2f.data.copy()
+            out[p + "intf_scale"] = im.norm.scale.copy()
+            out[p + "intf_shift"] = im.norm.shift.copy()
+        else:
+            out[p + "intf_Phi"] = np.ascontiguousarray(im.Phi)
         if kind == "nm":
             sn = extract_subnet(im, io)
             out[p + "int_W1"] = np.ascontiguousarray(sn.W1)
@@ -95,7 +110,7 @@ def extract(inst) -> dict:
         "kind": kind, "activation": act, "nx": grid.nx, "ny": grid.ny,
         "nu": grid.nu, "nsub_x": part.nsub_x, "nsub_y": part.nsub_y,
         "nblocks": len(part.subdomains), "n_int": n_int, "n_gam": n_gam,
-        "n_c": int(inst.n_mult), "rbf_kernel": rbf.kernel,
+        "n_c": int(inst.n_mult), "ndof": int(grid.ndof), "rbf_kernel": rbf.kernel,
         "rbf_epsilon": float(rbf.epsilon),
         "provenance": {k: (v if isinstance(v, (int, float, str)) else str(v))
                        for k, v in inst.provenance.items()},
@@ -207,6 +222,27 @@ def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
     return g
 
 
+def state_goldens(inst, g: dict, n: int) -> dict:
+    """Reference ``instance.decode`` (driver.py:148-152) of the golden
+    solutions, and ``relative_error`` (driver.py:496-507) against the
+    monolithic FOM (``solve_monolithic``, the reference's compute_error path
+    driver.py:566-569) for the first ``n`` mu."""
+    from ddrom.burgers import ParameterPoint
+    from ddrom.driver import relative_error, restrict_blocks
+    from ddrom.burgers import solve_monolithic
+
+    part = inst.partition
+    out = {"mu": g["mu"][:n], "x": g["x"][:n]}
+    for k in range(n):
+        states = inst.decode(g["x"][k])
+        out[f"s{k}"] = np.concatenate([np.concatenate([xi, xg]) for xi, xg in states])
+        p = ParameterPoint(float(g["mu"][k, 0]), float(g["mu"][k, 1]))
+        fom, _ = solve_monolithic(part.grid, p)
+        out[f"fom{k}"] = np.asarray(fom, dtype=float)
+        out[f"err{k}"] = np.float64(relative_error(restrict_blocks(part, fom), states))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cache", default=os.path.join(ROOT, "artifacts_cache"))
@@ -216,6 +252,9 @@ def main():
     ap.add_argument("--B", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--detail", type=int, default=3)
+    ap.add_argument("--states", type=int, default=3, help="mu with decoded-state goldens")
+    ap.add_argument("--artifacts-only", action="store_true",
+                    help="rewrite the artifacts and state goldens, keep *_golden.npz")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     for name in a.names:
@@ -223,8 +262,14 @@ def main():
             inst = pickle.load(f)
         art = extract(inst)
         np.savez_compressed(os.path.join(a.out, f"{name}_artifacts.npz"), **art)
-        gd = goldens(inst, a.B, a.seed, a.detail)
-        np.savez_compressed(os.path.join(a.out, f"{name}_golden.npz"), **gd)
+        gpath = os.path.join(a.out, f"{name}_golden.npz")
+        if a.artifacts_only:
+            gd = dict(np.load(gpath))
+        else:
+            gd = goldens(inst, a.B, a.seed, a.detail)
+            np.savez_compressed(gpath, **gd)
+        st = state_goldens(inst, gd, a.states)
+        np.savez_compressed(os.path.join(a.out, f"{name}_states.npz"), **st)
         print(name, "n_iter", gd["n_iter"].tolist(), "failure",
               gd["failure"].tolist(), flush=True)
 
