@@ -242,7 +242,37 @@ def run_gpu(args):
     ms_per_step = total_ms / args.steps
     value = world * B * args.steps / (total_ms / 1e3)
 
-    # parity spot check of this very run against the oracle (4 mu, not timed)
+    # full decode of the batch's solutions (RomInstance.decode, driver.py:148-152):
+    # reported beside the solve, not part of `value`
+    dec = None
+    if inst.has_full_decoders:
+        Lst = C.c_int64()
+        N.check(L.ddnm_ctx_state_len(ctx.h, C.byref(Lst)))
+        st_d = torch.empty((B, Lst.value), dtype=torch.float64, device=dev)
+
+        def dstep():
+            N.check(L.ddnm_decode_batch_device(ctx.h, B, C.c_void_p(outs["x"].data_ptr()), None,
+                                               C.c_void_p(st_d.data_ptr()), None,
+                                               C.c_void_p(stream.cuda_stream)))
+        for _ in range(3):
+            dstep()
+        dts = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dstep()
+            e1.record(stream)
+            e1.synchronize()
+            dts.append(e0.elapsed_time(e1))
+        dms = float(np.median(dts))
+        dec = {"kernel": "k_decode", "ms_per_batch": dms, "states_per_s": B / (dms / 1e3),
+               "state_len": Lst.value, "bytes_written_per_batch": B * Lst.value * 8,
+               "share_of_solve": dms / ms_per_step}
+        del st_d
+
+    # per-mu outcome of the last timed step (config summary)
     n_iter = outs["n_iter"].cpu().numpy()
     status = outs["status"].cpu().numpy()
 
@@ -311,6 +341,7 @@ def run_gpu(args):
         "e2e": e2e,
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
+        "decode": dec,
     }
     print(json.dumps(line), flush=True)
     if dist:

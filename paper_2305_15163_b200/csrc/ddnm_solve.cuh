@@ -413,6 +413,55 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
 // --------------------------------------------------------------------------
 // one eval_gradients (sqp.py:117-146) for every slot in `mask` at (xt, lt).
 // Results land in eval buffer `ebi[s]` of each slot.
+// Phase D: the Gram block H = R^T R, the projections R^T r and r^T r of one
+// block for every active slot (sqp.py:124-133 per block), as the upper 8x8
+// tiles of [R | r]^T [R | r] on FP64 tensor cores (mma.m8n8k4): one warp per
+// (slot, tile), rows in k-steps of 4, two accumulator chains (even / odd
+// steps) summed at the end.
+template <int G, int W>
+__device__ void gram_dmma(const View& V, const BlockDev& B, unsigned mask, const int* ebi) {
+  const Params& P = V.P;
+  constexpr int NTB = (W + 1 + 7) / 8, NTILE = NTB * (NTB + 1) / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nr = B.nrows;
+  for (int t = warp; t < G * NTILE; t += nw) {
+    const int s = t / NTILE;
+    if (!((mask >> s) & 1u)) continue;
+    int q = t - s * NTILE, I = 0;
+    while (q >= NTB - I) { q -= NTB - I; ++I; }
+    const int J = I + q;
+    const double* sc = V.scr(s);
+    const double* R = sc + P.scr_R;
+    const double* rv = sc + P.scr_r;
+    // column c of [R | r] (zero past W): A element (row k, col 8I + m), B (row k, col 8J + n)
+    const int ca = 8 * I + (lane >> 2), cb = 8 * J + (lane >> 2), kr = lane & 3;
+    const double* pa = ca < W ? R + ca : rv;
+    const double* pb = cb < W ? R + cb : rv;
+    const int sa = ca < W ? W : 1, sb = cb < W ? W : 1;
+    const bool za = ca > W, zb = cb > W;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    for (int k0 = 0; k0 < nr; k0 += 8) {
+      const int r0 = k0 + kr, r1 = k0 + 4 + kr;
+      const double a0 = (!za && r0 < nr) ? pa[r0 * sa] : 0.0;
+      const double b0 = (!zb && r0 < nr) ? pb[r0 * sb] : 0.0;
+      const double a1 = (!za && r1 < nr) ? pa[r1 * sa] : 0.0;
+      const double b1 = (!zb && r1 < nr) ? pb[r1 * sb] : 0.0;
+      dmma_884(c0, a0, b0);
+      dmma_884(c1, a1, b1);
+    }
+    double* e = V.eb(s, ebi[s]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3) + h;
+      if (i > j || j > W) continue;
+      const double v = c0[h] + c1[h];
+      if (j < W) eb_H(e, B)[tri_idx(W, i, j)] = v;
+      else if (i < W) eb_proj(e, B)[i] = v;
+      else *eb_rr(e, B, P.n_C) = v;
+    }
+  }
+}
+
 template <int G, int NI, int NG>
 __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gslot0,
                             bool dump) {
@@ -566,54 +615,10 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
           for (int i = tid; i < P.n_C * NG; i += T) o.cjac[mu * P.tot_cjac + B.cjac_off + i] = eb_cjac(const_cast<double*>(e), B, P.n_C)[i];
       }
     }
-    // ---- phase D: Gram block, projections, r^T r (thread per entry) ----
-    {
-      const int ntri = W * (W + 1) / 2, nt = ntri + W + 1;
-      for (int t = tid; t < G * nt; t += T) {
-        const int s = t / nt;
-        int q = t - s * nt;
-        if (!((mask >> s) & 1u)) continue;
-        const double* sc = V.scr(s);
-        const double* R = sc + P.scr_R;
-        const double* rv = sc + P.scr_r;
-        // (a, b) column pair: R_i.R_j, R_i.r or r.r
-        const double* pa;
-        const double* pb;
-        int sa, sb, i = 0, j = 0, kind = 0;
-        if (q < ntri) {
-          while (q >= W - i) { q -= W - i; ++i; }
-          j = i + q;
-          pa = R + i; pb = R + j; sa = W; sb = W;
-        } else if (q < ntri + W) {
-          kind = 1; i = q - ntri;
-          pa = R + i; pb = rv; sa = W; sb = 1;
-        } else {
-          kind = 2;
-          pa = rv; pb = rv; sa = 1; sb = 1;
-        }
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        const int nr = B.nrows;
-        int r = 0;
-        for (; r + 4 <= nr; r += 4) {
-          a0 = fma(pa[(size_t)r * sa], pb[(size_t)r * sb], a0);
-          a1 = fma(pa[(size_t)(r + 1) * sa], pb[(size_t)(r + 1) * sb], a1);
-          a2 = fma(pa[(size_t)(r + 2) * sa], pb[(size_t)(r + 2) * sb], a2);
-          a3 = fma(pa[(size_t)(r + 3) * sa], pb[(size_t)(r + 3) * sb], a3);
-        }
-        for (; r < nr; ++r) a0 = fma(pa[(size_t)r * sa], pb[(size_t)r * sb], a0);
-        const double acc = (a0 + a1) + (a2 + a3);
-        double* e = V.eb(s, ebi[s]);
-        if (kind == 0) {
-          eb_H(e, B)[tri_idx(W, i, j)] = acc;
-        } else if (kind == 1) {
-          eb_proj(e, B)[i] = acc;
-        } else {
-          *eb_rr(e, B, P.n_C) = acc;
-        }
-      }
-      __syncthreads();
-      DDNM_MARK(V, 4);
-    }
+    // ---- phase D: Gram block, projections, r^T r on FP64 tensor cores ----
+    gram_dmma<G, W>(V, B, mask, ebi);
+    __syncthreads();
+    DDNM_MARK(V, 4);
   }
 }
 
