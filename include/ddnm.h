@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DDNM_ABI_VERSION 1
+#define DDNM_ABI_VERSION 2
 
 /* return codes */
 #define DDNM_OK 0
@@ -54,6 +54,10 @@ extern "C" {
 #define DDNM_ACT_SWISH 0           /* autoencoder.py:31-45 */
 #define DDNM_ACT_SIGMOID 1
 
+/* coupling of the interface latents (RomInstance.constraint_mode) */
+#define DDNM_CON_WFPC 0            /* weak FOM-port: C A_i g^Gamma(x_Gamma), driver.py:366-373 */
+#define DDNM_CON_SRPC 1            /* strong ROM-port: Ahat_i x_Gamma, driver.py:374-378      */
+
 /* One decoder.  AUTOENCODER: g = (W2 act(W1 x + b1)) * scale + shift with W2 a
  * CSR matrix [n_out x n_hidden] in storage (= accumulation) order
  * (hyper.py:163-197).  LINEAR: g = Phi x, Phi = W1 [n_out x latent]. */
@@ -71,15 +75,17 @@ typedef struct {
 
 /* One subdomain block as build_problem instantiates it (driver.py:360-435):
  * interior decoder restricted to the HR outputs `io` (extract_subnet,
- * hyper.py:200-222, or LinearMap.restrict_outputs, pod.py:95-97), the full
- * interface decoder (WFPC keeps it whole, driver.py:398-402), the sampled
- * residual rows and the local column order of RestrictedResidual
- * (driver.py:392-396, partition.py:361-425), and CA = C @ A_i
- * (driver.py:368-369). */
+ * hyper.py:200-222, or LinearMap.restrict_outputs, pod.py:95-97), the
+ * interface decoder -- WFPC: the full map (driver.py:398-402); SRPC: its
+ * restriction to the `gio` outputs (driver.py:400-402), gio then indexes
+ * that restriction (0..n_gio-1) --, the sampled residual rows and the local
+ * column order of RestrictedResidual (driver.py:392-396,
+ * partition.py:361-425), the constraint matrix, and for gappy HR the
+ * weights pinv(basis[rows]) (hyper.py:153-160). */
 typedef struct {
   int32_t n_int, n_gam;      /* latent dims of this block */
   ddnm_decoder interior;     /* n_out == n_io */
-  ddnm_decoder interface;    /* n_out == N_Gamma (all interface dofs) */
+  ddnm_decoder interface;    /* WFPC: n_out == N_Gamma; SRPC: n_out == n_gio */
   int32_t n_rows;            /* HR sample rows */
   const int64_t* res_rows;   /* [n_rows] global residual rows, sorted */
   int32_t n_cols;            /* n_io + n_gio */
@@ -87,7 +93,10 @@ typedef struct {
   int32_t n_io;
   int32_t n_gio;
   const int64_t* gio;        /* [n_gio] positions in the interface outputs */
-  const double* CA;          /* [n_c][interface.n_out] */
+  const double* CA;          /* WFPC: C @ A_i [n_c][N_Gamma] (driver.py:368-369);
+                                SRPC: Ahat_i [n_c][n_gam] (driver.py:375) */
+  int32_t n_basis;           /* gappy HR: residual basis size; 0 = collocation */
+  const double* weights;     /* gappy HR: [n_basis][n_rows] */
 } ddnm_block;
 
 /* Thin-plate-spline RBF initializer (driver.py:59-90 + scipy RBFInterpolator
@@ -105,7 +114,9 @@ typedef struct {
 typedef struct {
   int32_t abi_version;       /* DDNM_ABI_VERSION */
   int32_t map_kind;          /* DDNM_MAP_* (same for every block) */
-  int32_t activation;        /* DDNM_ACT_* */
+  int32_t activation;        /* DDNM_ACT_* of the interior maps */
+  int32_t gam_activation;    /* DDNM_ACT_* of the interface maps (SRPC port nets: sigmoid) */
+  int32_t constraint_mode;   /* DDNM_CON_* */
   int32_t nx, ny;            /* interior FD grid (burgers.py:67-106) */
   double nu;
   int32_t n_blocks;
@@ -128,7 +139,9 @@ typedef struct {
   int32_t n_primal;          /* n_D = sum (n_int + n_gam) */
   int32_t n_mult;            /* n_C */
   int32_t n_blocks;
-  int32_t total_rows;        /* sum of HR rows over blocks */
+  int32_t total_rows;        /* sum of HR sample rows over blocks */
+  int32_t total_out_rows;    /* sum of HR output rows (gappy: n_basis, else n_rows) */
+  int32_t total_out_R;       /* sum of out rows * (n_int + n_gam) */
   int32_t total_int_out;     /* sum n_io */
   int32_t total_gam_out;     /* sum N_Gamma */
   int32_t total_R;           /* sum n_rows * (n_int + n_gam) */
@@ -167,13 +180,13 @@ typedef struct {
   double* con;               /* [B][n_C] */
   double* merit;             /* [B] */
   double* objective;         /* [B] */
-  double* Br;                /* [B][total_rows] */
-  double* R;                 /* [B][total_R]  per block [n_rows][n_int+n_gam] = [R_int | R_gam] */
+  double* Br;                /* [B][total_out_rows] (the weighted rows for gappy HR) */
+  double* R;                 /* [B][total_out_R] per block [out rows][n_int+n_gam] = [R_int | R_gam] */
   double* cval;              /* [B][n_blocks][n_C] */
   double* cjac;              /* [B][total_cjac] per block [n_C][n_gam] */
   double* int_g;             /* [B][total_int_out] interior subnet outputs */
   double* int_J;             /* [B][total_int_J] */
-  double* gam_g;             /* [B][total_gam_out] full interface decoder */
+  double* gam_g;             /* [B][total_gam_out] interface decoder (WFPC: full) */
   double* gam_J;             /* [B][total_gam_J] */
   double* bvals;             /* [B][total_rows][3] sampled (bx, by, c) of assemble() */
   double* step;              /* [B][n_D + n_C] KKT step (s, s_lam) at (x, lam) */
@@ -224,11 +237,13 @@ int ddnm_last_profile(const ddnm_ctx* ctx, uint64_t* cycles16);
 
 /* ---- full decode (RomInstance.decode, driver.py:148-152) ---------------- */
 
-/* Register the full interior maps: interior[b] is block b's whole interior
- * decoder (n_out = all interior dofs; the ddnm_block carries only its HR
+/* Register the full maps: interior[b] is block b's whole interior decoder
+ * (n_out = all interior dofs; the ddnm_block carries only its HR
  * restriction), same latent dim, map kind and activation as the artifacts.
- * The interface map of block b is the block's `interface` decoder. */
-int ddnm_ctx_set_full_decoders(ddnm_ctx* ctx, const ddnm_decoder* interior);
+ * interface[b] is its whole interface decoder; NULL (WFPC only) uses the
+ * blocks' `interface` decoders, which are already whole. */
+int ddnm_ctx_set_full_decoders(ddnm_ctx* ctx, const ddnm_decoder* interior,
+                               const ddnm_decoder* interface);
 
 /* Length of one decoded state: sum over blocks of (interior n_out + N_Gamma),
  * laid out [blk0 interior | blk0 interface | blk1 interior | ...] -- the

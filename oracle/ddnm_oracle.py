@@ -292,18 +292,24 @@ class Block:
     gam_map: object
     gio: np.ndarray
     n_io: int
-    CA: np.ndarray
+    CA: np.ndarray            # WFPC: C @ A_i [n_c x N_Gamma]; SRPC: Ahat_i [n_c x n_gam]
     stencil: Stencil
+    srpc: bool = False        # interface map = subnet on the gio outputs (driver.py:400-402)
+    weights: np.ndarray = None  # gappy HR: pinv of the sampled residual basis
 
     def residual(self, xi, xg, bb):
-        """Collocation HR closure (driver.py:404-432)."""
+        """HR closure (driver.py:404-432): collocation, or gappy weighting
+        ``weights @`` of the sampled residual and Jacobian (hyper.py:107-118)."""
         if self.n_io:
             v_int = self.int_map.decode(xi)
             J_int_rows = np.asarray(self.int_map.jacobian(xi))
         else:
             v_int = np.zeros(0)
             J_int_rows = None
-        if self.gio.size:
+        if self.gio.size and self.srpc:
+            v_gam = self.gam_map.decode(xg)
+            J_gam_rows = np.asarray(self.gam_map.jacobian(xg))
+        elif self.gio.size:
             g = self.gam_map.decode(xg)
             J = np.asarray(self.gam_map.jacobian(xg))
             v_gam, J_gam_rows = g[self.gio], J[self.gio]
@@ -317,10 +323,14 @@ class Block:
         else:
             R_int = np.zeros((Jd.shape[0], self.n_int))
         R_gam = Jd[:, self.n_io:] @ J_gam_rows
+        if self.weights is not None:
+            return self.weights @ r, self.weights @ R_int, self.weights @ R_gam
         return r, R_int, R_gam
 
     def constraint(self, xg):
-        """WFPC constraint closure (driver.py:371-373)."""
+        """WFPC (driver.py:371-373) or SRPC (driver.py:374-378) constraint."""
+        if self.srpc:
+            return self.CA @ xg, self.CA.copy()
         g = self.gam_map.decode(xg)
         J = np.asarray(self.gam_map.jacobian(xg))
         return self.CA @ g, self.CA @ J
@@ -351,14 +361,17 @@ class Instance:
                 gm = SparseDecoder(d[p + "gam_W1"], d[p + "gam_b1"],
                                    d[p + "gam_W2_indptr"], d[p + "gam_W2_indices"],
                                    d[p + "gam_W2_data"], d[p + "gam_scale"],
-                                   d[p + "gam_shift"], m["activation"])
+                                   d[p + "gam_shift"],
+                                   m.get("gam_activation", m["activation"]))
             else:
                 im = LinearDecoder(d[p + "int_Phi"])
                 gm = LinearDecoder(d[p + "gam_Phi"])
             st = Stencil(self.nx, self.ny, self.nu, d[p + "res_rows"],
                          d[p + "cols"])
+            srpc = m.get("constraint", "wfpc") == "srpc"
             self.blocks.append(Block(ni, ng, im, gm, gio, int(io.size),
-                                     d[p + "CA"], st))
+                                     d[p + "Ahat"] if srpc else d[p + "CA"], st, srpc,
+                                     d.get(p + "weights")))
         self.offsets = np.cumsum([0] + [b.n_int + b.n_gam
                                         for b in self.blocks])[:-1]
         self.n_primal = int(sum(b.n_int + b.n_gam for b in self.blocks))
@@ -371,21 +384,27 @@ class Instance:
             if p + "int_cols" not in d:
                 self.full_interior = None
                 break
-            if self.kind == "nm":
-                self.full_interior.append(SparseDecoder(
-                    d[p + "intf_W1"], d[p + "intf_b1"], d[p + "intf_W2_indptr"],
-                    d[p + "intf_W2_indices"], d[p + "intf_W2_data"], d[p + "intf_scale"],
-                    d[p + "intf_shift"], m["activation"]))
-            else:
-                self.full_interior.append(LinearDecoder(d[p + "intf_Phi"]))
+            full = []
+            for pre, act in (("intf_", m["activation"]),
+                             ("gamf_", m.get("gam_activation", m["activation"]))):
+                if pre == "gamf_" and p + pre + "scale" not in d and p + pre + "Phi" not in d:
+                    full.append(self.blocks[b].gam_map)     # WFPC: gam_ is the full map
+                elif self.kind == "nm":
+                    full.append(SparseDecoder(
+                        d[p + pre + "W1"], d[p + pre + "b1"], d[p + pre + "W2_indptr"],
+                        d[p + pre + "W2_indices"], d[p + pre + "W2_data"],
+                        d[p + pre + "scale"], d[p + pre + "shift"], act))
+                else:
+                    full.append(LinearDecoder(d[p + pre + "Phi"]))
+            self.full_interior.append(tuple(full))
             self.cols.append((d[p + "int_cols"], d[p + "gam_cols"]))
 
     def decode(self, x):
         """RomInstance.decode (driver.py:148-152): [(x_int, x_gam), ...]."""
         if self.full_interior is None:
             raise ValueError("artifacts carry no full interior maps")
-        return [(fm.decode(xi), b.gam_map.decode(xg))
-                for fm, b, (xi, xg) in zip(self.full_interior, self.blocks, self.split(x))]
+        return [(fi.decode(xi), fg.decode(xg))
+                for (fi, fg), (xi, xg) in zip(self.full_interior, self.split(x))]
 
     def restrict_blocks(self, state):
         """driver.py:477-480 / Partition.restrict (partition.py:232-235)."""
@@ -478,14 +497,35 @@ def kkt_matrix(inst: Instance, ev: Eval):
     return K
 
 
-def solve_kkt(inst: Instance, ev: Eval, reg_scale=1e-12):
-    """sqp.py:162-208; returns (s, s_lam, regularized)."""
+def solve_kkt(inst: Instance, ev: Eval, reg_scale=1e-12, equilibrate=False, noise=None):
+    """sqp.py:162-208; returns (s, s_lam, regularized).
+
+    Test instruments (not the reference's algorithm), used by the tests to
+    measure how much a problem's trajectory depends on round-off in the
+    linear solve: ``equilibrate`` factors the row-equilibrated system D K
+    (another valid FP64 solve of the same equations); ``noise`` (a numpy
+    Generator) perturbs the Hessian diagonal by one unit round-off of each
+    row's largest entry, the backward error any stable LU is allowed."""
     n = inst.n_primal
     K = kkt_matrix(inst, ev)
+    if noise is not None:
+        rmax = np.max(np.abs(K[:n, :n]), axis=1)
+        K[np.arange(n), np.arange(n)] += 1.1e-16 * rmax * noise.standard_normal(n)
     rhs = -ev.optimality
     rhs_norm = max(np.linalg.norm(rhs), 1e-300)
 
     def attempt(mat):
+        if equilibrate:
+            dr = 1.0 / np.maximum(np.max(np.abs(mat), axis=1), 1e-300)
+            lu, piv = scipy.linalg.lu_factor(mat * dr[:, None])
+            pivot = float(np.abs(np.diag(lu)).min())
+            sol = scipy.linalg.lu_solve((lu, piv), rhs * dr)
+            if not np.all(np.isfinite(sol)):
+                return sol, np.inf, pivot
+            sol += scipy.linalg.lu_solve((lu, piv), (rhs - mat @ sol) * dr)
+            if not np.all(np.isfinite(sol)):
+                return sol, np.inf, pivot
+            return sol, np.linalg.norm(rhs - mat @ sol) / rhs_norm, pivot
         lu, piv = scipy.linalg.lu_factor(mat)
         pivot = float(np.abs(np.diag(lu)).min())
         sol = scipy.linalg.lu_solve((lu, piv), rhs)
@@ -536,7 +576,8 @@ class Result:
     margins: list = field(default_factory=list)
 
 
-def iterate(inst: Instance, bbs, x0, lam0, cfg=SqpConfig()) -> Result:
+def iterate(inst: Instance, bbs, x0, lam0, cfg=SqpConfig(), equilibrate=False,
+            noise=None) -> Result:
     """sqp.py:230-299 (plus an eval counter and decision margins)."""
     x = np.array(x0, dtype=float)
     lam = np.array(lam0, dtype=float)
@@ -552,7 +593,7 @@ def iterate(inst: Instance, bbs, x0, lam0, cfg=SqpConfig()) -> Result:
         margins.append(abs(merits[-1] - cfg.tol))
         if not (merits[-1] >= cfg.tol and n_iter < cfg.max_iter):
             break
-        s, s_lam, reg = solve_kkt(inst, ev, cfg.reg_scale)
+        s, s_lam, reg = solve_kkt(inst, ev, cfg.reg_scale, equilibrate, noise)
         regs += int(reg)
         alpha = 1.0
         accepted = None
@@ -620,7 +661,8 @@ def multiplier_least_squares(inst: Instance, bbs, x0):
     return lam
 
 
-def solve(inst: Instance, a, lam_mu, cfg=SqpConfig(), x0=None, lam0=None):
+def solve(inst: Instance, a, lam_mu, cfg=SqpConfig(), x0=None, lam0=None,
+          equilibrate=False, noise=None):
     """driver.py:554-597 without the FOM error (compute_error=False)."""
     bbs = inst.boundary(a, lam_mu)
     if x0 is None:
@@ -629,4 +671,4 @@ def solve(inst: Instance, a, lam_mu, cfg=SqpConfig(), x0=None, lam0=None):
         lam0 = lam_ls if lam0 is None else lam0
     elif lam0 is None:
         lam0 = multiplier_least_squares(inst, bbs, np.asarray(x0, float))
-    return iterate(inst, bbs, x0, lam0, cfg)
+    return iterate(inst, bbs, x0, lam0, cfg, equilibrate, noise)

@@ -16,9 +16,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libddnm.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAP_AUTOENCODER, MAP_LINEAR = 0, 1
 ACT_SWISH, ACT_SIGMOID = 0, 1
+CON_WFPC, CON_SRPC = 0, 1
 STATUS_OK, STATUS_LINE_SEARCH, STATUS_KKT_SINGULAR, STATUS_LSTSQ_RANK = 0, 1, 2, 3
 
 _dp = C.POINTER(C.c_double)
@@ -44,7 +45,8 @@ class Block(C.Structure):
     _fields_ = [("n_int", C.c_int32), ("n_gam", C.c_int32), ("interior", Decoder),
                 ("interface", Decoder), ("n_rows", C.c_int32), ("res_rows", _lp),
                 ("n_cols", C.c_int32), ("cols", _lp), ("n_io", C.c_int32),
-                ("n_gio", C.c_int32), ("gio", _lp), ("CA", _dp)]
+                ("n_gio", C.c_int32), ("gio", _lp), ("CA", _dp), ("n_basis", C.c_int32),
+                ("weights", _dp)]
 
 
 class Rbf(C.Structure):
@@ -55,7 +57,8 @@ class Rbf(C.Structure):
 
 class Artifacts(C.Structure):
     _fields_ = [("abi_version", C.c_int32), ("map_kind", C.c_int32),
-                ("activation", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32),
+                ("activation", C.c_int32), ("gam_activation", C.c_int32),
+                ("constraint_mode", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32),
                 ("nu", C.c_double), ("n_blocks", C.c_int32), ("n_c", C.c_int32),
                 ("blocks", C.POINTER(Block)), ("rbf", Rbf)]
 
@@ -68,7 +71,8 @@ class SqpCfg(C.Structure):
 
 class Info(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
-        "n_primal", "n_mult", "n_blocks", "total_rows", "total_int_out", "total_gam_out",
+        "n_primal", "n_mult", "n_blocks", "total_rows", "total_out_rows", "total_out_R",
+        "total_int_out", "total_gam_out",
         "total_R", "total_cjac", "total_int_J", "total_gam_J", "slots_per_cta", "ctas",
         "smem_bytes", "device")]
 
@@ -117,7 +121,8 @@ def lib():
                                   C.POINTER(EvalOut)]
     L.ddnm_last_counters.argtypes = [C.c_void_p, _lp, _lp]
     L.ddnm_last_profile.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
-    L.ddnm_ctx_set_full_decoders.argtypes = [C.c_void_p, C.POINTER(Decoder)]
+    L.ddnm_ctx_set_full_decoders.argtypes = [C.c_void_p, C.POINTER(Decoder),
+                                             C.POINTER(Decoder)]
     L.ddnm_ctx_state_len.argtypes = [C.c_void_p, _lp]
     L.ddnm_decode_batch.argtypes = [C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp]
     L.ddnm_decode_batch_device.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,

@@ -32,6 +32,10 @@ DDNM_DECL(4, 3)
 DDNM_DECL(8, 4)
 DDNM_DECL(20, 8)
 DDNM_DECL(8, 5)
+DDNM_DECL(6, 11)
+DDNM_DECL(4, 9)
+DDNM_DECL(8, 11)
+DDNM_DECL(20, 19)
 }  // namespace ddnm
 
 namespace {
@@ -53,7 +57,9 @@ int fail(int code, const std::string& msg) {
 using Kernels = KernelEntry;
 
 // (n_int, n_gam) pairs with compiled kernels: config 0/2 NM (6,4), config 1
-// LS (20,8), configs 3/4 (8,5), and the small test instances (4,3), (8,4).
+// LS (20,8), configs 3/4 (8,5), the small test instances (4,3), (8,4), and
+// the SRPC variants (interface latents = sum of port latents): NM (6,11),
+// (4,9), LS (20,19), (8,11).
 const std::vector<Kernels>& kernel_table() {
   static const std::vector<Kernels> t = [] {
     std::vector<Kernels> v;
@@ -62,6 +68,10 @@ const std::vector<Kernels>& kernel_table() {
     ddnm::register_8_4(v);
     ddnm::register_20_8(v);
     ddnm::register_8_5(v);
+    ddnm::register_6_11(v);
+    ddnm::register_4_9(v);
+    ddnm::register_8_11(v);
+    ddnm::register_20_19(v);
     return v;
   }();
   return t;
@@ -225,6 +235,7 @@ int check_decoder(const ddnm_decoder& d, int lat, int kind, const char* what) {
     snprintf(buf, sizeof buf, "%s decoder: missing weights", what);
     return fail(DDNM_EINVAL, buf);
   }
+  if (kind == DDNM_MAP_AUTOENCODER && d.n_out == 0) return 0;   // empty restriction (no gio)
   if (kind == DDNM_MAP_AUTOENCODER) {
     if (d.n_hidden <= 0 || !d.b1 || !d.indptr || !d.indices || !d.data || !d.scale || !d.shift) {
       snprintf(buf, sizeof buf, "%s decoder: incomplete autoencoder arrays", what);
@@ -247,11 +258,17 @@ struct HostWindows {        // contiguous-window decoders: per-output k0 and wid
   int maxw = 0;
 };
 
-int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, DecDev& d,
+int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, int act, DecDev& d,
                    HostWindows& hw) {
+  std::memset(&d, 0, sizeof d);
   d.n_out = h.n_out;
   d.n_hidden = kind == DDNM_MAP_AUTOENCODER ? h.n_hidden : 0;
+  d.act = act;
   int rc;
+  if (kind == DDNM_MAP_AUTOENCODER && h.n_out == 0) {
+    d.n_hidden = 0;      // empty SRPC interface restriction: nothing to evaluate
+    return 0;
+  }
   if (kind == DDNM_MAP_AUTOENCODER) {
     const size_t nnz = (size_t)h.indptr[h.n_out];
     d.ldw = h.n_hidden + 32;
@@ -355,6 +372,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   if (a->nx < 2 || a->ny < 2 || !(a->nu > 0)) return fail(DDNM_EINVAL, "bad grid");
   if (a->map_kind != DDNM_MAP_AUTOENCODER && a->map_kind != DDNM_MAP_LINEAR)
     return fail(DDNM_EINVAL, "unknown map kind");
+  if (a->constraint_mode != DDNM_CON_WFPC && a->constraint_mode != DDNM_CON_SRPC)
+    return fail(DDNM_EINVAL, "unknown constraint mode");
   const int ni = a->blocks[0].n_int, ng = a->blocks[0].n_gam;
   for (int b = 0; b < a->n_blocks; ++b) {
     const ddnm_block& k = a->blocks[b];
@@ -369,6 +388,10 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     if ((rc = check_decoder(k.interface, ng, a->map_kind, "interface"))) return rc;
     for (int g = 0; g < k.n_gio; ++g)
       if (k.gio[g] < 0 || k.gio[g] >= k.interface.n_out) return fail(DDNM_EINVAL, "gio out of range");
+    if (a->constraint_mode == DDNM_CON_SRPC && k.interface.n_out != k.n_gio)
+      return fail(DDNM_EINVAL, "SRPC interface decoder must be restricted to the gio outputs");
+    if (k.n_basis < 0 || k.n_basis > k.n_rows || (k.n_basis > 0 && !k.weights))
+      return fail(DDNM_EINVAL, "gappy weights need 1..n_rows basis vectors");
   }
   auto* c = new ddnm_ctx();
   int rc = 0;
@@ -395,6 +418,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.n_C = a->n_c;
   P.map_kind = a->map_kind;
   c->map_kind = a->map_kind;
+  P.con_mode = a->constraint_mode;
   P.act = a->activation;
   P.nx = a->nx;
   P.ny = a->ny;
@@ -403,7 +427,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.hy = 0.05 / (a->ny + 1);
   const int W = ni + ng;
   int xoff = 0, row_off = 0, iout = 0, gout = 0, Roff = 0, cjoff = 0, ijoff = 0, gjoff = 0, eboff = 0;
-  int max_nh = 0, max_io = 0, max_gam = 0, max_rows = 0;
+  int max_nh = 0, max_io = 0, max_gam = 0, max_rows = 0, max_nbz = 0, out_off = 0, outR_off = 0;
   std::vector<HostWindows> hwin(2 * a->n_blocks);
   for (int b = 0; b < P.nb; ++b) {
     const ddnm_block& k = a->blocks[b];
@@ -412,8 +436,11 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     B.nrows = k.n_rows; B.n_io = k.n_io; B.n_gio = k.n_gio;
     B.xoff = xoff; B.row_off = row_off; B.iout_off = iout; B.gout_off = gout; B.R_off = Roff;
     B.cjac_off = cjoff; B.intJ_off = ijoff; B.gamJ_off = gjoff; B.eb_off = eboff;
-    if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, B.in, hwin[2 * b]))) return bail(rc);
-    if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, B.ga, hwin[2 * b + 1]))) return bail(rc);
+    if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, a->activation, B.in, hwin[2 * b])))
+      return bail(rc);
+    if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, a->gam_activation, B.ga,
+                             hwin[2 * b + 1])))
+      return bail(rc);
     HostRows hr;
     if ((rc = build_stencil(a, k, hr))) return bail(rc);
     StRows& R = B.rows;
@@ -432,7 +459,18 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
         (rc = upload(c, hr.yc.data(), hr.yc.size(), const_cast<double**>(&R.yc))))
       return bail(rc);
     if ((rc = upload_i32(c, k.gio, (size_t)k.n_gio, const_cast<int**>(&B.gio)))) return bail(rc);
-    if ((rc = upload(c, k.CA, (size_t)P.n_C * k.interface.n_out, const_cast<double**>(&B.CA)))) return bail(rc);
+    const size_t ca_cols = a->constraint_mode == DDNM_CON_SRPC ? (size_t)ng : (size_t)k.interface.n_out;
+    if ((rc = upload(c, k.CA, (size_t)P.n_C * ca_cols, const_cast<double**>(&B.CA)))) return bail(rc);
+    B.nbz = k.n_basis;
+    B.wts = nullptr;
+    if (k.n_basis > 0 &&
+        (rc = upload(c, k.weights, (size_t)k.n_basis * k.n_rows, const_cast<double**>(&B.wts))))
+      return bail(rc);
+    B.out_off = out_off;
+    B.outR_off = outR_off;
+    out_off += k.n_basis > 0 ? k.n_basis : k.n_rows;
+    outR_off += (k.n_basis > 0 ? k.n_basis : k.n_rows) * W;
+    max_nbz = std::max(max_nbz, (int)k.n_basis);
     xoff += W; row_off += k.n_rows; iout += k.n_io; gout += k.interface.n_out;
     Roff += k.n_rows * W; cjoff += P.n_C * ng; ijoff += k.n_io * ni; gjoff += k.interface.n_out * ng;
     eboff += W * (W + 1) / 2 + W + P.n_C + P.n_C * ng + 1;
@@ -446,6 +484,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.total_rows = row_off;
   P.tot_iout = iout; P.tot_gout = gout; P.tot_R = Roff; P.tot_cjac = cjoff;
   P.tot_intJ = ijoff; P.tot_gamJ = gjoff;
+  P.tot_out = out_off; P.tot_outR = outR_off;
   c->n_D = P.n_D; c->n_C = P.n_C; c->nb = P.nb;
   c->tot_rows = row_off; c->tot_iout = iout; c->tot_gout = gout; c->tot_R = Roff;
   c->tot_cjac = cjoff; c->tot_intJ = ijoff; c->tot_gamJ = gjoff;
@@ -485,6 +524,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
       P.scr_R = scr; scr += max_rows * W;
       P.scr_r = scr; scr += max_rows;
     }
+    P.scr_RB = -1;
+    if (max_nbz > 0) { P.scr_RB = scr; scr += max_nbz * (W + 1); }
     return scr;
   };
   int scr = plan_scratch(0);
@@ -633,6 +674,8 @@ int ddnm_ctx_info(const ddnm_ctx* c, ddnm_info* i) {
   i->n_mult = c->n_C;
   i->n_blocks = c->nb;
   i->total_rows = c->tot_rows;
+  i->total_out_rows = c->P.tot_out;
+  i->total_out_R = c->P.tot_outR;
   i->total_int_out = c->tot_iout;
   i->total_gam_out = c->tot_gout;
   i->total_R = c->tot_R;
@@ -804,8 +847,8 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
       {"con", o->con, B * nC * 8},
       {"merit", o->merit, B * 8ul},
       {"objective", o->objective, B * 8ul},
-      {"Br", o->Br, B * (size_t)c->tot_rows * 8},
-      {"R", o->R, B * (size_t)c->tot_R * 8},
+      {"Br", o->Br, B * (size_t)c->P.tot_out * 8},
+      {"R", o->R, B * (size_t)c->P.tot_outR * 8},
       {"cval", o->cval, B * (size_t)c->nb * nC * 8},
       {"cjac", o->cjac, B * (size_t)c->tot_cjac * 8},
       {"int_g", o->int_g, B * (size_t)c->tot_iout * 8},
@@ -852,24 +895,34 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
   return 0;
 }
 
-int ddnm_ctx_set_full_decoders(ddnm_ctx* c, const ddnm_decoder* interior) {
+int ddnm_ctx_set_full_decoders(ddnm_ctx* c, const ddnm_decoder* interior,
+                               const ddnm_decoder* interface) {
   if (!c || !interior) return fail(DDNM_EINVAL, "null argument");
+  if (c->P.con_mode == DDNM_CON_SRPC && !interface)
+    return fail(DDNM_EINVAL, "SRPC needs the full interface maps");
   CUDA_TRY(cudaSetDevice(c->device));
   int rc;
   const int nb = c->nb;
-  for (int b = 0; b < nb; ++b)
+  for (int b = 0; b < nb; ++b) {
     if ((rc = check_decoder(interior[b], c->P.blk[b].ni, c->map_kind, "full interior"))) return rc;
+    if (interface && (rc = check_decoder(interface[b], c->P.blk[b].ng, c->map_kind, "full interface")))
+      return rc;
+  }
   std::vector<DecodeJob> jobs(2 * nb);
   int off = 0, max_h = 0;
   for (int b = 0; b < nb; ++b) {
     const BlockDev& B = c->P.blk[b];
     HostWindows hw;
     DecodeJob& ji = jobs[2 * b];
-    if ((rc = upload_decoder(c, interior[b], B.ni, c->map_kind, ji.D, hw))) return rc;
+    if ((rc = upload_decoder(c, interior[b], B.ni, c->map_kind, B.in.act, ji.D, hw))) return rc;
     ji.x_off = B.xoff; ji.lat = B.ni; ji.out_off = off;
     off += ji.D.n_out;
     DecodeJob& jg = jobs[2 * b + 1];
-    jg.D = B.ga;
+    if (interface) {
+      if ((rc = upload_decoder(c, interface[b], B.ng, c->map_kind, B.ga.act, jg.D, hw))) return rc;
+    } else {
+      jg.D = B.ga;
+    }
     jg.x_off = B.xoff + B.ni; jg.lat = B.ng; jg.out_off = off;
     off += jg.D.n_out;
     max_h = std::max({max_h, ji.D.n_hidden, jg.D.n_hidden});

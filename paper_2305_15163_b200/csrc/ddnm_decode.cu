@@ -20,6 +20,7 @@ constexpr int DEC_MU = 8;
 constexpr int DEC_THREADS = 256;
 
 __device__ __forceinline__ double act_only(int act, double z, const double* tab) {
+  // per map: interior swish, SRPC port nets sigmoid
   const double s = expit_fast(z, tab);
   return act == ACT_SWISH ? __dmul_rn(z, s) : s;   // autoencoder.py:31-36
 }
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(DEC_THREADS) k_decode(DecodeParams p) {
       }
 #pragma unroll
       for (int m = 0; m < DEC_MU; ++m)
-        if (m < MU) hid[(size_t)m * H + k] = act_only(p.act, z[m], k_exp2_32);
+        if (m < MU) hid[(size_t)m * H + k] = act_only(D.act, z[m], k_exp2_32);
     }
     __syncthreads();
   }

@@ -37,6 +37,7 @@ enum Status { ST_OK = 0, ST_LINE_SEARCH = 1, ST_KKT_SINGULAR = 2, ST_LSTSQ_RANK 
 
 struct DecDev {
   int n_out, n_hidden;
+  int act;                // ACT_* of this map (SRPC port nets are Sigmoid)
   const double* W1;       // LINEAR: Phi [n_out][lat]  (AE: unused on device)
   const double* W1t;      // AE: W1 transposed [lat][ldw] (coalesced per latent column),
   int ldw;                //     ldw = n_hidden + 32, zero padded
@@ -101,7 +102,10 @@ struct BlockDev {
   const double* tile_v;   // [n_tiles][10][32] B-operand W2 values per tile
   StRows rows;
   const int* gio;
-  const double* CA;       // [n_c][ga.n_out]
+  const double* CA;       // WFPC: C A_i [n_c][ga.n_out]; SRPC: Ahat_i [n_c][ng]
+  int nbz;                // gappy HR: residual basis size (0: collocation)
+  const double* wts;      // gappy HR: weights [nbz][nrows] (hyper.py:153-160)
+  int out_off, outR_off;  // offsets of the weighted rows in the Br / R dumps
 };
 
 struct SqpCfg {
@@ -122,6 +126,7 @@ struct EvalOut {
 
 struct Params {
   int nb, n_D, n_C, nK, map_kind, act;
+  int con_mode;           // 0 WFPC (CA g^Gamma), 1 SRPC (Ahat x_Gamma)
   int nx, ny;
   double nu, hx, hy;
   int total_rows;
@@ -143,6 +148,8 @@ struct Params {
   int sm_scr;             // per slot scratch (scr_size)
   int scr_size;
   int scr_sig, scr_dsig, scr_gint, scr_jint, scr_ggam, scr_jgam, scr_R, scr_r;
+  int scr_RB;             // gappy: weighted [R | r] rows [max nbz][W + 1], or -1
+  int tot_out, tot_outR;  // sum over blocks of HR output rows (nbz or nrows), x W
   int nh_tot;             // max over blocks of (int hidden + gam hidden)
   // work
   int B;

@@ -84,7 +84,7 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
 #pragma unroll
     for (int d = 0; d < L; ++d) z = fma(w[d], x[d], z);
     double a, da;
-    act_pair(V.P.act, z, a, da, k_exp2_32);
+    act_pair(D.act, z, a, da, k_exp2_32);
     double* sc = V.scr(s);
     sc[V.P.scr_sig + sig_off + k] = a;
     sc[V.P.scr_dsig + sig_off + k] = da;
@@ -413,17 +413,68 @@ __device__ __forceinline__ void stencil_row(const View& V, const BlockDev& B, in
 // --------------------------------------------------------------------------
 // one eval_gradients (sqp.py:117-146) for every slot in `mask` at (xt, lt).
 // Results land in eval buffer `ebi[s]` of each slot.
+// Phase C2 (gappy HR only): [R' | r'] = weights [R | r] (hyper.py:107-118:
+// apply_sampled / apply_sampled_matrix), weights [nbz][nrows] in global
+// memory (mu-independent), on FP64 tensor cores: one warp per (slot, 8-row
+// tile of the weighted rows, 8-column tile of [R | r]), k-steps of 4 sampled
+// rows with four accumulator chains.  Output rows R' [nbz][W] then r' [nbz].
+template <int G, int W>
+__device__ void gappy_weight(const View& V, const BlockDev& B, unsigned mask) {
+  const Params& P = V.P;
+  constexpr int NTN = (W + 1 + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nr = B.nrows, nz = B.nbz, NTM = (nz + 7) / 8;
+  for (int t = warp; t < G * NTM * NTN; t += nw) {
+    const int s = t / (NTM * NTN);
+    if (!((mask >> s) & 1u)) continue;
+    const int q = t - s * NTM * NTN, I = q / NTN, J = q - I * NTN;
+    double* sc = V.scr(s);
+    const double* R = sc + P.scr_R;
+    const double* rv = sc + P.scr_r;
+    const int ra = 8 * I + (lane >> 2), cb = 8 * J + (lane >> 2), kr = lane & 3;
+    const double* pa = B.wts + (size_t)min(ra, nz - 1) * nr;
+    const double* pb = cb < W ? R + cb : rv;
+    const int sb = cb < W ? W : 1;
+    const bool za = ra >= nz, zb = cb > W;
+    double c[4][2] = {};
+    for (int k0 = 0; k0 < nr; k0 += 16) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = k0 + 4 * u + kr;
+        a[u] = (!za && r < nr) ? __ldg(pa + r) : 0.0;
+        b[u] = (!zb && r < nr) ? pb[r * sb] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma_884(c[u], a[u], b[u]);
+    }
+    double* Ro = sc + P.scr_RB;
+    double* ro = Ro + nz * W;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3) + h;
+      if (i >= nz || j > W) continue;
+      const double v = (c[0][h] + c[2][h]) + (c[1][h] + c[3][h]);
+      if (j < W) Ro[i * W + j] = v;
+      else ro[i] = v;
+    }
+  }
+}
+
 // Phase D: the Gram block H = R^T R, the projections R^T r and r^T r of one
 // block for every active slot (sqp.py:124-133 per block), as the upper 8x8
 // tiles of [R | r]^T [R | r] on FP64 tensor cores (mma.m8n8k4): one warp per
-// (slot, tile), rows in k-steps of 4, two accumulator chains (even / odd
-// steps) summed at the end.
+// (slot, tile), rows in k-steps of 4, four accumulator chains (step mod 4)
+// summed at the end.
 template <int G, int W>
 __device__ void gram_dmma(const View& V, const BlockDev& B, unsigned mask, const int* ebi) {
   const Params& P = V.P;
   constexpr int NTB = (W + 1 + 7) / 8, NTILE = NTB * (NTB + 1) / 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nr = B.nrows;
+  // collocation: the sampled rows; gappy: the weighted rows (phase C2)
+  const int nr = B.nbz > 0 ? B.nbz : B.nrows;
+  const int offR = B.nbz > 0 ? P.scr_RB : P.scr_R;
+  const int offr = B.nbz > 0 ? P.scr_RB + B.nbz * W : P.scr_r;
   for (int t = warp; t < G * NTILE; t += nw) {
     const int s = t / NTILE;
     if (!((mask >> s) & 1u)) continue;
@@ -431,24 +482,28 @@ __device__ void gram_dmma(const View& V, const BlockDev& B, unsigned mask, const
     while (q >= NTB - I) { q -= NTB - I; ++I; }
     const int J = I + q;
     const double* sc = V.scr(s);
-    const double* R = sc + P.scr_R;
-    const double* rv = sc + P.scr_r;
+    const double* R = sc + offR;
+    const double* rv = sc + offr;
     // column c of [R | r] (zero past W): A element (row k, col 8I + m), B (row k, col 8J + n)
     const int ca = 8 * I + (lane >> 2), cb = 8 * J + (lane >> 2), kr = lane & 3;
     const double* pa = ca < W ? R + ca : rv;
     const double* pb = cb < W ? R + cb : rv;
     const int sa = ca < W ? W : 1, sb = cb < W ? W : 1;
     const bool za = ca > W, zb = cb > W;
-    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-    for (int k0 = 0; k0 < nr; k0 += 8) {
-      const int r0 = k0 + kr, r1 = k0 + 4 + kr;
-      const double a0 = (!za && r0 < nr) ? pa[r0 * sa] : 0.0;
-      const double b0 = (!zb && r0 < nr) ? pb[r0 * sb] : 0.0;
-      const double a1 = (!za && r1 < nr) ? pa[r1 * sa] : 0.0;
-      const double b1 = (!zb && r1 < nr) ? pb[r1 * sb] : 0.0;
-      dmma_884(c0, a0, b0);
-      dmma_884(c1, a1, b1);
+    double c[4][2] = {};
+    for (int k0 = 0; k0 < nr; k0 += 16) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = k0 + 4 * u + kr;
+        a[u] = (!za && r < nr) ? pa[r * sa] : 0.0;
+        b[u] = (!zb && r < nr) ? pb[r * sb] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma_884(c[u], a[u], b[u]);
     }
+    double c0[2] = {c[0][0] + c[2][0], c[0][1] + c[2][1]};
+    double c1[2] = {c[1][0] + c[3][0], c[1][1] + c[3][1]};
     double* e = V.eb(s, ebi[s]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -540,7 +595,25 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       const int ngo = B.ga.n_out;
       // 8-lane group per (slot, constraint row): cval = CA g, cjac = CA J
       // (driver.py:371-373); the remaining threads start on stencil rows
-      const int nct = 8 * G * P.n_C, nct32 = (nct + 31) & ~31;
+      const int nct = P.con_mode == 1 ? 0 : 8 * G * P.n_C, nct32 = (nct + 31) & ~31;
+      if (P.con_mode == 1) {
+        // SRPC (driver.py:374-378): value Ahat x_Gamma, constant Jacobian Ahat
+        for (int t = tid; t < G * P.n_C; t += T) {
+          const int s = t / P.n_C, c = t - s * P.n_C;
+          if (!((mask >> s) & 1u)) continue;
+          const double* xg = V.vec(s, 4) + B.xoff + NI;
+          const double* ah = B.CA + (size_t)c * NG;
+          double* e = V.eb(s, ebi[s]);
+          double v = 0.0;
+#pragma unroll
+          for (int d = 0; d < NG; ++d) {
+            const double a = __ldg(ah + d);
+            v = fma(a, xg[d], v);
+            eb_cjac(e, B, P.n_C)[c * NG + d] = a;
+          }
+          eb_cval(e, B)[c] = v;
+        }
+      }
       for (int t = tid; t < nct32; t += T) {
         const int grp = min(t, nct - 1) >> 3, q = t & 7;
         const int s = grp / P.n_C, c = grp - s * P.n_C;
@@ -580,6 +653,10 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         stencil_row<NI, NG>(V, B, s, row, bv);
       }
       __syncthreads();
+      if (B.nbz > 0) {
+        gappy_weight<G, W>(V, B, mask);
+        __syncthreads();
+      }
       DDNM_MARK(V, 3);
     }
     // ---- optional dumps of every intermediate (ddnm_eval_batch) ----
@@ -600,10 +677,13 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
           for (int i = tid; i < B.ga.n_out; i += T) o.gam_g[mu * P.tot_gout + B.gout_off + i] = sc[P.scr_ggam + i];
         if (o.gam_J)
           for (int i = tid; i < B.ga.n_out * NG; i += T) o.gam_J[mu * P.tot_gamJ + B.gamJ_off + i] = Jgam[i];
+        const int nz = B.nbz > 0 ? B.nbz : B.nrows;
+        const double* Rs = sc + (B.nbz > 0 ? P.scr_RB : P.scr_R);
+        const double* rs = B.nbz > 0 ? Rs + nz * W : sc + P.scr_r;
         if (o.Br)
-          for (int i = tid; i < B.nrows; i += T) o.Br[mu * P.total_rows + B.row_off + i] = sc[P.scr_r + i];
+          for (int i = tid; i < nz; i += T) o.Br[mu * P.tot_out + B.out_off + i] = rs[i];
         if (o.R)
-          for (int i = tid; i < B.nrows * W; i += T) o.R[mu * P.tot_R + B.R_off + i] = sc[P.scr_R + i];
+          for (int i = tid; i < nz * W; i += T) o.R[mu * P.tot_outR + B.outR_off + i] = Rs[i];
         if (o.bvals)
           for (int i = tid; i < B.nrows * 3; i += T)
             o.bvals[(mu * P.total_rows + B.row_off) * 3 + i] =
@@ -665,6 +745,51 @@ __device__ void finalize_eval(const View& V, int s, double* e, const double* lt)
 // warp-level dense LU with partial pivoting (LAPACK dgetf2 semantics:
 // idamax pivot = first max, scale by reciprocal when |pivot| >= sfmin).
 // K row-major with leading dimension ld.  Returns 0 or k+1 for a zero pivot.
+// Rank-1 update of the trailing block of a warp LU after pivot step k:
+// M[i][j] -= M[i][k] M[k][j] for k < i, j < m.  The (i, j) elements are dealt
+// to the lanes 4 at a time with every load issued before the stores, so one
+// step costs a couple of shared-memory round trips instead of one per row.
+__device__ __forceinline__ void warp_rank1(double* M, int ld, int k, int m) {
+  const int lane = threadIdx.x & 31;
+  const int n = m - k - 1;
+  if (n <= 0) return;
+  const int nn = n * n, qi = WARP / n, qj = WARP - qi * n;
+  int i = lane / n, j = lane - (lane / n) * n;
+  double* base = M + (size_t)(k + 1) * ld + (k + 1);
+  const double* lcol = M + (size_t)(k + 1) * ld + k;
+  const double* urow = M + (size_t)k * ld + (k + 1);
+  for (int e0 = lane; e0 < nn; e0 += 4 * WARP) {
+    double l[4], u[4], a[4];
+    int off[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      off[t] = -1;
+      if (e0 + t * WARP < nn) {
+        off[t] = i * ld + j;
+        l[t] = lcol[i * ld];
+        u[t] = urow[j];
+        a[t] = base[off[t]];
+      }
+      i += qi; j += qj;
+      if (j >= n) { j -= n; ++i; }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (off[t] >= 0) base[off[t]] = fma(-l[t], u[t], a[t]);
+  }
+}
+
+// Row permutation of a sequence of LAPACK-style swaps (swap(y[k], y[piv[k]])
+// for k = 0..cnt-1): the source index of element i after all of them.
+__device__ __forceinline__ int swap_source(const int* piv, int cnt, int i) {
+  for (int k = cnt - 1; k >= 0; --k) {
+    const int p = piv[k];
+    if (i == k) i = p;
+    else if (i == p) i = k;
+  }
+  return i;
+}
+
 static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
   const int lane = threadIdx.x & 31;
   int info = 0;
@@ -701,22 +826,7 @@ static __device__ int warp_lu(double* K, int ld, int n, int* piv) {
       info = k + 1;
     }
     __syncwarp();
-    // rank-1 update of the trailing block, lanes over (i, j) pairs
-    for (int j = k + 1 + lane; j < n; j += WARP) {
-      const double ukj = K[k * ld + j];
-      int i = k + 1;
-      for (; i + 4 <= n; i += 4) {
-        const double l0 = K[i * ld + k], l1 = K[(i + 1) * ld + k];
-        const double l2 = K[(i + 2) * ld + k], l3 = K[(i + 3) * ld + k];
-        const double a0 = K[i * ld + j], a1 = K[(i + 1) * ld + j];
-        const double a2 = K[(i + 2) * ld + j], a3 = K[(i + 3) * ld + j];
-        K[i * ld + j] = fma(-l0, ukj, a0);
-        K[(i + 1) * ld + j] = fma(-l1, ukj, a1);
-        K[(i + 2) * ld + j] = fma(-l2, ukj, a2);
-        K[(i + 3) * ld + j] = fma(-l3, ukj, a3);
-      }
-      for (; i < n; ++i) K[i * ld + j] = fma(-K[i * ld + k], ukj, K[i * ld + j]);
-    }
+    warp_rank1(K, ld, k, n);
     __syncwarp();
   }
   return info;
@@ -727,13 +837,7 @@ static __device__ void warp_lu_solve(const double* K, int ld, int n, const int* 
   const int lane = threadIdx.x & 31;
   if (n <= WARP) {
     // register version: lane i holds b_i
-    if (lane == 0)
-      for (int k = 0; k < n; ++k) {
-        const int p = piv[k];
-        if (p != k) { const double t = b[k]; b[k] = b[p]; b[p] = t; }
-      }
-    __syncwarp();
-    double bl = lane < n ? b[lane] : 0.0;
+    double bl = lane < n ? b[swap_source(piv, n, lane)] : 0.0;
     for (int k = 0; k < n; ++k) {
       const double bk = __shfl_sync(0xffffffffu, bl, k);
       if (lane > k && lane < n) bl = fma(-K[lane * ld + k], bk, bl);
@@ -1251,23 +1355,7 @@ __device__ bool kkt_block_factor(const Params& P, const double* e, int b, double
       for (int i = k + 1 + lane; i < m; i += WARP) M[i * ld + k] /= pv;
     }
     __syncwarp();
-    // lanes over columns; each lane loads its column's rows and the column-k
-    // multipliers 4 at a time before storing (no load-after-store stalls)
-    for (int j = k + 1 + lane; j < m; j += WARP) {
-      const double ukj = M[k * ld + j];
-      int i = k + 1;
-      for (; i + 4 <= m; i += 4) {
-        const double l0 = M[i * ld + k], l1 = M[(i + 1) * ld + k];
-        const double l2 = M[(i + 2) * ld + k], l3 = M[(i + 3) * ld + k];
-        const double a0 = M[i * ld + j], a1 = M[(i + 1) * ld + j];
-        const double a2 = M[(i + 2) * ld + j], a3 = M[(i + 3) * ld + j];
-        M[i * ld + j] = fma(-l0, ukj, a0);
-        M[(i + 1) * ld + j] = fma(-l1, ukj, a1);
-        M[(i + 2) * ld + j] = fma(-l2, ukj, a2);
-        M[(i + 3) * ld + j] = fma(-l3, ukj, a3);
-      }
-      for (; i < m; ++i) M[i * ld + j] = fma(-M[i * ld + k], ukj, M[i * ld + j]);
-    }
+    warp_rank1(M, ld, k, m);
     __syncwarp();
   }
   return ok;
@@ -1281,15 +1369,11 @@ __device__ void kkt_block_forward(const Params& P, int b, const double* M, const
   constexpr int W = NI + NG;
   const int lane = threadIdx.x & 31;
   const int nC = P.n_C, ld = W + nC + 1;
-  if (lane == 0)
-    for (int k = 0; k < W; ++k) {
-      const int p = piv[k];
-      if (p != k) { const double t = y[k]; y[k] = y[p]; y[p] = t; }
-    }
-  __syncwarp();
-  // lane i holds row i of [y_b; tE] (W + nC <= 32) across the steps
+  // lane i holds row i of [y_b; tE] (W + nC <= 32) across the steps; the
+  // block's row swaps are applied as a gather
   const int m = W + nC;
-  double yl = lane < W ? y[lane] : 0.0;
+  double yl = lane < W ? y[swap_source(piv, W, lane)] : 0.0;
+  __syncwarp();
   for (int k = 0; k < W; ++k) {
     const double yk = __shfl_sync(0xffffffffu, yl, k);
     if (lane > k && lane < m) yl = fma(-M[lane * ld + k], yk, yl);

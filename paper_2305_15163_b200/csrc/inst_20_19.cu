@@ -1,0 +1,12 @@
+// Kernel specialisations for latent dims (n_int, n_gam) = (20, 19): SRPC LS config-1 variant (20, 19).
+#include <vector>
+
+#include "ddnm_registry.h"
+#include "ddnm_solve.cuh"
+
+namespace ddnm {
+void register_20_19(std::vector<KernelEntry>& t) {
+  t.push_back(KernelEntry{20, 19, 1, (const void*)&k_solve<1, 20, 19>,
+                          (const void*)&k_eval<1, 20, 19>});
+}
+}  // namespace ddnm

@@ -1,0 +1,14 @@
+// Kernel specialisations for latent dims (n_int, n_gam) = (4, 9): SRPC NM tiny variant (4, 9).
+#include <vector>
+
+#include "ddnm_registry.h"
+#include "ddnm_solve.cuh"
+
+namespace ddnm {
+void register_4_9(std::vector<KernelEntry>& t) {
+  t.push_back(KernelEntry{4, 9, 1, (const void*)&k_solve<1, 4, 9>,
+                          (const void*)&k_eval<1, 4, 9>});
+  t.push_back(KernelEntry{4, 9, 2, (const void*)&k_solve<2, 4, 9>,
+                          (const void*)&k_eval<2, 4, 9>});
+}
+}  // namespace ddnm

@@ -1,0 +1,14 @@
+// Kernel specialisations for latent dims (n_int, n_gam) = (6, 11): SRPC NM config-0 variant (6, 11).
+#include <vector>
+
+#include "ddnm_registry.h"
+#include "ddnm_solve.cuh"
+
+namespace ddnm {
+void register_6_11(std::vector<KernelEntry>& t) {
+  t.push_back(KernelEntry{6, 11, 1, (const void*)&k_solve<1, 6, 11>,
+                          (const void*)&k_eval<1, 6, 11>});
+  t.push_back(KernelEntry{6, 11, 2, (const void*)&k_solve<2, 6, 11>,
+                          (const void*)&k_eval<2, 6, 11>});
+}
+}  // namespace ddnm

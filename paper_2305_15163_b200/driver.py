@@ -51,6 +51,9 @@ class RomInstance:
         self.n_mult = int(m["n_c"])
         self.n_primal = sum(a + b for a, b in self.latent_layout)
         self.provenance = dict(m.get("provenance", {}))
+        self.constraint_mode = m.get("constraint", "wfpc")
+        self.srpc = self.constraint_mode == "srpc"
+        self.hr_mode = m.get("hr", "collocation")
         self._ctx = {}
         self._lock = threading.Lock()
         self._keep = []
@@ -87,6 +90,9 @@ class RomInstance:
             io, gio = a[p + "io"], a[p + "gio"]
             self._fill_decoder(blk.interior, p + "int_", arr)
             self._fill_decoder(blk.interface, p + "gam_", arr)
+            if self.srpc:
+                # the interface decoder is the restriction to gio (driver.py:400-402)
+                gio = np.arange(gio.size, dtype=np.int64)
             blk.n_rows = a[p + "res_rows"].size
             blk.res_rows = arr(a[p + "res_rows"], "i")
             blk.n_cols = a[p + "cols"].size
@@ -94,12 +100,18 @@ class RomInstance:
             blk.n_io = io.size
             blk.n_gio = gio.size
             blk.gio = arr(gio, "i")
-            blk.CA = arr(a[p + "CA"])
+            blk.CA = arr(a[p + "Ahat"] if self.srpc else a[p + "CA"])
+            if p + "weights" in a:
+                blk.n_basis = a[p + "weights"].shape[0]
+                blk.weights = arr(a[p + "weights"])
         art = N.Artifacts()
         art.abi_version = N.ABI_VERSION
         art.map_kind = N.MAP_AUTOENCODER if self.kind == "nm" else N.MAP_LINEAR
         act = m.get("activation", "swish")
+        gact = m.get("gam_activation", act)
         art.activation = N.ACT_SIGMOID if act == "sigmoid" else N.ACT_SWISH
+        art.gam_activation = N.ACT_SIGMOID if gact == "sigmoid" else N.ACT_SWISH
+        art.constraint_mode = N.CON_SRPC if self.srpc else N.CON_WFPC
         art.nx, art.ny, art.nu = m["nx"], m["ny"], m["nu"]
         art.n_blocks = self.n_blocks
         art.n_c = self.n_mult
@@ -160,9 +172,12 @@ class RomInstance:
             return N.ptr(x, C.c_double if kind == "f" else C.c_int64)
 
         decs = (N.Decoder * self.n_blocks)()
+        gdecs = (N.Decoder * self.n_blocks)() if self.srpc else None
         for b in range(self.n_blocks):
             self._fill_decoder(decs[b], f"b{b}_intf_", arr)
-        N.check(N.lib().ddnm_ctx_set_full_decoders(h, decs))
+            if self.srpc:
+                self._fill_decoder(gdecs[b], f"b{b}_gamf_", arr)
+        N.check(N.lib().ddnm_ctx_set_full_decoders(h, decs, gdecs))
 
     def decode(self, x, device: int = -1):
         """RomInstance.decode (driver.py:148-152) on the device:
@@ -489,9 +504,10 @@ class EvalBatch:
         ni, ng = L["n_int"], L["n_gam"]
         w = ni + ng
         r0, r1 = L["row"]
-        R = self.R[k, L["R"][0]:L["R"][1]].reshape(r1 - r0, w)
+        o0, o1 = L["out"]
+        R = self.R[k, L["R"][0]:L["R"][1]].reshape(o1 - o0, w)
         return {
-            "Br": self.Br[k, r0:r1], "R_int": R[:, :ni], "R_gam": R[:, ni:],
+            "Br": self.Br[k, o0:o1], "R_int": R[:, :ni], "R_gam": R[:, ni:],
             "con_val": self.cval[k, b], "con_jac": self.cjac[k, L["cjac"][0]:L["cjac"][1]]
             .reshape(-1, ng),
             "int_g": self.int_g[k, L["iout"][0]:L["iout"][1]],
@@ -515,8 +531,8 @@ def eval_gradients_batch(instance: RomInstance, mus, x, lam, *, reg_scale: float
     x = N.f64(x).reshape(B, nD)
     lam = N.f64(lam).reshape(B, nC)
     o = dict(rho=np.empty((B, nD)), con=np.empty((B, nC)), merit=np.empty(B),
-             objective=np.empty(B), Br=np.empty((B, inf.total_rows)),
-             R=np.empty((B, inf.total_R)), cval=np.empty((B, inf.n_blocks, nC)),
+             objective=np.empty(B), Br=np.empty((B, inf.total_out_rows)),
+             R=np.empty((B, inf.total_out_R)), cval=np.empty((B, inf.n_blocks, nC)),
              cjac=np.empty((B, inf.total_cjac)), int_g=np.empty((B, inf.total_int_out)),
              int_J=np.empty((B, inf.total_int_J)), gam_g=np.empty((B, inf.total_gam_out)),
              gam_J=np.empty((B, inf.total_gam_J)), bvals=np.empty((B, inf.total_rows, 3)),
@@ -528,14 +544,15 @@ def eval_gradients_batch(instance: RomInstance, mus, x, lam, *, reg_scale: float
             setattr(eo, k, N.ptr(v, C.c_int32 if v.dtype == np.int32 else C.c_double))
     N.check(N.lib().ddnm_eval_batch(ctx.h, B, N.ptr(mu), N.ptr(x), N.ptr(lam), reg_scale,
                                     C.byref(eo)))
-    layout, offs = {}, dict(row=0, R=0, cjac=0, iout=0, intJ=0, gout=0, gamJ=0)
+    layout, offs = {}, dict(row=0, out=0, R=0, cjac=0, iout=0, intJ=0, gout=0, gamJ=0)
     a = instance.arrays
     for b, (ni, ng) in enumerate(instance.latent_layout):
         p = f"b{b}_"
         nrows = a[p + "res_rows"].size
+        nout = a[p + "weights"].shape[0] if p + "weights" in a else nrows
         nio = a[p + "io"].size
-        ngo = int(a[p + "n_interface"])
-        sizes = dict(row=nrows, R=nrows * (ni + ng), cjac=nC * ng, iout=nio,
+        ngo = a[p + "gio"].size if instance.srpc else int(a[p + "n_interface"])
+        sizes = dict(row=nrows, out=nout, R=nout * (ni + ng), cjac=nC * ng, iout=nio,
                      intJ=nio * ni, gout=ngo, gamJ=ngo * ng)
         layout[b] = {"n_int": ni, "n_gam": ng}
         for key, sz in sizes.items():

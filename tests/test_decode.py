@@ -8,7 +8,7 @@ against its monolithic FOM solve (``solve_monolithic``) for three mu."""
 import numpy as np
 import pytest
 
-from tests.conftest import NAMES, golden_path
+from tests.conftest import ALL, golden_path
 
 
 def _states(name):
@@ -21,7 +21,7 @@ def _flat(blocks):
 
 # -- CPU: oracle pinned to the reference, host-side index helpers ---------------
 
-@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("name", ALL)
 def test_oracle_decode_matches_reference(name, oracle_instances):
     from oracle import ddnm_oracle as O
     inst, s = oracle_instances[name], _states(name)
@@ -62,7 +62,7 @@ def test_restrict_and_assemble_host_helpers(name, oracle_instances):
 # -- GPU: device decode ----------------------------------------------------------
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("name", ALL)
 def test_decode_matches_reference_golden(name, gpu_instances):
     import paper_2305_15163_b200 as P
     inst, s = gpu_instances[name], _states(name)

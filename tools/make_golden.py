@@ -50,9 +50,11 @@ def extract(inst) -> dict:
     grid = part.grid
     out = {}
     kind = "nm" if isinstance(inst.interior_maps[0], Autoencoder) else "ls"
+    srpc = inst.constraint_mode == "srpc"
     n_int = [m.latent_dim for m in inst.interior_maps]
     n_gam = [g.latent_dim for g in inst.interface_maps]
     act = inst.interior_maps[0].activation if kind == "nm" else "linear"
+    gam_act = inst.interface_maps[0].activation if kind == "nm" else "linear"
     for i, sub in enumerate(part.subdomains):
         hr = inst.hr[i]
         rows = hr.apply_B_rows()
@@ -65,7 +67,12 @@ def extract(inst) -> dict:
         out[p + "gio"] = gio.astype(np.int64)
         out[p + "n_interior"] = np.int64(sub.n_interior)
         out[p + "n_interface"] = np.int64(sub.n_interface)
-        out[p + "CA"] = inst.wfpc_C @ inst.fom_constraints.blocks[i].toarray()
+        if srpc:   # driver.py:374-378
+            out[p + "Ahat"] = inst.rom_constraints.blocks[i].toarray()
+        else:      # driver.py:366-373
+            out[p + "CA"] = inst.wfpc_C @ inst.fom_constraints.blocks[i].toarray()
+        if hr.mode == "gappy":   # hyper.py:107-118,153-160
+            out[p + "weights"] = np.ascontiguousarray(hr.weights)
         # global dof columns of the block (Partition.restrict, partition.py:232-235)
         out[p + "int_cols"] = sub.interior_cols.astype(np.int64)
         out[p + "gam_cols"] = sub.interface_cols.astype(np.int64)
@@ -82,6 +89,20 @@ def extract(inst) -> dict:
             out[p + "intf_shift"] = im.norm.shift.copy()
         else:
             out[p + "intf_Phi"] = np.ascontiguousarray(im.Phi)
+        if srpc:
+            # the residual uses the interface map restricted to gio
+            # (driver.py:400-402); the full map is kept for the decode
+            if kind == "nm":
+                W2f = gm.W2g.tocsr()
+                out[p + "gamf_W1"] = np.ascontiguousarray(gm.W1g)
+                out[p + "gamf_b1"] = gm.b1g.copy()
+                out[p + "gamf_W2_indptr"] = W2f.indptr.astype(np.int64)
+                out[p + "gamf_W2_indices"] = W2f.indices.astype(np.int64)
+                out[p + "gamf_W2_data"] = W2f.data.copy()
+                out[p + "gamf_scale"] = gm.norm.scale.copy()
+                out[p + "gamf_shift"] = gm.norm.shift.copy()
+            else:
+                out[p + "gamf_Phi"] = np.ascontiguousarray(gm.Phi)
         if kind == "nm":
             sn = extract_subnet(im, io)
             out[p + "int_W1"] = np.ascontiguousarray(sn.W1)
@@ -92,22 +113,40 @@ def extract(inst) -> dict:
             out[p + "int_scale"] = sn.scale.copy()
             out[p + "int_shift"] = sn.shift.copy()
             out[p + "int_hidden_idx"] = sn.hidden_idx.astype(np.int64)
-            W2g = gm.W2g.tocsr()
-            out[p + "gam_W1"] = np.ascontiguousarray(gm.W1g)
-            out[p + "gam_b1"] = gm.b1g.copy()
-            out[p + "gam_W2_indptr"] = W2g.indptr.astype(np.int64)
-            out[p + "gam_W2_indices"] = W2g.indices.astype(np.int64)
-            out[p + "gam_W2_data"] = W2g.data.copy()
-            out[p + "gam_scale"] = gm.norm.scale.copy()
-            out[p + "gam_shift"] = gm.norm.shift.copy()
+            if srpc:
+                sg = extract_subnet(gm, gio) if gio.size else None
+                H = sg.W1.shape[0] if sg is not None else 0
+                out[p + "gam_W1"] = (np.ascontiguousarray(sg.W1) if sg is not None
+                                     else np.zeros((0, gm.latent_dim)))
+                out[p + "gam_b1"] = sg.b1.copy() if sg is not None else np.zeros(0)
+                out[p + "gam_W2_indptr"] = (sg.W2.indptr.astype(np.int64) if sg is not None
+                                            else np.zeros(1, np.int64))
+                out[p + "gam_W2_indices"] = (sg.W2.indices.astype(np.int64) if sg is not None
+                                             else np.zeros(0, np.int64))
+                out[p + "gam_W2_data"] = sg.W2.data.copy() if sg is not None else np.zeros(0)
+                out[p + "gam_scale"] = sg.scale.copy() if sg is not None else np.zeros(0)
+                out[p + "gam_shift"] = sg.shift.copy() if sg is not None else np.zeros(0)
+                del H
+            else:
+                W2g = gm.W2g.tocsr()
+                out[p + "gam_W1"] = np.ascontiguousarray(gm.W1g)
+                out[p + "gam_b1"] = gm.b1g.copy()
+                out[p + "gam_W2_indptr"] = W2g.indptr.astype(np.int64)
+                out[p + "gam_W2_indices"] = W2g.indices.astype(np.int64)
+                out[p + "gam_W2_data"] = W2g.data.copy()
+                out[p + "gam_scale"] = gm.norm.scale.copy()
+                out[p + "gam_shift"] = gm.norm.shift.copy()
         else:
             assert isinstance(im, LinearMap) and isinstance(gm, LinearMap)
             out[p + "int_Phi"] = np.ascontiguousarray(im.restrict_outputs(io).Phi)
-            out[p + "gam_Phi"] = np.ascontiguousarray(gm.Phi)
+            out[p + "gam_Phi"] = np.ascontiguousarray(
+                gm.restrict_outputs(gio).Phi if srpc else gm.Phi)
     ini = inst.initializer
     rbf = ini._rbf
     meta = {
-        "kind": kind, "activation": act, "nx": grid.nx, "ny": grid.ny,
+        "kind": kind, "activation": act, "gam_activation": gam_act,
+        "constraint": inst.constraint_mode, "hr": inst.hr[0].mode,
+        "nx": grid.nx, "ny": grid.ny,
         "nu": grid.nu, "nsub_x": part.nsub_x, "nsub_y": part.nsub_y,
         "nblocks": len(part.subdomains), "n_int": n_int, "n_gam": n_gam,
         "n_c": int(inst.n_mult), "ndof": int(grid.ndof), "rbf_kernel": rbf.kernel,
@@ -198,18 +237,27 @@ def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
                 rows = inst.hr[i].apply_B_rows()
                 io, gio = hr_rows_for_subdomain(part, i, rows)
                 im, gm = inst.interior_maps[i], inst.interface_maps[i]
+                srpc = inst.constraint_mode == "srpc"
                 if hasattr(im, "restrict_outputs"):
                     si = im.restrict_outputs(io)
                 else:
                     si = extract_subnet(im, io)
+                if srpc and gio.size:
+                    gm = (gm.restrict_outputs(gio) if hasattr(gm, "restrict_outputs")
+                          else extract_subnet(gm, gio))
                 g[q + "int_g"] = si.decode(xi)
                 g[q + "int_J"] = np.asarray(si.jacobian(xi))
-                g[q + "gam_g"] = gm.decode(xg)
-                g[q + "gam_J"] = np.asarray(gm.jacobian(xg))
+                if srpc and not gio.size:
+                    g[q + "gam_g"] = np.zeros(0)
+                    g[q + "gam_J"] = np.zeros((0, xg.size))
+                else:
+                    g[q + "gam_g"] = gm.decode(xg)
+                    g[q + "gam_J"] = np.asarray(gm.jacobian(xg))
                 cols = np.concatenate([sub.interior_cols[io],
                                        sub.interface_cols[gio]])
                 rr = RestrictedResidual(ops, sub.res_rows[rows], cols)
-                v = np.concatenate([g[q + "int_g"], g[q + "gam_g"][gio]])
+                v = np.concatenate([g[q + "int_g"],
+                                    g[q + "gam_g"] if srpc else g[q + "gam_g"][gio]])
                 g[q + "stencil_r"] = rr.residual(v)
                 g[q + "stencil_Jd"] = rr.jacobian(v).toarray()
                 n = part.grid.nnode
@@ -248,7 +296,8 @@ def main():
     ap.add_argument("--cache", default=os.path.join(ROOT, "artifacts_cache"))
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden"))
     ap.add_argument("--names", nargs="*",
-                    default=["tiny_nm", "tiny_ls", "c0_nm", "c0_ls"])
+                    default=["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "tiny_nmg", "tiny_srpc",
+                             "tiny_lsg", "tiny_lss", "c0_nmg", "c0_srpc"])
     ap.add_argument("--B", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--detail", type=int, default=3)
