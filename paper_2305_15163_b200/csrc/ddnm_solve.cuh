@@ -1680,7 +1680,7 @@ static __device__ void row_bvals(const Params& P, const StRows& RW, int row, dou
 // the persistent kernel
 
 template <int G, int NI, int NG>
-__global__ void __launch_bounds__(DDNM_MAX_THREADS) k_solve(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_constant__ Params P) {
   View V(P, ddnm_smem);
   SlotState* st = V.st();
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
