@@ -264,6 +264,47 @@ int ddnm_decode_batch_device(ddnm_ctx* ctx, int32_t B, const double* d_x,
                              const double* d_fom, double* d_states,
                              double* d_err, void* stream);
 
+
+/* ---- subdomain-sharded solve -------------------
+ * Round-synchronous batched SQP in which each rank evaluates only its blocks
+ * [blk_lo, blk_hi) of every mu (the HR residual closures of driver.py:404-432
+ * and the constraint closures, one SqpBlock each, sqp.py:28-41), the block
+ * pieces (Gram H_b = R_b^T R_b, R_b^T r_b, cval_b, cjac_b, r_b^T r_b -- what
+ * eval_gradients and _kkt_matrix need of a block, sqp.py:117-159) are
+ * all-gathered, and every rank then runs the identical SQP decision and KKT
+ * solve (sqp.py:230-299), so all ranks hold bit-identical results.  The
+ * caller owns the collective (NCCL all-gather between the eval and the step);
+ * with one rank the packets are the gathered buffer.  Device pointers; all
+ * work is asynchronous on `stream` -- the caller's cudaStream_t, used as is
+ * (0 is the legacy default stream, not the context's stream), so kernels
+ * order with the caller's collective -- except where a count is returned. */
+typedef struct ddnm_dd ddnm_dd;
+
+/* Doubles of one mu's packet for blocks [blk_lo, blk_hi). */
+int ddnm_dd_packet_len(const ddnm_ctx* ctx, int32_t blk_lo, int32_t blk_hi, int64_t* len);
+
+/* Start a sharded solve of B parameters (device arrays as in
+ * ddnm_solve_batch_device); this rank evaluates blocks [blk_lo, blk_hi).
+ * Results are written to d_out as slots finish.  n_active (host, may be
+ * NULL) receives the number of running mu (synchronises the stream). */
+int ddnm_dd_begin(ddnm_ctx* ctx, int32_t B, const double* d_mu, const double* d_x0,
+                  const double* d_lam0, const ddnm_sqp_cfg* cfg, int32_t blk_lo,
+                  int32_t blk_hi, const ddnm_solve_out* d_out, void* stream,
+                  ddnm_dd** out, int32_t* n_active);
+
+/* This rank's block pieces at every running mu's trial point:
+ * d_packets[B][pk_stride] (pk_stride >= ddnm_dd_packet_len of the range). */
+int ddnm_dd_eval(ddnm_dd* dd, double* d_packets, int64_t pk_stride, void* stream);
+
+/* One SQP round from the gathered pieces d_gathered[nranks][B][pk_stride];
+ * rank r evaluated blocks [bounds[r], bounds[r+1]) (bounds[0] = 0,
+ * bounds[nranks] = n_blocks).  n_active as in ddnm_dd_begin. */
+int ddnm_dd_step(ddnm_dd* dd, const double* d_gathered, int32_t nranks,
+                 const int32_t* bounds, int64_t pk_stride, void* stream,
+                 int32_t* n_active);
+
+int ddnm_dd_end(ddnm_dd* dd);
+
 #ifdef __cplusplus
 }
 #endif

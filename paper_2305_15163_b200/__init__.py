@@ -12,6 +12,8 @@ from .driver import (BatchResult, DecodeBatch, EvalBatch, RomInstance, RomSoluti
                      build_problem, decode_batch, eval_gradients_batch, init_guess,
                      solve_rom, solve_rom_batch)
 from .errors import ConvergenceError, FormatError, SingularityError
+from .subdomain import (ShardedSolve, block_bounds,
+                        solve_rom_batch_subdomain_sharded)
 from .sqp import SqpBlock, SqpConfig, SqpProblem, SqpResult, iterate
 
 __version__ = "0.1.0"
@@ -23,4 +25,5 @@ __all__ = [
     "eval_gradients_batch", "init_guess", "solve_rom", "solve_rom_batch",
     "ConvergenceError", "FormatError", "SingularityError",
     "SqpBlock", "SqpConfig", "SqpProblem", "SqpResult", "iterate",
+    "ShardedSolve", "block_bounds", "solve_rom_batch_subdomain_sharded",
 ]

@@ -127,6 +127,14 @@ def lib():
     L.ddnm_decode_batch.argtypes = [C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp]
     L.ddnm_decode_batch_device.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddnm_dd_packet_len.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _lp]
+    L.ddnm_dd_begin.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.POINTER(SqpCfg), C.c_int32, C.c_int32, C.POINTER(SolveOut),
+                                C.c_void_p, C.POINTER(C.c_void_p), _ip]
+    L.ddnm_dd_eval.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    L.ddnm_dd_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _ip, C.c_int64, C.c_void_p,
+                               _ip]
+    L.ddnm_dd_end.argtypes = [C.c_void_p]
     if L.ddnm_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libddnm.so ABI version mismatch; rebuild")
     _lib = L
@@ -137,7 +145,8 @@ EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_
             "ddnm_ctx_info", "ddnm_solve_batch", "ddnm_solve_batch_device",
             "ddnm_eval_batch", "ddnm_last_counters", "ddnm_last_profile",
             "ddnm_ctx_set_full_decoders", "ddnm_ctx_state_len", "ddnm_decode_batch",
-            "ddnm_decode_batch_device")
+            "ddnm_decode_batch_device", "ddnm_dd_packet_len", "ddnm_dd_begin",
+            "ddnm_dd_eval", "ddnm_dd_step", "ddnm_dd_end")
 
 
 def check(rc: int):

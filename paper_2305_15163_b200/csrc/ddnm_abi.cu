@@ -95,6 +95,8 @@ struct ddnm_ctx {
   double* gbv = nullptr;      // boundary values per global slot
   double* gJ = nullptr;       // interior Jacobian rows per global slot
   double* gJg = nullptr;      // interface Jacobian rows per global slot
+  double* kkt_g = nullptr;    // KKT workspace per global slot (KG kernels)
+  size_t kkt_stride = 0;      // doubles per slot, 0: KKT in shared memory
   size_t gbv_slots = 0;
   int* work = nullptr;
   unsigned long long* counters = nullptr;
@@ -481,6 +483,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   }
   P.n_D = xoff;
   P.nK = P.n_D + P.n_C;
+  P.b_lo = 0;
+  P.b_hi = P.nb;
   P.total_rows = row_off;
   P.tot_iout = iout; P.tot_gout = gout; P.tot_R = Roff; P.tot_cjac = cjoff;
   P.tot_intJ = ijoff; P.tot_gamJ = gjoff;
@@ -546,13 +550,15 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // preferring the interior Jacobian rows in shared memory
   const size_t smem_cap = (size_t)prop.sharedMemPerBlockOptin - 1024;
   const int rbf_need2 = rbf_need;
-  auto scr_total = [&](int level) {
+  // kg: the KKT workspace lives in a per-slot global scratch (kernels
+  // instantiated with KG = true), so it does not count against shared memory
+  auto scr_total = [&](int level, bool kg = false) {
     int s0 = plan_scratch(level);
-    int t = std::max(std::max(s0, kkt_need), std::max(ls_need, rbf_need2));
+    int t = std::max(std::max(s0, kg ? 0 : kkt_need), std::max(ls_need, rbf_need2));
     return (t + 1) & ~1;
   };
-  auto footprint = [&](int G, int level) {
-    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + scr_total(level))) * 8;
+  auto footprint = [&](int G, int level, bool kg = false) {
+    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + scr_total(level, kg))) * 8;
   };
   const Kernels* kern = nullptr;
   int kern_level = 0;
@@ -561,13 +567,16 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // largest G that fits wins, at the lowest level that fits it (measured at
   // config 0 with the tensor-core Gram: 4 slots with the Jacobian rows in L2
   // 35.7-37.1 ms per 4096 mu, vs 41.5 ms for 2 slots with them in shared memory)
-  for (const auto& k : kernel_table()) {
-    if (k.ni != ni || k.ng != ng) continue;
-    if (slots > 0 && k.g != slots) continue;
-    for (int level = lvl_lo; level <= lvl_hi; ++level) {
-      if (footprint(k.g, level) > smem_cap) continue;
-      if (!kern || k.g > kern->g) { kern = &k; kern_level = level; }
-      break;
+  // kernels with the KKT workspace in global memory only when nothing else fits
+  for (int pass = 0; pass < 2 && !kern; ++pass) {
+    for (const auto& k : kernel_table()) {
+      if (k.ni != ni || k.ng != ng || k.kkt_global != (pass == 1)) continue;
+      if (slots > 0 && k.g != slots) continue;
+      for (int level = lvl_lo; level <= lvl_hi; ++level) {
+        if (footprint(k.g, level, k.kkt_global) > smem_cap) continue;
+        if (!kern || k.g > kern->g) { kern = &k; kern_level = level; }
+        break;
+      }
     }
   }
   if (!kern) {
@@ -576,8 +585,10 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
              ni, ng, slots, smem_cap);
     return bail(fail(DDNM_EUNSUPPORTED, buf));
   }
-  P.scr_size = scr_total(kern_level);
+  P.scr_size = scr_total(kern_level, kern->kkt_global);
   c->K = *kern;
+  c->kkt_stride = kern->kkt_global ? (size_t)((kkt_need + 31) & ~31) : 0;
+  P.kkt_stride = (long long)c->kkt_stride;
   // tiles of consecutive outputs for the tensor-core sweep (P = 8 / G outputs each)
   if (getenv("DDNM_DMMA") && ae && 8 % kern->g == 0) {
     const int Pt = 8 / kern->g;
@@ -637,9 +648,11 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.sm_vec = state_d * P.G;
   P.sm_eb = P.sm_vec + P.G * 8 * P.nK;
   P.sm_scr = P.sm_eb + P.G * 2 * P.eb_size;
-  c->smem = footprint(P.G, kern_level);
+  c->smem = footprint(P.G, kern_level, kern->kkt_global);
   if (cudaFuncSetAttribute(kern->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
-      cudaFuncSetAttribute(kern->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess)
+      cudaFuncSetAttribute(kern->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
+      cudaFuncSetAttribute(kern->dd_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
+      cudaFuncSetAttribute(kern->dd_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cannot reserve dynamic shared memory"));
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern->solve, c->threads, c->smem) != cudaSuccess || occ < 1)
@@ -661,6 +674,7 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   if (c->gbv) cudaFree(c->gbv);
   if (c->gJ) cudaFree(c->gJ);
   if (c->gJg) cudaFree(c->gJg);
+  if (c->kkt_g) cudaFree(c->kkt_g);
   if (c->work) cudaFree(c->work);
   if (c->counters) cudaFree(c->counters);
   if (c->prof) cudaFree(c->prof);
@@ -703,6 +717,9 @@ static int ensure_gbv(ddnm_ctx* c, size_t slots) {
   if (c->gJg) cudaFree(c->gJg);
   c->gJg = nullptr;
   CUDA_TRY(cudaMalloc(&c->gJg, slots * std::max(c->P.gJg_stride, 1) * sizeof(double)));
+  if (c->kkt_g) cudaFree(c->kkt_g);
+  c->kkt_g = nullptr;
+  if (c->kkt_stride) CUDA_TRY(cudaMalloc(&c->kkt_g, slots * c->kkt_stride * sizeof(double)));
   c->gbv_slots = slots;
   return 0;
 }
@@ -747,6 +764,7 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
   P.gbv = c->gbv;
   P.gJ = c->gJ;
   P.gJg = c->gJg;
+  P.kkt_g = c->kkt_g;
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
@@ -886,6 +904,7 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
   P.gbv = c->gbv;
   P.gJ = c->gJ;
   P.gJg = c->gJg;
+  P.kkt_g = c->kkt_g;
   P.work = c->work;
   P.counters = c->counters;
   void* args[] = {&P};
@@ -1005,6 +1024,171 @@ int ddnm_decode_batch(ddnm_ctx* c, int32_t B, const double* x, const double* fom
   if (err) CUDA_TRY(cudaMemcpyAsync(err, de, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+
+// ---- subdomain-sharded round-synchronous solve ----------
+
+}  // extern "C"
+
+struct ddnm_dd {
+  ddnm_ctx* c = nullptr;
+  Params P{};
+  int B = 0, ctas = 0;
+  SlotState* st = nullptr;
+  double* vec = nullptr;
+  double* ecur = nullptr;
+  int* active = nullptr;
+  cudaStream_t stream = nullptr;  // the caller's stream of the last call
+};
+
+namespace {
+int eb_span(const ddnm_ctx* c, int lo, int hi, int* off) {
+  const Params& P = c->P;
+  if (lo < 0 || hi > P.nb || lo >= hi) return fail(DDNM_EINVAL, "empty or out-of-range block range");
+  *off = P.blk[lo].eb_off;
+  return (hi < P.nb ? P.blk[hi].eb_off : P.eb_rho) - *off;
+}
+
+int dd_run(ddnm_dd* d, const void* kern, cudaStream_t s, int32_t* n_active) {
+  ddnm_ctx* c = d->c;
+  CUDA_TRY(cudaMemsetAsync(d->active, 0, sizeof(int), s));
+  void* args[] = {&d->P};
+  CUDA_TRY(cudaLaunchKernel(kern, dim3(d->ctas), dim3(c->threads), args, c->smem, s));
+  if (n_active) {
+    int h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, d->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *n_active = h;
+  }
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int ddnm_dd_packet_len(const ddnm_ctx* c, int32_t blk_lo, int32_t blk_hi, int64_t* len) {
+  if (!c || !len) return fail(DDNM_EINVAL, "null argument");
+  int off = 0;
+  const int n = eb_span(c, blk_lo, blk_hi, &off);
+  if (n < 0) return n;
+  *len = n;
+  return 0;
+}
+
+int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0,
+                  const double* d_lam0, const ddnm_sqp_cfg* cfg, int32_t blk_lo, int32_t blk_hi,
+                  const ddnm_solve_out* o, void* stream, ddnm_dd** out, int32_t* n_active) {
+  if (!c || !cfg || !o || !out || !d_mu || !o->x || !o->lam) return fail(DDNM_EINVAL, "null argument");
+  *out = nullptr;
+  if (B < 1) return fail(DDNM_EINVAL, "batch must be positive");
+  if (!(cfg->tol > 0) || cfg->max_iter < 1 || !(cfg->armijo_c1 > 0) || !(cfg->backtrack_factor > 0) ||
+      !(cfg->backtrack_factor < 1) || cfg->max_halvings < 0)
+    return fail(DDNM_EINVAL, "invalid solver configuration");
+  if (!d_x0 && c->P.rbf_P == 0) return fail(DDNM_EINVAL, "instance has no fitted initializer");
+  int off = 0;
+  int rc = eb_span(c, blk_lo, blk_hi, &off);
+  if (rc < 0) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* d = new ddnm_dd();
+  d->stream = s;
+  d->c = c;
+  d->B = B;
+  d->ctas = (B + c->P.G - 1) / c->P.G;
+  auto bail = [&](int r) { ddnm_dd_end(d); return r; };
+  if ((rc = ensure_gbv(c, (size_t)d->ctas * c->P.G))) return bail(rc);
+  if (cudaMalloc(&d->st, (size_t)B * sizeof(SlotState)) != cudaSuccess ||
+      cudaMalloc(&d->vec, (size_t)B * 8 * c->P.nK * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&d->ecur, (size_t)B * c->P.eb_size * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&d->active, sizeof(int)) != cudaSuccess)
+    return bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve state"));
+  Params& P = d->P;
+  P = c->P;
+  P.B = B;
+  P.mu = d_mu;
+  P.x0_in = d_x0;
+  P.lam0_in = d_lam0;
+  P.cfg.tol = cfg->tol;
+  P.cfg.c1 = cfg->armijo_c1;
+  P.cfg.factor = cfg->backtrack_factor;
+  P.cfg.reg_scale = cfg->reg_scale;
+  P.cfg.max_iter = cfg->max_iter;
+  P.cfg.max_halvings = cfg->max_halvings;
+  P.so.x = o->x; P.so.lam = o->lam; P.so.merit = o->merit; P.so.objective = o->objective;
+  P.so.merit_hist = o->merit_hist; P.so.obj_hist = o->obj_hist; P.so.alpha_hist = o->alpha_hist;
+  P.so.x0 = o->x0; P.so.lam0 = o->lam0;
+  P.so.n_iter = o->n_iter; P.so.n_evals = o->n_evals; P.so.status = o->status; P.so.n_reg = o->n_reg;
+  P.gbv = c->gbv;
+  P.gJ = c->gJ;
+  P.gJg = c->gJg;
+  P.kkt_g = c->kkt_g;
+  P.work = c->work;
+  P.counters = c->counters;
+  P.prof = nullptr;
+  P.b_lo = blk_lo;
+  P.b_hi = blk_hi;
+  P.dd_st = d->st;
+  P.dd_vec = d->vec;
+  P.dd_ecur = d->ecur;
+  P.dd_active = d->active;
+  if ((rc = fill_nan(s, o->merit_hist, (size_t)B * (cfg->max_iter + 1)))) return bail(rc);
+  if ((rc = fill_nan(s, o->obj_hist, (size_t)B * (cfg->max_iter + 1)))) return bail(rc);
+  if ((rc = fill_nan(s, o->alpha_hist, (size_t)B * cfg->max_iter))) return bail(rc);
+  if (cudaMemsetAsync(c->counters, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess)
+    return bail(fail(DDNM_ECUDA, "memset failed"));
+  P.dd_init = 1;
+  if ((rc = dd_run(d, c->K.dd_step, s, n_active))) return bail(rc);
+  P.dd_init = 0;
+  *out = d;
+  return 0;
+}
+
+int ddnm_dd_eval(ddnm_dd* d, double* d_packets, int64_t pk_stride, void* stream) {
+  if (!d || !d_packets) return fail(DDNM_EINVAL, "null argument");
+  int off = 0;
+  const int len = eb_span(d->c, d->P.b_lo, d->P.b_hi, &off);
+  if (pk_stride < len) return fail(DDNM_EINVAL, "packet stride shorter than this rank's packet");
+  CUDA_TRY(cudaSetDevice(d->c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  d->stream = s;
+  d->P.dd_pk = d_packets;
+  d->P.pk_stride = (int)pk_stride;
+  return dd_run(d, d->c->K.dd_eval, s, nullptr);
+}
+
+int ddnm_dd_step(ddnm_dd* d, const double* d_gathered, int32_t nranks, const int32_t* bounds,
+                 int64_t pk_stride, void* stream, int32_t* n_active) {
+  if (!d || !d_gathered || !bounds) return fail(DDNM_EINVAL, "null argument");
+  const int nb = d->P.nb;
+  if (nranks < 1 || nranks > nb) return fail(DDNM_EINVAL, "need 1..n_blocks ranks");
+  if (bounds[0] != 0 || bounds[nranks] != nb) return fail(DDNM_EINVAL, "rank bounds must cover every block");
+  for (int r = 0; r < nranks; ++r) {
+    int off = 0;
+    const int len = eb_span(d->c, bounds[r], bounds[r + 1], &off);
+    if (len < 0) return len;
+    if (len > pk_stride) return fail(DDNM_EINVAL, "packet stride shorter than a rank's packet");
+  }
+  CUDA_TRY(cudaSetDevice(d->c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  d->stream = s;
+  d->P.dd_gath = d_gathered;
+  d->P.dd_nranks = nranks;
+  d->P.pk_stride = (int)pk_stride;
+  for (int r = 0; r <= nranks; ++r) d->P.dd_bnd[r] = bounds[r];
+  return dd_run(d, d->c->K.dd_step, s, n_active);
+}
+
+int ddnm_dd_end(ddnm_dd* d) {
+  if (!d) return 0;
+  cudaSetDevice(d->c->device);
+  cudaStreamSynchronize(d->stream);
+  if (d->st) cudaFree(d->st);
+  if (d->vec) cudaFree(d->vec);
+  if (d->ecur) cudaFree(d->ecur);
+  if (d->active) cudaFree(d->active);
+  delete d;
   return 0;
 }
 

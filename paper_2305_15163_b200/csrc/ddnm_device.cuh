@@ -108,6 +108,12 @@ struct BlockDev {
   int out_off, outR_off;  // offsets of the weighted rows in the Br / R dumps
 };
 
+struct SlotState {
+  int mu, phase, n_iter, n_trials, n_evals, n_reg, status, need_kkt;
+  int lam_given, pad;
+  double alpha, merit, obj, best_merit;
+};
+
 struct SqpCfg {
   double tol, c1, factor, reg_scale;
   int max_iter, max_halvings;
@@ -169,6 +175,20 @@ struct Params {
   int* work;              // [0]: next mu; [1]: finished CTAs
   unsigned long long* counters;  // [0] block-evals, [1] KKT solves
   unsigned long long* prof;      // [15] per-phase clock totals (DDNM_PROF=1), or null
+  // blocks evaluated by eval_blocks: [b_lo, b_hi) (all blocks except in k_dd_eval)
+  int b_lo, b_hi;
+  // round-synchronous subdomain-sharded solve (k_dd_eval / k_dd_step)
+  SlotState* dd_st;       // [B] per-mu SQP state
+  double* dd_vec;         // [B][8][nK] x, lam, s, slam, xt, lt, best x, best lam
+  double* dd_ecur;        // [B][eb_size] current (accepted) evaluation
+  double* dd_pk;          // [B][pk_stride] this rank's block pieces (k_dd_eval)
+  const double* dd_gath;  // [dd_nranks][B][pk_stride] gathered pieces (k_dd_step)
+  int pk_stride, dd_nranks, dd_init;
+  int dd_bnd[MAXB + 1];   // block range of rank r: [dd_bnd[r], dd_bnd[r+1])
+  int* dd_active;         // k_dd_step: count of slots still running
+  // KKT workspace in global memory (kernels instantiated with KG = true)
+  double* kkt_g;          // per global slot [kkt_stride]
+  long long kkt_stride;
 };
 
 // RomInstance.decode (driver.py:148-152): one full decoder of one block.
@@ -188,11 +208,6 @@ struct DecodeParams {
   double* err;            // [B] relative_error (driver.py:496-507) when fom
 };
 
-struct SlotState {
-  int mu, phase, n_iter, n_trials, n_evals, n_reg, status, need_kkt;
-  int lam_given, pad;
-  double alpha, merit, obj, best_merit;
-};
 
 // ---------------------------------------------------------------------------
 // scalar helpers

@@ -5,7 +5,10 @@
 namespace ddnm {
 struct KernelEntry {
   int ni, ng, g;
+  bool kkt_global;       // KKT workspace in global memory (kernels with KG = true)
   const void* solve;
   const void* eval;
+  const void* dd_eval;   // subdomain-sharded round kernels
+  const void* dd_step;
 };
 }  // namespace ddnm

@@ -525,7 +525,7 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
   const int lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   SlotState* st = V.st();
   constexpr int W = NI + NG;
-  for (int b = 0; b < P.nb; ++b) {
+  for (int b = P.b_lo; b < P.b_hi; ++b) {
     const BlockDev& B = P.blk[b];
     const int nhi = P.map_kind == MAP_AE ? B.in.n_hidden : 0;
     // ---- phase A: hidden layer of both decoders ----
@@ -1278,6 +1278,15 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
 // Blocks run on separate warps.  If a multiplier row would win a pivot (or
 // a pivot is exactly zero) the slot falls back to the dense warp LU, so the
 // pivot sequence always equals the dense one.
+// KKT workspace of slot s: shared memory, or (KG: instances whose KKT
+// matrices do not fit next to the evaluation scratch, e.g. 16 blocks with
+// n_C = 40) a per-slot global scratch that stays L2-resident while in use
+template <bool KG>
+__device__ __forceinline__ double* kws(const View& V, int s) {
+  if constexpr (KG) return V.P.kkt_g + (size_t)(V.gslot0 + s) * V.P.kkt_stride;
+  else return V.scr(s);
+}
+
 struct KktLayout {
   int ldm, msz, off_piv, off_S, off_pivS, off_tE, off_rhs, off_sol, off_res, off_tmp, ldS;
 };
@@ -1410,7 +1419,7 @@ __device__ void kkt_block_backward(const Params& P, const double* M, double* y, 
 // CTA-wide KKT stage for every slot in kmask (eval buffer ebi[s]).
 // Solution (s, s_lam) -> vec(s, 2), vec(s, 3); kres[s] = 0 ok, 1 regularized,
 // 2 singular.  Warp w < G*nb works on (slot w / nb, block w % nb).
-template <int G, int NI, int NG>
+template <int G, int NI, int NG, bool KG>
 __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kres,
                           int* kflag) {
   const Params& P = V.P;
@@ -1426,7 +1435,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   for (int t = warp; t < G * nb; t += nw) {
     const int s = t / nb, b = t - s * nb;
     if (!((kmask >> s) & 1u) || !kflag[s]) continue;
-    double* sc = V.scr(s);
+    double* sc = kws<KG>(V, s);
     const bool ok = kkt_block_factor<NI, NG>(P, V.eb(s, ebi[s]), b, sc + b * L.msz,
                                              reinterpret_cast<int*>(sc + L.off_piv) + b * W);
     if (!ok && lane == 0) atomicAnd(&kflag[s], 0);
@@ -1436,7 +1445,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   // 2. Schur block S = sum_b (in block order), its LU; rhs = -[rho; con]
   if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
     const int s = warp;
-    double* sc = V.scr(s);
+    double* sc = kws<KG>(V, s);
     double* S = sc + L.off_S;
     for (int idx = lane; idx < nC * nC; idx += WARP) {
       const int i = idx / nC, j = idx - i * nC;
@@ -1459,7 +1468,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     for (int t = warp; t < G * nb; t += nw) {
       const int s = t / nb, b = t - s * nb;
       if (!((kmask >> s) & 1u) || !kflag[s]) continue;
-      double* sc = V.scr(s);
+      double* sc = kws<KG>(V, s);
       double* y = sc + (pass == 0 ? L.off_sol : L.off_res) + b * W;
       const double* src = sc + (pass == 0 ? L.off_rhs : L.off_res) + b * W;
       if (pass == 0) for (int i = lane; i < W; i += WARP) y[i] = src[i];
@@ -1472,7 +1481,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     DDNM_MARK(V, 10);
     if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
       const int s = warp;
-      double* sc = V.scr(s);
+      double* sc = kws<KG>(V, s);
       double* y = sc + (pass == 0 ? L.off_sol : L.off_res) + P.n_D;
       const double* src = sc + (pass == 0 ? L.off_rhs : L.off_res) + P.n_D;
       for (int c = lane; c < nC; c += WARP) {
@@ -1488,7 +1497,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     for (int t = warp; t < G * nb; t += nw) {
       const int s = t / nb, b = t - s * nb;
       if (!((kmask >> s) & 1u) || !kflag[s]) continue;
-      double* sc = V.scr(s);
+      double* sc = kws<KG>(V, s);
       double* y = sc + (pass == 0 ? L.off_sol : L.off_res);
       kkt_block_backward<NI, NG>(P, sc + b * L.msz, y + b * W, y + P.n_D);
     }
@@ -1496,7 +1505,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
     DDNM_MARK(V, 10);
     if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
       const int s = warp;
-      double* sc = V.scr(s);
+      double* sc = kws<KG>(V, s);
       const double* e = V.eb(s, ebi[s]);
       double* sol = sc + L.off_sol;
       double* res = sc + L.off_res;
@@ -1540,7 +1549,7 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   // slot at a time with the whole CTA
   for (int ss = 0; ss < G; ++ss) {
     if (!((kmask >> ss) & 1u) || kflag[ss]) continue;   // uniform (shared flags)
-    double* work = V.scr(ss);
+    double* work = kws<KG>(V, ss);
     double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
     const int r = cta_kkt<NI, NG>(P, V.eb(ss, ebi[ss]), work, sol);
     if (warp == 0) {
@@ -1677,14 +1686,204 @@ static __device__ void row_bvals(const Params& P, const StRows& RW, int row, dou
 }
 
 // --------------------------------------------------------------------------
+// per-slot pieces of one SQP round, shared by the persistent kernel (k_solve)
+// and the round-synchronous subdomain-sharded kernels (k_dd_eval / k_dd_step)
+
+// a new parameter: boundary values of every sampled row (CTA-wide)
+__device__ __forceinline__ void slot_bvals(const View& V, int s, int mu) {
+  const Params& P = V.P;
+  const double a = P.mu[2 * mu], lm = P.mu[2 * mu + 1];
+  double* gb = P.gbv + (size_t)(V.gslot0 + s) * P.total_rows * 3;
+  for (int b = 0; b < P.nb; ++b) {
+    const BlockDev& B = P.blk[b];
+    for (int r = threadIdx.x; r < B.nrows; r += blockDim.x)
+      row_bvals(P, B.rows, r, a, lm, gb + (B.row_off + r) * 3);
+  }
+}
+
+// a new parameter: initial latents (given or RBF, driver.py:82-90) into xt
+// and the given multipliers (or 0 before the least squares) into lt (warp s)
+__device__ __forceinline__ void slot_start(const View& V, int s) {
+  const Params& P = V.P;
+  const int lane = threadIdx.x & 31;
+  const int mu = V.st()[s].mu;
+  double* xt = V.vec(s, 4);
+  double* lt = V.vec(s, 5);
+  if (P.x0_in) {
+    for (int j = lane; j < P.n_D; j += WARP) xt[j] = P.x0_in[(size_t)mu * P.n_D + j];
+  } else {
+    warp_rbf(P, P.mu[2 * mu], P.mu[2 * mu + 1], xt, V.scr(s));
+  }
+  for (int c = lane; c < P.n_C; c += WARP) lt[c] = P.lam0_in ? P.lam0_in[(size_t)mu * P.n_C + c] : 0.0;
+  if (lane == 0) V.st()[s].lam_given = P.lam0_in != nullptr;
+  __syncwarp();
+  if (P.so.x0) for (int j = lane; j < P.n_D; j += WARP) P.so.x0[(size_t)mu * P.n_D + j] = xt[j];
+}
+
+// the SQP decision after slot s's evaluation in eval buffer ebi (warp s):
+// initial point (least-squares multipliers, driver.py:461-471), Armijo test,
+// best-iterate bookkeeping and line-search failure (sqp.py:255-293), the
+// tol / max_iter test; sets need_kkt when a step is required.
+template <int NI, int NG>
+__device__ __forceinline__ void slot_decide(const View& V, int s, int ebi, int* cur) {
+  const Params& P = V.P;
+  const SqpCfg& cfg = P.cfg;
+  const int lane = threadIdx.x & 31;
+  SlotState& S = V.st()[s];
+  const int mu = S.mu;
+  double* e = V.eb(s, ebi);
+  double* lt = V.vec(s, 5);
+  double* x = V.vec(s, 0);
+  double* lam = V.vec(s, 1);
+  double* xt = V.vec(s, 4);
+  finalize_eval<NI, NG>(V, s, e, lt);
+  bool check = false;
+  if (S.phase == PH_INIT) {
+    if (!S.lam_given) {
+      // multiplier least squares at lam = 0, then rho at lam0
+      const bool ok = warp_lstsq<NI, NG>(P, e, V.scr(s), lt);
+      if (!ok) {
+        if (lane == 0) { S.status = ST_LSTSQ_RANK; }
+      }
+      __syncwarp();
+      finalize_eval<NI, NG>(V, s, e, lt);
+    }
+    if (P.so.lam0) for (int c = lane; c < P.n_C; c += WARP) P.so.lam0[(size_t)mu * P.n_C + c] = lt[c];
+    for (int j = lane; j < P.n_D; j += WARP) { x[j] = xt[j]; V.vec(s, 6)[j] = xt[j]; }
+    for (int c = lane; c < P.n_C; c += WARP) { lam[c] = lt[c]; V.vec(s, 7)[c] = lt[c]; }
+    if (lane == 0) {
+      S.merit = e[P.eb_scal]; S.obj = e[P.eb_scal + 1]; S.best_merit = S.merit;
+      S.n_evals = 1;
+      if (P.so.merit_hist) P.so.merit_hist[(size_t)mu * (cfg.max_iter + 1)] = S.merit;
+      if (P.so.obj_hist) P.so.obj_hist[(size_t)mu * (cfg.max_iter + 1)] = S.obj;
+    }
+    check = true;
+  } else {  // PH_TRIAL
+    const double tm = e[P.eb_scal];
+    const double rhs = (1.0 - cfg.c1 * S.alpha) * S.merit;
+    if (lane == 0) S.n_evals += 1;
+    if (tm <= rhs) {
+      for (int j = lane; j < P.n_D; j += WARP) x[j] = xt[j];
+      for (int c = lane; c < P.n_C; c += WARP) lam[c] = lt[c];
+      __syncwarp();
+      if (lane == 0) {
+        cur[s] = ebi;
+        if (P.so.alpha_hist) P.so.alpha_hist[(size_t)mu * cfg.max_iter + S.n_iter] = S.alpha;
+        S.n_iter += 1;
+        S.merit = tm; S.obj = e[P.eb_scal + 1];
+        if (P.so.merit_hist) P.so.merit_hist[(size_t)mu * (cfg.max_iter + 1) + S.n_iter] = S.merit;
+        if (P.so.obj_hist) P.so.obj_hist[(size_t)mu * (cfg.max_iter + 1) + S.n_iter] = S.obj;
+      }
+      const bool better = tm < S.best_merit;
+      __syncwarp();
+      if (better) {
+        for (int j = lane; j < P.n_D; j += WARP) V.vec(s, 6)[j] = x[j];
+        for (int c = lane; c < P.n_C; c += WARP) V.vec(s, 7)[c] = lam[c];
+        if (lane == 0) S.best_merit = tm;
+      }
+      check = true;
+    } else {
+      const int tr = S.n_trials + 1;
+      __syncwarp();
+      if (tr >= cfg.max_halvings + 1) {
+        // line-search failure: return the best iterate (sqp.py:275-293)
+        for (int j = lane; j < P.n_D; j += WARP) x[j] = V.vec(s, 6)[j];
+        for (int c = lane; c < P.n_C; c += WARP) lam[c] = V.vec(s, 7)[c];
+        if (lane == 0) { S.status = ST_LINE_SEARCH; S.phase = PH_DONE; S.n_trials = tr; }
+      } else {
+        const double al = S.alpha * cfg.factor;
+        const double* sv = V.vec(s, 2);
+        const double* sl = V.vec(s, 3);
+        for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], __dmul_rn(al, sv[j]));
+        for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], __dmul_rn(al, sl[c]));
+        if (lane == 0) { S.alpha = al; S.n_trials = tr; }
+      }
+    }
+  }
+  __syncwarp();
+  if (check) {
+    if (S.status == ST_LSTSQ_RANK) {
+      if (lane == 0) S.phase = PH_DONE;
+    } else if (!(S.merit >= cfg.tol && S.n_iter < cfg.max_iter)) {
+      if (lane == 0) S.phase = PH_DONE;
+    } else {
+      if (lane == 0) S.need_kkt = 1;
+    }
+  }
+  __syncwarp();
+}
+
+// KKT solves of every slot that needs a step (CTA-wide, block-structured LU
+// with the dense fallback), then the full-step trial point (sqp.py:162-208,
+// 262-265).  Ends with __syncthreads when any slot needed a step.
+template <int G, int NI, int NG, bool KG>
+__device__ __forceinline__ void kkt_advance(const View& V, const int* cur, int* kres, int* kflag,
+                                            unsigned long long* kkts) {
+  const Params& P = V.P;
+  SlotState* st = V.st();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned kmask = 0;
+  for (int s = 0; s < G; ++s) if (st[s].need_kkt) kmask |= 1u << s;
+  if (!kmask) return;
+  kkt_stage<G, NI, NG, KG>(V, kmask, cur, kres, kflag);
+  if (warp < G && ((kmask >> warp) & 1u)) {
+    const int s = warp;
+    SlotState& S = st[s];
+    const int r = kres[s];
+    if (lane == 0) { S.need_kkt = 0; atomicAdd(kkts, 1ull); }
+    if (r == 2) {
+      if (lane == 0) { S.status = ST_KKT_SINGULAR; S.phase = PH_DONE; }
+    } else {
+      if (lane == 0) S.n_reg += r;
+      const double* sv = V.vec(s, 2);
+      const double* sl = V.vec(s, 3);
+      const double* x = V.vec(s, 0);
+      const double* lam = V.vec(s, 1);
+      double* xt = V.vec(s, 4);
+      double* lt = V.vec(s, 5);
+      for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], sv[j]);
+      for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], sl[c]);
+      if (lane == 0) { S.alpha = 1.0; S.n_trials = 0; S.phase = PH_TRIAL; }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// results of a slot that finished this round (warp s): SqpResult fields
+__device__ __forceinline__ void slot_write(const View& V, int s) {
+  const Params& P = V.P;
+  const int lane = threadIdx.x & 31;
+  SlotState& S = V.st()[s];
+  const int mu = S.mu;
+  const double* x = V.vec(s, 0);
+  const double* lam = V.vec(s, 1);
+  for (int j = lane; j < P.n_D; j += WARP) P.so.x[(size_t)mu * P.n_D + j] = x[j];
+  for (int c = lane; c < P.n_C; c += WARP) P.so.lam[(size_t)mu * P.n_C + c] = lam[c];
+  if (lane == 0) {
+    if (P.so.n_iter) P.so.n_iter[mu] = S.n_iter;
+    if (P.so.n_evals) P.so.n_evals[mu] = S.n_evals;
+    if (P.so.status) P.so.status[mu] = S.status;
+    if (P.so.n_reg) P.so.n_reg[mu] = S.n_reg;
+    if (P.so.merit) P.so.merit[mu] = S.merit;
+    if (P.so.objective) P.so.objective[mu] = S.obj;
+  }
+}
+
+__device__ __forceinline__ void slot_reset(SlotState& S, int mu) {
+  S.mu = mu; S.phase = PH_INIT; S.n_iter = 0; S.n_trials = 0;
+  S.n_evals = 0; S.n_reg = 0; S.status = ST_OK; S.need_kkt = 0;
+  S.alpha = 1.0;
+}
+
+// --------------------------------------------------------------------------
 // the persistent kernel
 
-template <int G, int NI, int NG>
+template <int G, int NI, int NG, bool KG>
 __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_constant__ Params P) {
   View V(P, ddnm_smem);
   SlotState* st = V.st();
-  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int W = NI + NG;
+  const int tid = threadIdx.x, T = blockDim.x, warp = tid >> 5;
   const int gslot0 = blockIdx.x * G;
   __shared__ int s_cur[G];
   __shared__ int s_ebi[G];
@@ -1700,7 +1899,6 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
   for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
   __syncthreads();
   if (tid == 0) s_prof[15] = clock64();
-  const SqpCfg& cfg = P.cfg;
   for (;;) {
     // ---- retire finished slots, fetch new mu ----
     if (tid == 0) {
@@ -1709,9 +1907,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
         if (st[s].phase == PH_DONE) {
           const int mu = atomicAdd(P.work, 1);
           if (mu < P.B) {
-            st[s].mu = mu; st[s].phase = PH_INIT; st[s].n_iter = 0; st[s].n_trials = 0;
-            st[s].n_evals = 0; st[s].n_reg = 0; st[s].status = ST_OK; st[s].need_kkt = 0;
-            st[s].alpha = 1.0;
+            slot_reset(st[s], mu);
             nm |= 1u << s;
           } else {
             st[s].mu = -1; st[s].phase = PH_IDLE;
@@ -1729,30 +1925,9 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
     if (mask == 0) break;
     // ---- initialise new slots: boundary values (CTA-wide), x0 / lam0 (warp per slot) ----
     if (newmask) {
-      for (int s = 0; s < G; ++s) {
-        if (!((newmask >> s) & 1u)) continue;
-        const int mu = st[s].mu;
-        const double a = P.mu[2 * mu], lm = P.mu[2 * mu + 1];
-        double* gb = P.gbv + (size_t)(gslot0 + s) * P.total_rows * 3;
-        for (int b = 0; b < P.nb; ++b) {
-          const BlockDev& B = P.blk[b];
-          for (int r = tid; r < B.nrows; r += T) row_bvals(P, B.rows, r, a, lm, gb + (B.row_off + r) * 3);
-        }
-      }
-      if (warp < G && ((newmask >> warp) & 1u)) {
-        const int s = warp, mu = st[s].mu;
-        double* xt = V.vec(s, 4);
-        double* lt = V.vec(s, 5);
-        if (P.x0_in) {
-          for (int j = lane; j < P.n_D; j += WARP) xt[j] = P.x0_in[(size_t)mu * P.n_D + j];
-        } else {
-          warp_rbf(P, P.mu[2 * mu], P.mu[2 * mu + 1], xt, V.scr(s));
-        }
-        for (int c = lane; c < P.n_C; c += WARP) lt[c] = P.lam0_in ? P.lam0_in[(size_t)mu * P.n_C + c] : 0.0;
-        if (lane == 0) st[s].lam_given = P.lam0_in != nullptr;
-        __syncwarp();
-        if (P.so.x0) for (int j = lane; j < P.n_D; j += WARP) P.so.x0[(size_t)mu * P.n_D + j] = xt[j];
-      }
+      for (int s = 0; s < G; ++s)
+        if ((newmask >> s) & 1u) slot_bvals(V, s, st[s].mu);
+      if (warp < G && ((newmask >> warp) & 1u)) slot_start(V, warp);
       __syncthreads();
       DDNM_MARK(V, 5);
     }
@@ -1763,142 +1938,14 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
     eval_blocks<G, NI, NG>(V, mask, s_ebi, gslot0, false);
     if (tid == 0) s_evals += (unsigned long long)__popc(mask) * P.nb;
     // ---- per-slot state machine (warp s) ----
-    if (warp < G && ((mask >> warp) & 1u)) {
-      const int s = warp;
-      SlotState& S = st[s];
-      const int mu = S.mu;
-      double* e = V.eb(s, s_ebi[s]);
-      double* lt = V.vec(s, 5);
-      double* x = V.vec(s, 0);
-      double* lam = V.vec(s, 1);
-      double* xt = V.vec(s, 4);
-      finalize_eval<NI, NG>(V, s, e, lt);
-      bool check = false;
-      if (S.phase == PH_INIT) {
-        if (!S.lam_given) {
-          // multiplier least squares at lam = 0, then rho at lam0
-          const bool ok = warp_lstsq<NI, NG>(P, e, V.scr(s), lt);
-          if (!ok) {
-            if (lane == 0) { S.status = ST_LSTSQ_RANK; }
-          }
-          __syncwarp();
-          finalize_eval<NI, NG>(V, s, e, lt);
-        }
-        if (P.so.lam0) for (int c = lane; c < P.n_C; c += WARP) P.so.lam0[(size_t)mu * P.n_C + c] = lt[c];
-        for (int j = lane; j < P.n_D; j += WARP) { x[j] = xt[j]; V.vec(s, 6)[j] = xt[j]; }
-        for (int c = lane; c < P.n_C; c += WARP) { lam[c] = lt[c]; V.vec(s, 7)[c] = lt[c]; }
-        if (lane == 0) {
-          S.merit = e[P.eb_scal]; S.obj = e[P.eb_scal + 1]; S.best_merit = S.merit;
-          S.n_evals = 1;
-          if (P.so.merit_hist) P.so.merit_hist[(size_t)mu * (cfg.max_iter + 1)] = S.merit;
-          if (P.so.obj_hist) P.so.obj_hist[(size_t)mu * (cfg.max_iter + 1)] = S.obj;
-        }
-        check = true;
-      } else {  // PH_TRIAL
-        const double tm = e[P.eb_scal];
-        const double rhs = (1.0 - cfg.c1 * S.alpha) * S.merit;
-        if (lane == 0) S.n_evals += 1;
-        if (tm <= rhs) {
-          for (int j = lane; j < P.n_D; j += WARP) x[j] = xt[j];
-          for (int c = lane; c < P.n_C; c += WARP) lam[c] = lt[c];
-          __syncwarp();
-          if (lane == 0) {
-            s_cur[s] = s_ebi[s];
-            if (P.so.alpha_hist) P.so.alpha_hist[(size_t)mu * cfg.max_iter + S.n_iter] = S.alpha;
-            S.n_iter += 1;
-            S.merit = tm; S.obj = e[P.eb_scal + 1];
-            if (P.so.merit_hist) P.so.merit_hist[(size_t)mu * (cfg.max_iter + 1) + S.n_iter] = S.merit;
-            if (P.so.obj_hist) P.so.obj_hist[(size_t)mu * (cfg.max_iter + 1) + S.n_iter] = S.obj;
-          }
-          const bool better = tm < S.best_merit;
-          __syncwarp();
-          if (better) {
-            for (int j = lane; j < P.n_D; j += WARP) V.vec(s, 6)[j] = x[j];
-            for (int c = lane; c < P.n_C; c += WARP) V.vec(s, 7)[c] = lam[c];
-            if (lane == 0) S.best_merit = tm;
-          }
-          check = true;
-        } else {
-          const int tr = S.n_trials + 1;
-          __syncwarp();
-          if (tr >= cfg.max_halvings + 1) {
-            // line-search failure: return the best iterate (sqp.py:275-293)
-            for (int j = lane; j < P.n_D; j += WARP) x[j] = V.vec(s, 6)[j];
-            for (int c = lane; c < P.n_C; c += WARP) lam[c] = V.vec(s, 7)[c];
-            if (lane == 0) { S.status = ST_LINE_SEARCH; S.phase = PH_DONE; S.n_trials = tr; }
-          } else {
-            const double al = S.alpha * cfg.factor;
-            const double* sv = V.vec(s, 2);
-            const double* sl = V.vec(s, 3);
-            for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], __dmul_rn(al, sv[j]));
-            for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], __dmul_rn(al, sl[c]));
-            if (lane == 0) { S.alpha = al; S.n_trials = tr; }
-          }
-        }
-      }
-      __syncwarp();
-      if (check) {
-        if (S.status == ST_LSTSQ_RANK) {
-          if (lane == 0) S.phase = PH_DONE;
-        } else if (!(S.merit >= cfg.tol && S.n_iter < cfg.max_iter)) {
-          if (lane == 0) S.phase = PH_DONE;
-        } else {
-          if (lane == 0) S.need_kkt = 1;
-        }
-      }
-      __syncwarp();
-    }
+    if (warp < G && ((mask >> warp) & 1u)) slot_decide<NI, NG>(V, warp, s_ebi[warp], s_cur);
     __syncthreads();
     DDNM_MARK(V, 6);
     // ---- KKT solves (block-structured LU across warps, dense fallback) ----
-    {
-      unsigned kmask = 0;
-      for (int s = 0; s < G; ++s) if (st[s].need_kkt) kmask |= 1u << s;
-      if (kmask) {
-        kkt_stage<G, NI, NG>(V, kmask, s_cur, s_kres, s_kflag);
-        if (warp < G && ((kmask >> warp) & 1u)) {
-          const int s = warp;
-          SlotState& S = st[s];
-          const int r = s_kres[s];
-          if (lane == 0) { S.need_kkt = 0; atomicAdd(&s_kkts, 1ull); }
-          if (r == 2) {
-            if (lane == 0) { S.status = ST_KKT_SINGULAR; S.phase = PH_DONE; }
-          } else {
-            if (lane == 0) S.n_reg += r;
-            const double* sv = V.vec(s, 2);
-            const double* sl = V.vec(s, 3);
-            const double* x = V.vec(s, 0);
-            const double* lam = V.vec(s, 1);
-            double* xt = V.vec(s, 4);
-            double* lt = V.vec(s, 5);
-            for (int j = lane; j < P.n_D; j += WARP) xt[j] = __dadd_rn(x[j], sv[j]);
-            for (int c = lane; c < P.n_C; c += WARP) lt[c] = __dadd_rn(lam[c], sl[c]);
-            if (lane == 0) { S.alpha = 1.0; S.n_trials = 0; S.phase = PH_TRIAL; }
-          }
-          __syncwarp();
-        }
-        __syncthreads();
-      }
-    }
+    kkt_advance<G, NI, NG, KG>(V, s_cur, s_kres, s_kflag, &s_kkts);
     DDNM_MARK(V, 7);
     // ---- write results of finished slots ----
-    if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) {
-      const int s = warp;
-      SlotState& S = st[s];
-      const int mu = S.mu;
-      const double* x = V.vec(s, 0);
-      const double* lam = V.vec(s, 1);
-      for (int j = lane; j < P.n_D; j += WARP) P.so.x[(size_t)mu * P.n_D + j] = x[j];
-      for (int c = lane; c < P.n_C; c += WARP) P.so.lam[(size_t)mu * P.n_C + c] = lam[c];
-      if (lane == 0) {
-        if (P.so.n_iter) P.so.n_iter[mu] = S.n_iter;
-        if (P.so.n_evals) P.so.n_evals[mu] = S.n_evals;
-        if (P.so.status) P.so.status[mu] = S.status;
-        if (P.so.n_reg) P.so.n_reg[mu] = S.n_reg;
-        if (P.so.merit) P.so.merit[mu] = S.merit;
-        if (P.so.objective) P.so.objective[mu] = S.obj;
-      }
-    }
+    if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) slot_write(V, warp);
     __syncthreads();
   }
   if (tid == 0) {
@@ -1907,6 +1954,157 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
     if (P.prof)
       for (int i = 0; i < 15; ++i) atomicAdd(P.prof + i, s_prof[i]);
   }
+}
+
+// --------------------------------------------------------------------------
+// round-synchronous kernels for subdomain sharding.
+//
+// Every rank owns a contiguous block range [b_lo, b_hi) and holds the whole
+// per-mu SQP state in global memory (dd_st, dd_vec, dd_ecur).  One SQP round
+// of the batch is
+//   k_dd_eval   this rank's blocks at every active slot's trial point ->
+//               packets [B][pk_stride] = the block pieces of the eval buffer
+//               (Gram H_b, R_b^T r_b, cval_b, cjac_b, r_b^T r_b)
+//   all-gather  of the packets over the ranks (NCCL)
+//   k_dd_step   every rank, identically: assemble all blocks' pieces in block
+//               order, then the same decision / KKT / trial update as k_solve
+// so all ranks hold bit-identical states and results.  CTA c owns mu
+// c*G .. c*G+G-1 for the whole solve (no work counter: rounds are global).
+
+template <int G>
+__device__ __forceinline__ unsigned dd_load_state(const View& V, int* mu_of) {
+  const Params& P = V.P;
+  SlotState* st = V.st();
+  __shared__ unsigned s_m;
+  if (threadIdx.x < G) {
+    const int s = threadIdx.x, mu = blockIdx.x * G + s;
+    if (mu < P.B) st[s] = P.dd_st[mu];
+    else { st[s].mu = -1; st[s].phase = PH_IDLE; }
+    mu_of[s] = mu;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned m = 0;
+    for (int s = 0; s < G; ++s) if (st[s].phase == PH_INIT || st[s].phase == PH_TRIAL) m |= 1u << s;
+    s_m = m;
+  }
+  __syncthreads();
+  return s_m;
+}
+
+template <int G, int NI, int NG>
+__global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_eval(const __grid_constant__ Params P) {
+  View V(P, ddnm_smem);
+  const int tid = threadIdx.x, T = blockDim.x;
+  __shared__ int s_mu[G];
+  __shared__ int s_ebi[G];
+  const unsigned mask = dd_load_state<G>(V, s_mu);
+  if (mask == 0) return;
+  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+  if (tid < G) s_ebi[tid] = 0;
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    const double* src = P.dd_vec + ((size_t)s_mu[s] * 8 + 4) * P.nK;
+    for (int j = tid; j < P.n_D; j += T) V.vec(s, 4)[j] = src[j];
+  }
+  __syncthreads();
+  eval_blocks<G, NI, NG>(V, mask, s_ebi, blockIdx.x * G, false);
+  const int off = P.blk[P.b_lo].eb_off;
+  const int len = (P.b_hi < P.nb ? P.blk[P.b_hi].eb_off : P.eb_rho) - off;
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    double* dst = P.dd_pk + (size_t)s_mu[s] * P.pk_stride;
+    const double* e = V.eb(s, 0) + off;
+    for (int i = tid; i < len; i += T) dst[i] = e[i];
+  }
+  if (tid == 0) atomicAdd(P.counters, (unsigned long long)__popc(mask) * (P.b_hi - P.b_lo));
+}
+
+template <int G, int NI, int NG, bool KG>
+__global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_constant__ Params P) {
+  View V(P, ddnm_smem);
+  SlotState* st = V.st();
+  const int tid = threadIdx.x, T = blockDim.x, warp = tid >> 5;
+  __shared__ int s_mu[G];
+  __shared__ int s_cur[G];
+  __shared__ int s_ebi[G];
+  __shared__ int s_kres[G], s_kflag[G];
+  __shared__ unsigned long long s_kkts;
+  if (P.dd_init) {
+    // new batch: every slot takes its mu, boundary values, x0 / lam0
+    if (tid < G) {
+      const int mu = blockIdx.x * G + tid;
+      s_mu[tid] = mu;
+      if (mu < P.B) slot_reset(st[tid], mu);
+      else { st[tid].mu = -1; st[tid].phase = PH_IDLE; }
+    }
+    for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+    __syncthreads();
+    for (int s = 0; s < G; ++s)
+      if (st[s].mu >= 0) slot_bvals(V, s, st[s].mu);
+    if (warp < G && st[warp].mu >= 0) slot_start(V, warp);
+    __syncthreads();
+    for (int s = 0; s < G; ++s) {
+      if (st[s].mu < 0) continue;
+      double* dst = P.dd_vec + (size_t)s_mu[s] * 8 * P.nK;
+      for (int i = tid; i < 8 * P.nK; i += T) dst[i] = V.vec(s, 0)[i];
+    }
+    if (tid < G && st[tid].mu >= 0) {
+      P.dd_st[s_mu[tid]] = st[tid];
+      atomicAdd(P.dd_active, 1);
+    }
+    return;
+  }
+  const unsigned mask = dd_load_state<G>(V, s_mu);
+  if (mask == 0) return;
+  if (tid == 0) s_kkts = 0;
+  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+  // state, current eval buffer (slot 0) and the gathered trial evaluation
+  // (slot 1; slot 0 for the first evaluation of a new mu)
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    const int mu = s_mu[s];
+    const double* src = P.dd_vec + (size_t)mu * 8 * P.nK;
+    for (int i = tid; i < 8 * P.nK; i += T) V.vec(s, 0)[i] = src[i];
+    const int ebi = st[s].phase == PH_INIT ? 0 : 1;
+    if (ebi == 1) {
+      const double* ec = P.dd_ecur + (size_t)mu * P.eb_size;
+      for (int i = tid; i < P.eb_size; i += T) V.eb(s, 0)[i] = ec[i];
+    }
+    double* e = V.eb(s, ebi);
+    for (int r = 0; r < P.dd_nranks; ++r) {
+      const int b0 = P.dd_bnd[r], b1 = P.dd_bnd[r + 1];
+      const int off = P.blk[b0].eb_off;
+      const int len = (b1 < P.nb ? P.blk[b1].eb_off : P.eb_rho) - off;
+      const double* g = P.dd_gath + ((size_t)r * P.B + mu) * P.pk_stride;
+      for (int i = tid; i < len; i += T) e[off + i] = g[i];
+    }
+    if (tid == 0) { s_cur[s] = 0; s_ebi[s] = ebi; }
+  }
+  __syncthreads();
+  if (warp < G && ((mask >> warp) & 1u)) slot_decide<NI, NG>(V, warp, s_ebi[warp], s_cur);
+  __syncthreads();
+  kkt_advance<G, NI, NG, KG>(V, s_cur, s_kres, s_kflag, &s_kkts);
+  if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) slot_write(V, warp);
+  __syncthreads();
+  for (int s = 0; s < G; ++s) {
+    if (!((mask >> s) & 1u)) continue;
+    const int mu = s_mu[s];
+    double* dst = P.dd_vec + (size_t)mu * 8 * P.nK;
+    for (int i = tid; i < 8 * P.nK; i += T) dst[i] = V.vec(s, 0)[i];
+    if (st[s].phase != PH_DONE) {
+      // the accepted (or first) evaluation is the next round's current one
+      double* ec = P.dd_ecur + (size_t)mu * P.eb_size;
+      const double* e = V.eb(s, s_cur[s]);
+      if (s_cur[s] != 0 || s_ebi[s] == 0)
+        for (int i = tid; i < P.eb_size; i += T) ec[i] = e[i];
+    }
+  }
+  if (tid < G && ((mask >> tid) & 1u)) {
+    P.dd_st[s_mu[tid]] = st[tid];
+    if (st[tid].phase != PH_DONE) atomicAdd(P.dd_active, 1);
+  }
+  if (tid == 0) atomicAdd(P.counters + 1, s_kkts);
 }
 
 }  // namespace ddnm
@@ -1919,7 +2117,7 @@ namespace ddnm {
 
 // ddnm_eval_batch: one eval_gradients per mu at a given (x, lam), dumping every
 // intermediate, plus (optionally) the KKT step at that point.  mu = CTA*G + s.
-template <int G, int NI, int NG>
+template <int G, int NI, int NG, bool KG>
 __global__ void __launch_bounds__(DDNM_MAX_THREADS) k_eval(const __grid_constant__ Params P) {
   View V(P, ddnm_smem);
   SlotState* st = V.st();
@@ -1971,7 +2169,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS) k_eval(const __grid_constant
   if (P.eval_step) {
     __shared__ int s_kres[G], s_kflag[G];
     __syncthreads();
-    kkt_stage<G, NI, NG>(V, mask, s_ebi, s_kres, s_kflag);
+    kkt_stage<G, NI, NG, KG>(V, mask, s_ebi, s_kres, s_kflag);
     if (warp < G && ((mask >> warp) & 1u)) {
       const int s = warp;
       const size_t mu = (size_t)st[s].mu;

@@ -6,7 +6,9 @@
 
 namespace ddnm {
 void register_20_19(std::vector<KernelEntry>& t) {
-  t.push_back(KernelEntry{20, 19, 1, (const void*)&k_solve<1, 20, 19>,
-                          (const void*)&k_eval<1, 20, 19>});
+  t.push_back(KernelEntry{20, 19, 1, false, (const void*)&k_solve<1, 20, 19, false>,
+                          (const void*)&k_eval<1, 20, 19, false>,
+                          (const void*)&k_dd_eval<1, 20, 19>,
+                          (const void*)&k_dd_step<1, 20, 19, false>});
 }
 }  // namespace ddnm

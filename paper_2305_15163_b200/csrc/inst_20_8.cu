@@ -6,7 +6,9 @@
 
 namespace ddnm {
 void register_20_8(std::vector<KernelEntry>& t) {
-  t.push_back(KernelEntry{20, 8, 1, (const void*)&k_solve<1, 20, 8>,
-                          (const void*)&k_eval<1, 20, 8>});
+  t.push_back(KernelEntry{20, 8, 1, false, (const void*)&k_solve<1, 20, 8, false>,
+                          (const void*)&k_eval<1, 20, 8, false>,
+                          (const void*)&k_dd_eval<1, 20, 8>,
+                          (const void*)&k_dd_step<1, 20, 8, false>});
 }
 }  // namespace ddnm

@@ -6,9 +6,13 @@
 
 namespace ddnm {
 void register_4_3(std::vector<KernelEntry>& t) {
-  t.push_back(KernelEntry{4, 3, 1, (const void*)&k_solve<1, 4, 3>,
-                          (const void*)&k_eval<1, 4, 3>});
-  t.push_back(KernelEntry{4, 3, 2, (const void*)&k_solve<2, 4, 3>,
-                          (const void*)&k_eval<2, 4, 3>});
+  t.push_back(KernelEntry{4, 3, 1, false, (const void*)&k_solve<1, 4, 3, false>,
+                          (const void*)&k_eval<1, 4, 3, false>,
+                          (const void*)&k_dd_eval<1, 4, 3>,
+                          (const void*)&k_dd_step<1, 4, 3, false>});
+  t.push_back(KernelEntry{4, 3, 2, false, (const void*)&k_solve<2, 4, 3, false>,
+                          (const void*)&k_eval<2, 4, 3, false>,
+                          (const void*)&k_dd_eval<2, 4, 3>,
+                          (const void*)&k_dd_step<2, 4, 3, false>});
 }
 }  // namespace ddnm

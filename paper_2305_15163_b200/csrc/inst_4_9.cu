@@ -6,9 +6,13 @@
 
 namespace ddnm {
 void register_4_9(std::vector<KernelEntry>& t) {
-  t.push_back(KernelEntry{4, 9, 1, (const void*)&k_solve<1, 4, 9>,
-                          (const void*)&k_eval<1, 4, 9>});
-  t.push_back(KernelEntry{4, 9, 2, (const void*)&k_solve<2, 4, 9>,
-                          (const void*)&k_eval<2, 4, 9>});
+  t.push_back(KernelEntry{4, 9, 1, false, (const void*)&k_solve<1, 4, 9, false>,
+                          (const void*)&k_eval<1, 4, 9, false>,
+                          (const void*)&k_dd_eval<1, 4, 9>,
+                          (const void*)&k_dd_step<1, 4, 9, false>});
+  t.push_back(KernelEntry{4, 9, 2, false, (const void*)&k_solve<2, 4, 9, false>,
+                          (const void*)&k_eval<2, 4, 9, false>,
+                          (const void*)&k_dd_eval<2, 4, 9>,
+                          (const void*)&k_dd_step<2, 4, 9, false>});
 }
 }  // namespace ddnm

@@ -6,7 +6,9 @@
 
 namespace ddnm {
 void register_8_11(std::vector<KernelEntry>& t) {
-  t.push_back(KernelEntry{8, 11, 1, (const void*)&k_solve<1, 8, 11>,
-                          (const void*)&k_eval<1, 8, 11>});
+  t.push_back(KernelEntry{8, 11, 1, false, (const void*)&k_solve<1, 8, 11, false>,
+                          (const void*)&k_eval<1, 8, 11, false>,
+                          (const void*)&k_dd_eval<1, 8, 11>,
+                          (const void*)&k_dd_step<1, 8, 11, false>});
 }
 }  // namespace ddnm

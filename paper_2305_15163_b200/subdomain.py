@@ -1,0 +1,206 @@
+"""Subdomain sharding of the batched online solve.
+
+In the reference every subdomain is one ``SqpBlock`` (sqp.py:28-41) whose
+closures -- the HR residual chain of driver.py:404-432 and the constraint of
+driver.py:366-378 -- are independent of the other blocks; ``eval_gradients``
+(sqp.py:117-146) only sums their pieces and ``_kkt_matrix`` (sqp.py:149-159)
+only places them.  So with many subdomains the blocks are split across ranks
+(one process per GPU) and every SQP round of the whole mu batch is
+
+1. ``eval``: this rank evaluates its contiguous block range at every running
+   mu's trial point and packs, per mu, the block pieces the SQP needs (Gram
+   block H_b = R_bᵀR_b, R_bᵀr_b, cval_b, cjac_b, r_bᵀr_b);
+2. an all-gather of those packets (NCCL between GPUs, gloo in the CPU tests);
+3. ``step``: every rank assembles all blocks' pieces in block order and runs
+   the same Armijo decision / KKT solve / trial update (sqp.py:230-299), so
+   all ranks hold bit-identical iterates and results.
+
+Rounds are batch-synchronous: a mu that finished idles until the batch does.
+The round engine is pluggable: :class:`DeviceRoundEngine` drives the
+``ddnm_dd_*`` entry points of libddnm.so (include/ddnm.h); the CPU tests plug
+an oracle-backed engine into the same host loop.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _native as N
+from .sqp import SqpConfig
+
+
+def block_bounds(n_blocks: int, world: int) -> list:
+    """Contiguous block ranges per rank: rank r owns [b[r], b[r+1]); sizes
+    differ by at most one, lower ranks take the remainder."""
+    if world < 1 or n_blocks < world:
+        raise ValueError(f"cannot shard {n_blocks} blocks over {world} ranks")
+    q, r = divmod(n_blocks, world)
+    b = [0]
+    for k in range(world):
+        b.append(b[-1] + q + (1 if k < r else 0))
+    return b
+
+
+class DeviceRoundEngine:
+    """Round engine on the GPU: k_dd_eval / k_dd_step through the C ABI.
+    Packets live in torch CUDA tensors so torch.distributed (NCCL) can
+    all-gather them on the current stream."""
+
+    def __init__(self, instance, device: int = -1):
+        import torch
+        self.torch = torch
+        self.inst = instance
+        self.ctx = instance.context(device)
+        self.dev = torch.device("cuda", self.ctx.info.device)
+        self.h = None
+        self.n_blocks = instance.n_blocks
+
+    def packet_len(self, lo: int, hi: int) -> int:
+        n = C.c_int64()
+        N.check(N.lib().ddnm_dd_packet_len(self.ctx.h, lo, hi, C.byref(n)))
+        return int(n.value)
+
+    def buffer(self, n: int):
+        return self.torch.zeros(n, dtype=self.torch.float64, device=self.dev)
+
+    def _stream(self):
+        return C.c_void_p(self.torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def begin(self, mu, cfg: SqpConfig, x0, lam0, lo: int, hi: int) -> int:
+        from .driver import _cfg_struct
+        t = self.torch
+        B = mu.shape[0]
+        nD, nC, K = self.inst.n_primal, self.inst.n_mult, cfg.max_iter
+        f64 = dict(dtype=t.float64, device=self.dev)
+        i32 = dict(dtype=t.int32, device=self.dev)
+        self.mu = t.as_tensor(mu, **f64).contiguous()
+        self.x0 = None if x0 is None else t.as_tensor(np.asarray(x0, float).reshape(B, nD), **f64)
+        self.lam0 = None if lam0 is None else t.as_tensor(np.asarray(lam0, float).reshape(B, nC), **f64)
+        self.out = dict(
+            x=t.empty(B, nD, **f64), lam=t.empty(B, nC, **f64), n_iter=t.zeros(B, **i32),
+            n_evals=t.zeros(B, **i32), status=t.zeros(B, **i32), n_reg=t.zeros(B, **i32),
+            merit=t.empty(B, **f64), objective=t.empty(B, **f64),
+            merit_hist=t.empty(B, K + 1, **f64), obj_hist=t.empty(B, K + 1, **f64),
+            alpha_hist=t.empty(B, K, **f64), x0=t.empty(B, nD, **f64), lam0=t.empty(B, nC, **f64))
+        so = N.SolveOut()
+        for k, v in self.out.items():
+            ct = C.c_int32 if v.dtype == t.int32 else C.c_double
+            setattr(so, k, C.cast(C.c_void_p(v.data_ptr()), C.POINTER(ct)))
+        self.cfg = cfg
+        h = C.c_void_p()
+        n = C.c_int32()
+        N.check(N.lib().ddnm_dd_begin(
+            self.ctx.h, B, C.c_void_p(self.mu.data_ptr()),
+            None if self.x0 is None else C.c_void_p(self.x0.data_ptr()),
+            None if self.lam0 is None else C.c_void_p(self.lam0.data_ptr()),
+            C.byref(_cfg_struct(cfg)), lo, hi, C.byref(so), self._stream(), C.byref(h),
+            C.byref(n)))
+        self.h = h
+        return int(n.value)
+
+    def eval(self, packets, stride: int) -> None:
+        N.check(N.lib().ddnm_dd_eval(self.h, C.c_void_p(packets.data_ptr()), stride,
+                                     self._stream()))
+
+    def step(self, gathered, nranks: int, bounds, stride: int) -> int:
+        bnd = (C.c_int32 * len(bounds))(*bounds)
+        n = C.c_int32()
+        N.check(N.lib().ddnm_dd_step(self.h, C.c_void_p(gathered.data_ptr()), nranks, bnd,
+                                     stride, self._stream(), C.byref(n)))
+        return int(n.value)
+
+    def finish(self, mu):
+        from .driver import BatchResult
+        self.torch.cuda.current_stream(self.dev).synchronize()
+        out = {k: v.cpu().numpy() for k, v in self.out.items()}
+        N.lib().ddnm_dd_end(self.h)
+        self.h = None
+        return BatchResult(mu=mu, tol=self.cfg.tol, counters=self.ctx.counters(), **out)
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            try:
+                N.lib().ddnm_dd_end(h)
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
+
+
+class ShardedSolve:
+    """One rank's share of a subdomain-sharded batched solve.
+
+    ``eval()`` returns this rank's packets ([B * stride] doubles); the caller
+    all-gathers them rank-major into [world * B * stride] and passes that to
+    ``step()``, which returns the number of mu still running."""
+
+    def __init__(self, instance, mu, cfg: SqpConfig, rank: int, world: int, *, x0=None,
+                 lam0=None, engine=None, device: int = -1):
+        self.eng = engine or DeviceRoundEngine(instance, device)
+        nb = self.eng.n_blocks
+        self.bounds = block_bounds(nb, world)
+        self.rank, self.world = rank, world
+        self.mu = mu
+        self.B = mu.shape[0]
+        self.stride = max(self.eng.packet_len(self.bounds[r], self.bounds[r + 1])
+                          for r in range(world))
+        self.lo, self.hi = self.bounds[rank], self.bounds[rank + 1]
+        self.active = self.eng.begin(mu, cfg, x0, lam0, self.lo, self.hi)
+        self.packets = self.eng.buffer(self.B * self.stride)
+        self.rounds = 0
+        # every round evaluates one trial point per running mu; a solve takes
+        # at most max_iter KKT steps of at most max_halvings + 1 trials each
+        self.max_rounds = 2 + cfg.max_iter * (cfg.max_halvings + 1)
+
+    def eval(self):
+        self.eng.eval(self.packets, self.stride)
+        return self.packets
+
+    def step(self, gathered) -> int:
+        self.active = self.eng.step(gathered, self.world, self.bounds, self.stride)
+        self.rounds += 1
+        if self.active and self.rounds >= self.max_rounds:
+            raise RuntimeError("sharded solve did not terminate within the SQP round bound")
+        return self.active
+
+    def result(self):
+        return self.eng.finish(self.mu)
+
+
+def _all_gather(gathered, packets, world, group):
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, packets, group=group)
+    else:
+        dist.all_gather(list(gathered.view(world, -1).unbind(0)), packets, group=group)
+
+
+def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(), *,
+                                      x0=None, lam0=None, group=None, device: int = -1,
+                                      engine=None):
+    """Batched ``solve_rom`` (driver.py:554-597, compute_error=False) with the
+    subdomain blocks sharded over the ranks of ``group`` (every rank passes
+    the same ``mus``); every rank returns the same full ``BatchResult``."""
+    import torch.distributed as dist
+
+    from .driver import _mu_array
+    mu = _mu_array(mus)
+    dist_on = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if dist_on else 0
+    world = dist.get_world_size(group) if dist_on else 1
+    t0 = time.perf_counter()
+    sh = ShardedSolve(instance, mu, cfg, rank, world, x0=x0, lam0=lam0, engine=engine,
+                      device=device)
+    gathered = sh.packets if world == 1 else sh.eng.buffer(world * sh.B * sh.stride)
+    active = sh.active
+    while active:
+        packets = sh.eval()
+        if world > 1:
+            _all_gather(gathered, packets, world, group)
+        active = sh.step(gathered)
+    res = sh.result()
+    if hasattr(res, "seconds"):
+        res.seconds = time.perf_counter() - t0
+    return res

@@ -1,0 +1,308 @@
+"""Subdomain sharding: blocks split over ranks, per-round
+all-gather of block pieces, identical SQP on every rank.
+
+CPU tests run the shipping host loop (paper_2305_15163_b200/subdomain.py)
+over gloo with world size 2 and 4, plugging in an oracle-backed round engine
+(test infrastructure: packets hold the oracle's block pieces, the step drives
+a generator restatement of oracle.solve).  GPU tests run the device engine
+(k_dd_eval / k_dd_step) and compare it with the persistent megakernel, the
+oracle and the reference goldens."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import ddnm_oracle as O
+
+from .conftest import golden_path
+
+DD = "dd16_nm"      # 60x60, 4x4 subdomains, n = (8, 5), n_C = 40 (config 4's layout)
+
+
+def test_block_bounds():
+    from paper_2305_15163_b200 import block_bounds
+    assert block_bounds(16, 1) == [0, 16]
+    assert block_bounds(16, 8) == list(range(0, 17, 2))
+    assert block_bounds(4, 3) == [0, 2, 3, 4]
+    for nb in (1, 4, 16):
+        for w in range(1, nb + 1):
+            b = block_bounds(nb, w)
+            assert b[0] == 0 and b[-1] == nb and len(b) == w + 1
+            sz = np.diff(b)
+            assert sz.min() >= 1 and sz.max() - sz.min() <= 1
+    with pytest.raises(ValueError):
+        block_bounds(4, 5)
+    with pytest.raises(ValueError):
+        block_bounds(4, 0)
+
+
+# -- oracle-backed round engine (CPU stand-in for DeviceRoundEngine) ----------
+
+def _assemble(inst, pieces, lam):
+    """oracle.eval_gradients (sqp.py:117-146) from per-block pieces."""
+    rho = np.zeros(inst.n_primal)
+    con = np.zeros(inst.n_c)
+    evals = []
+    for blk, off, (Br, R_int, R_gam, cval, cjac) in zip(inst.blocks, inst.offsets, pieces):
+        rho[off:off + blk.n_int] = R_int.T @ Br
+        rho[off + blk.n_int:off + blk.n_int + blk.n_gam] = R_gam.T @ Br + cjac.T @ lam
+        con += cval
+        evals.append((Br, R_int, R_gam, cval, cjac))
+    return O.Eval(rho=rho, con=con, blocks=evals)
+
+
+def _solve_gen(inst, a, lm, cfg):
+    """oracle.solve (driver.py:554-597 + sqp.py:230-299) as a generator: it
+    yields every point it needs evaluated and receives that point's block
+    pieces (which do not depend on the multipliers)."""
+    x0 = O.rbf_query(inst, a, lm)
+    pieces = yield x0
+    ev0 = _assemble(inst, pieces, np.zeros(inst.n_c))
+    rows, rhs = [], []
+    for off, blk, be in zip(inst.offsets, inst.blocks, ev0.blocks):
+        gs = off + blk.n_int
+        rows.append(be[4].T)
+        rhs.append(-ev0.rho[gs:gs + blk.n_gam])
+    lam0, *_ = np.linalg.lstsq(np.vstack(rows), np.concatenate(rhs), rcond=None)
+    x = np.array(x0, dtype=float)
+    lam = np.array(lam0, dtype=float)
+    ev = _assemble(inst, pieces, lam)
+    merits, alphas = [ev.merit], []
+    best = (ev.merit, x.copy(), lam.copy())
+    failure, n_iter, n_evals = None, 0, 1
+    while merits[-1] >= cfg.tol and n_iter < cfg.max_iter:
+        try:
+            s, s_lam, _ = O.solve_kkt(inst, ev, cfg.reg_scale)
+        except O.OracleConvergenceError:
+            return x, lam, n_iter, n_evals, 2, merits
+        alpha = 1.0
+        accepted = None
+        for _ in range(cfg.max_halvings + 1):
+            pieces = yield x + alpha * s
+            trial = _assemble(inst, pieces, lam + alpha * s_lam)
+            n_evals += 1
+            if trial.merit <= (1.0 - cfg.armijo_c1 * alpha) * merits[-1]:
+                accepted = trial
+                break
+            alpha *= cfg.backtrack_factor
+        if accepted is None:
+            failure = "line_search"
+            break
+        x += alpha * s
+        lam += alpha * s_lam
+        ev = accepted
+        n_iter += 1
+        merits.append(ev.merit)
+        alphas.append(alpha)
+        if ev.merit < best[0]:
+            best = (ev.merit, x.copy(), lam.copy())
+    if failure is not None:
+        _, x, lam = best
+    return x, lam, n_iter, n_evals, 0 if failure is None else 1, merits
+
+
+class OracleRoundEngine:
+    def __init__(self, inst):
+        self.inst = inst
+        self.n_blocks = len(inst.blocks)
+        self.nout = [b.weights.shape[0] if b.weights is not None else b.stencil.rows.size
+                     for b in inst.blocks]
+        self.plen = [r * (1 + b.n_int + b.n_gam) + inst.n_c * (1 + b.n_gam)
+                     for r, b in zip(self.nout, inst.blocks)]
+        self.evals = 0
+
+    def packet_len(self, lo, hi):
+        return sum(self.plen[lo:hi])
+
+    def buffer(self, n):
+        import torch
+        return torch.zeros(n, dtype=torch.float64)
+
+    def begin(self, mu, cfg, x0, lam0, lo, hi):
+        assert x0 is None and lam0 is None
+        self.lo, self.hi = lo, hi
+        self.B = mu.shape[0]
+        self.bbs = [self.inst.boundary(a, lm) for a, lm in mu]
+        self.gens = [_solve_gen(self.inst, a, lm, cfg) for a, lm in mu]
+        self.xt = [next(g) for g in self.gens]
+        self.res = [None] * self.B
+        return self.B
+
+    def _split(self, x):
+        return self.inst.split(x)
+
+    def eval(self, packets, stride):
+        pk = packets.numpy()
+        for k in range(self.B):
+            if self.res[k] is not None:
+                continue
+            parts = self._split(self.xt[k])
+            pos = k * stride
+            for b in range(self.lo, self.hi):
+                blk = self.inst.blocks[b]
+                Br, R_int, R_gam = blk.residual(*parts[b], self.bbs[k][b])
+                cval, cjac = blk.constraint(parts[b][1])
+                flat = np.concatenate([Br, R_int.ravel(), R_gam.ravel(), cval,
+                                       np.atleast_2d(cjac).ravel()])
+                assert flat.size == self.plen[b]
+                pk[pos:pos + flat.size] = flat
+                pos += flat.size
+                self.evals += 1
+
+    def _unpack(self, flat, b):
+        blk, nc = self.inst.blocks[b], self.inst.n_c
+        r, ni, ng = self.nout[b], blk.n_int, blk.n_gam
+        sizes = [r, r * ni, r * ng, nc, nc * ng]
+        Br, Ri, Rg, cv, cj = np.split(flat[:self.plen[b]], np.cumsum(sizes)[:-1])
+        return Br, Ri.reshape(r, ni), Rg.reshape(r, ng), cv, cj.reshape(nc, ng)
+
+    def step(self, gathered, nranks, bounds, stride):
+        g = gathered.numpy().reshape(nranks, self.B, stride)
+        active = 0
+        for k in range(self.B):
+            if self.res[k] is not None:
+                continue
+            pieces = []
+            for r in range(nranks):
+                pos = 0
+                for b in range(bounds[r], bounds[r + 1]):
+                    pieces.append(self._unpack(g[r, k, pos:], b))
+                    pos += self.plen[b]
+            try:
+                self.xt[k] = self.gens[k].send(pieces)
+                active += 1
+            except StopIteration as stop:
+                self.res[k] = stop.value
+        return active
+
+    def finish(self, mu):
+        return self.res
+
+
+def _worker(rank, world, port, out_dir, name, B):
+    import torch.distributed as dist
+
+    from paper_2305_15163_b200 import SqpConfig, seeded_parameters
+    from paper_2305_15163_b200.subdomain import solve_rom_batch_subdomain_sharded
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    inst = O.Instance(golden_path(name, "artifacts"))
+    eng = OracleRoundEngine(inst)
+    res = solve_rom_batch_subdomain_sharded(inst, seeded_parameters(B, seed=5), SqpConfig(),
+                                            engine=eng)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"),
+             x=np.stack([r[0] for r in res]), lam=np.stack([r[1] for r in res]),
+             n_iter=np.array([r[2] for r in res]), n_evals=np.array([r[3] for r in res]),
+             status=np.array([r[4] for r in res]), block_evals=eng.evals)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("name,world,B", [("tiny_nm", 2, 4), (DD, 2, 2), (DD, 4, 2)])
+def test_sharded_rounds_match_unsharded_oracle(tmp_path, name, world, B):
+    """world ranks over gloo, each evaluating only its blocks: every rank ends
+    with the same results, bitwise equal to the unsharded oracle solve, and
+    the block evaluations split across the ranks."""
+    import torch.multiprocessing as mp
+
+    from paper_2305_15163_b200 import SqpConfig, block_bounds, seeded_parameters
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), name, B), nprocs=world,
+             join=True)
+    rs = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    for r in rs[1:]:
+        for k in ("x", "lam", "n_iter", "n_evals", "status"):
+            np.testing.assert_array_equal(r[k], rs[0][k])
+    inst = O.Instance(golden_path(name, "artifacts"))
+    mu = seeded_parameters(B, seed=5)
+    total_evals = 0
+    for k in range(B):
+        ref = O.solve(inst, mu[k, 0], mu[k, 1], O.SqpConfig())
+        np.testing.assert_array_equal(rs[0]["x"][k], ref.x)
+        np.testing.assert_array_equal(rs[0]["lam"][k], ref.lam)
+        assert rs[0]["n_iter"][k] == ref.n_iter
+        assert rs[0]["n_evals"][k] == ref.n_evals
+        total_evals += ref.n_evals
+    bnd = block_bounds(len(inst.blocks), world)
+    for r in range(world):
+        assert rs[r]["block_evals"] == total_evals * (bnd[r + 1] - bnd[r])
+
+
+# -- device engine -----------------------------------------------------------
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c0_nm", DD])
+def test_device_sharded_world1_equals_megakernel(name, gpu_instances):
+    """One rank owning every block: the round kernels reproduce the
+    persistent kernel bit for bit (same per-slot arithmetic)."""
+    import paper_2305_15163_b200 as P
+    inst = gpu_instances[name] if name in gpu_instances else P.RomInstance.load(
+        golden_path(name, "artifacts"))
+    mu = P.seeded_parameters(64, seed=3)
+    ref = P.solve_rom_batch(inst, mu)
+    res = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    for k in ("x", "lam", "n_iter", "n_evals", "status", "n_reg", "merit", "objective",
+              "x0", "lam0"):
+        np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=k)
+    np.testing.assert_array_equal(np.nan_to_num(res.merit_hist, nan=-1),
+                                  np.nan_to_num(ref.merit_hist, nan=-1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 16])
+def test_device_sharded_ranks_in_one_process(world):
+    """world rank states on one GPU, run one after the other in one process
+    (no rank waits on another): each evaluates only its block range, the
+    packets are concatenated rank-major (what the all-gather produces), and
+    every rank's result equals the one-rank solve bitwise."""
+    import torch
+
+    import paper_2305_15163_b200 as P
+    from paper_2305_15163_b200.subdomain import ShardedSolve
+    inst = P.RomInstance.load(golden_path(DD, "artifacts"))
+    mu = P.seeded_parameters(24, seed=4)
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    cfg = P.SqpConfig()
+    ranks = [ShardedSolve(inst, mu, cfg, r, world) for r in range(world)]
+    gathered = torch.empty(world * ranks[0].B * ranks[0].stride, dtype=torch.float64,
+                           device="cuda")
+    active = ranks[0].active
+    while active:
+        parts = [sh.eval().clone() for sh in ranks]
+        torch.cat(parts, out=gathered)
+        counts = [sh.step(gathered) for sh in ranks]
+        assert len(set(counts)) == 1
+        active = counts[0]
+    for sh in ranks:
+        r = sh.result()
+        for k in ("x", "lam", "n_iter", "n_evals", "status", "merit"):
+            np.testing.assert_array_equal(getattr(r, k), getattr(one, k), err_msg=k)
+
+
+@pytest.mark.gpu
+def test_device_sharded_matches_reference_goldens():
+    """dd16 (16 subdomains, n_C = 40) against the reference's own solves."""
+    import paper_2305_15163_b200 as P
+    g = dict(np.load(golden_path(DD, "golden")))
+    inst = P.RomInstance.load(golden_path(DD, "artifacts"))
+    res = P.solve_rom_batch_subdomain_sharded(inst, g["mu"])
+    for k in range(g["mu"].shape[0]):
+        assert _rel(res.x[k], g["x"][k]) < 1e-9, k
+        assert _rel(res.lam[k], g["lam"][k]) < 1e-9, k
+        assert res.status[k] == g["failure"][k], k
+    oi = O.Instance(golden_path(DD, "artifacts"))
+    for k in range(g["mu"].shape[0]):
+        r = O.solve(oi, *g["mu"][k])
+        if min(r.margins) > 1e-13 * r.merit_history[0]:
+            assert res.n_iter[k] == r.n_iter == g["n_iter"][k], k

@@ -115,7 +115,7 @@ def build(nx: int, ny: int, sx: int, sy: int, grid_n: int, snap_tol: float,
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c0", choices=["c0", "tiny"])
+    ap.add_argument("--config", default="c0", choices=["c0", "tiny", "dd16"])
     ap.add_argument("--out", default=os.path.join(
         os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
         "artifacts_cache"))
@@ -126,6 +126,12 @@ def main():
         # SURVEY.md §8(d1) config 0 (NM) + config 1 (LS) on the same snapshots
         build(60, 60, 2, 2, 6, 1e-7, 6, 4, 8, 1, a.epochs or 2000, 8, 16,
               180, (20, 8), a.out, a.procs, "c0")
+    elif a.config == "dd16":
+        # many-subdomain instance for subdomain sharding (config 4's layout at
+        # a trainable size): 60x60 grid, 4x4 subdomains, n = (8, 5) and
+        # n_C = 40 as config 4, 8x8 mu grid, 10% collocation rows
+        build(60, 60, 4, 4, 8, 1e-7, 8, 5, 8, 1, a.epochs or 2000, 40, 40,
+              45, None, a.out, a.procs, "dd16")
     else:
         # small fast instance for CPU unit tests: 24x24 grid, 2x2 subdomains
         build(24, 24, 2, 2, 4, 1e-7, 4, 3, 4, 1, a.epochs or 2000, 4, 8,
