@@ -31,6 +31,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ARTIFACT = os.path.join(ROOT, "tests", "golden", "c0_nm_artifacts.npz")
+# many-subdomain instance for the subdomain-sharded path (config 4's layout)
+DD_ARTIFACT = os.path.join(ROOT, "tests", "golden", "dd16_nm_artifacts.npz")
+DD_BATCH = 256
 METRIC = "DD NM-ROM-HR SQP solves/sec (batched mu)"
 UNIT = "solves/s"
 BATCH = 4096
@@ -295,6 +298,13 @@ def run_gpu(args):
     e2e = {"value": world * B / e2e_t, "unit": UNIT, "h2d_bytes_per_step": B * 2 * 8,
            "d2h_bytes_per_step": d2h}
 
+    sub = None
+    if not args.no_subdomain:
+        try:
+            sub = subdomain_bench(P, torch, dist, world, dev, stream, flush)
+        except Exception as exc:      # reported, never fatal for the headline line
+            sub = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -342,11 +352,48 @@ def run_gpu(args):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "decode": dec,
+        "subdomain": sub,
     }
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def subdomain_bench(P, torch, dist, world, dev, stream, flush, reps=3):
+    """The subdomain-sharded path: the 16-block dd16
+    instance, DD_BATCH seeded mu, blocks sharded over the ranks with an NCCL
+    all-gather of the block packets every SQP round (strong scaling: the
+    same batch at every N).  Device-timed with CUDA events, max over ranks."""
+    inst = P.RomInstance.load(DD_ARTIFACT)
+    mu = P.seeded_parameters(DD_BATCH, seed=2000)
+    P.solve_rom_batch_subdomain_sharded(inst, mu)            # warm-up (plans, buffers)
+    times, res = [], None
+    for _ in range(reps):
+        flush.fill_(2.0)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = P.solve_rom_batch_subdomain_sharded(inst, mu)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"workload": "dd16: 60x60 4x4 NM-ROM WFPC collocation HR, n=(8,5), n_C=40, "
+                        "45 rows/sub (config 4's layout at a trainable grid)",
+            "batch": DD_BATCH, "parallelism": f"subdomain-shard x{world} (NCCL all-gather of "
+                                              "block packets every SQP round)",
+            "scaling": "strong", "solves_per_s": DD_BATCH / (ms / 1e3), "ms_per_batch": ms,
+            "rounds": int(res.rounds), "mean_n_iter": float(res.n_iter.mean()),
+            "status_counts": np.bincount(res.status, minlength=4).tolist(),
+            "kernels": "k_dd_eval + k_dd_step per round"}
 
 
 def main():
@@ -357,6 +404,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-subdomain", action="store_true",
+                    help="skip the subdomain-sharded (dd16) measurement")
     ap.add_argument("--slots", type=int, default=0, help="mu slots per CTA (0 = largest that fits)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -203,4 +203,5 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
     res = sh.result()
     if hasattr(res, "seconds"):
         res.seconds = time.perf_counter() - t0
+        res.rounds = sh.rounds
     return res
