@@ -57,7 +57,21 @@ struct DecDev {
   const double* w1frag;   // [ceil(n_hidden/4)][32]: lane -> W1[4kb + (lane&3)][lane>>2]
   const double* v_row;    // [n_out][ell_w] W2 values, row-contiguous, 0-padded
   const int* row_w;       // [n_out] stored entries per row
+  // chained tensor-core sweep: W1 as the B operand, [ceil(n_hidden/4)][32]:
+  // lane -> k = 4kb + (lane&3), n = lane>>2: W1[k][n] (n < lat), 1 (n == lat), 0
+  const double* wbfrag;
 };
+
+// Chained tensor-core sweep (sweep_chain): a tile is 8 consecutive outputs of
+// one decoder with its k-block range [lo, hi] and the offset of its A
+// fragments (the banded W2 block, one 32-double fragment per k-block); a
+// chain is a run of consecutive tiles one warp walks k-block by k-block.
+// The host also flattens each chain's walk into steps: the k-block, the A
+// fragment index of each ring slot's live tile (-1: none) and the slots whose
+// tile ends there, so the device loop prefetches the next step's fragments.
+struct TileV2 { int o0, cnt, lo, hi, aoff; };
+struct ChainRec { int which, t0, nt, s0, ns; };     // which: 0 interior, 1 interface
+struct StepRec { int kb, last; int aidx[4]; };
 
 // A tensor-core sweep tile: up to 8/G consecutive outputs of one decoder with
 // everything its B operand needs, so a warp issues no dependent loads.
@@ -100,6 +114,11 @@ struct BlockDev {
   const TileRec* tiles;   // tensor-core sweep tiles of both decoders (or null)
   int n_tiles, n_tiles_in;  // total, interior (stored first)
   const double* tile_v;   // [n_tiles][10][32] B-operand W2 values per tile
+  const TileV2* t2;       // chained sweep tiles (interior, then interface)
+  const double* afr;      // their A fragments
+  const ChainRec* chains; // chains of tiles (null: per-output sweep)
+  const StepRec* steps;   // their k-block walks
+  int n_chains;
   StRows rows;
   const int* gio;
   const double* CA;       // WFPC: C A_i [n_c][ga.n_out]; SRPC: Ahat_i [n_c][ng]

@@ -314,6 +314,97 @@ __device__ __forceinline__ void sweep_tile(const View& V, const DecDev& D, const
   }
 }
 
+// phase B on the FP64 tensor cores, chained output tiles (default for banded
+// decoders with latent dim L <= 7):
+//   D[o][n] = sum_k W2[o][k] P[k][n],  P[k][n] = sigma'(z_k) W1[k][n] (n < L),
+//   P[k][L] = sigma(z_k)
+// gives the Jacobian rows (n < L) and the value (n = L) of 8 outputs per
+// mma.m8n8k4 -- hyper.py:190-197 with the reference's own intermediate
+// P = sigma' (.) W1 (the sum over the row's entries runs in k-blocks of 4).
+// A = the tile's banded W2 block (mu-independent, host-expanded fragments,
+// loaded once and used for every slot), B = P of one slot and one k-block
+// (formed once per slot and used by every live tile).  A warp walks the
+// k-blocks of its chain once with a ring of R live tiles; the host guarantees
+// tile j + R starts after tile j ends.
+template <int G, int L>
+__device__ __forceinline__ void sweep_chain(const View& V, const DecDev& D, const ChainRec& c,
+                                            const TileV2* tiles, const StepRec* steps,
+                                            const double* afr, int sig_off, int g_off, bool gam,
+                                            unsigned mask) {
+  if constexpr (L <= 7) {
+    constexpr int R = 4;
+    const int lane = threadIdx.x & 31, kq = lane & 3, n = lane >> 2;
+    const double* wb = D.wbfrag + lane;
+    const double* al = afr + lane;
+    const double* sp[G];
+#pragma unroll
+    for (int s = 0; s < G; ++s)
+      sp[s] = V.scr(s) + (n == L ? V.P.scr_sig : V.P.scr_dsig) + sig_off + kq;
+    double acc[R][G][2];
+    int jr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      jr[r] = r;
+#pragma unroll
+      for (int s = 0; s < G; ++s) acc[r][s][0] = acc[r][s][1] = 0.0;
+    }
+    // software pipeline: step records two steps ahead, fragments one ahead
+    const StepRec* sr = steps + c.s0;
+    StepRec s1 = sr[0];
+    StepRec s2 = c.ns > 1 ? sr[1] : s1;
+    double an[R], wn;
+    wn = __ldg(wb + (size_t)s1.kb * 32);
+#pragma unroll
+    for (int r = 0; r < R; ++r) an[r] = s1.aidx[r] >= 0 ? __ldg(al + (size_t)s1.aidx[r] * 32) : 0.0;
+    for (int i = 0; i < c.ns; ++i) {
+      double a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = an[r];
+      const double w = wn;
+      const StepRec now = s1;
+      s1 = s2;
+      if (i + 2 < c.ns) s2 = sr[i + 2];
+      if (i + 1 < c.ns) {
+        wn = __ldg(wb + (size_t)s1.kb * 32);
+#pragma unroll
+        for (int r = 0; r < R; ++r) an[r] = s1.aidx[r] >= 0 ? __ldg(al + (size_t)s1.aidx[r] * 32) : 0.0;
+      }
+      double b[G];
+#pragma unroll
+      for (int s = 0; s < G; ++s) b[s] = sp[s][4 * now.kb] * w;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (now.aidx[r] < 0) continue;                    // warp-uniform
+#pragma unroll
+        for (int s = 0; s < G; ++s) dmma_884(acc[r][s], a[r], b[s]);
+        if ((now.last >> r) & 1) {
+          const TileV2* t = tiles + c.t0 + jr[r];
+          const int o = __ldg(&t->o0) + n;
+          if (n < __ldg(&t->cnt)) {
+            const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
+#pragma unroll
+            for (int s = 0; s < G; ++s) {
+              if (!((mask >> s) & 1u)) continue;
+              double* jrow = (gam ? V.jgam(s) : V.jint(s)) + (size_t)o * L;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int col = 2 * kq + h;
+                if (col < L) jrow[col] = acc[r][s][h] * scl;
+                else if (col == L) V.scr(s)[g_off + o] = __dadd_rn(__dmul_rn(acc[r][s][h], scl), sh);
+              }
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < G; ++s) acc[r][s][0] = acc[r][s][1] = 0.0;
+          jr[r] += R;
+        }
+      }
+    }
+  } else {
+    __trap();   // the host builds chains only for latent dims <= 7
+  }
+}
+
 // phase B for a LinearMap (pod.py:86-93): g = Phi x
 template <int G, int L>
 __device__ __forceinline__ void linear_output(const View& V, const DecDev& D, int o, int xo,
@@ -547,7 +638,19 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       DDNM_MARK(V, 1);
     }
     // ---- phase B: outputs (+ Jacobian rows) ----
-    if (P.map_kind == MAP_AE && B.tiles) {
+    if (P.map_kind == MAP_AE && B.chains) {
+      // chained tensor-core sweep: warp per chain (interior chains first)
+      for (int ci = warp; ci < B.n_chains; ci += nw) {
+        const ChainRec cr = B.chains[ci];
+        if (cr.ns == 0) continue;
+        if (cr.which == 0)
+          sweep_chain<G, NI>(V, B.in, cr, B.t2, B.steps, B.afr, 0, P.scr_gint, false, mask);
+        else
+          sweep_chain<G, NG>(V, B.ga, cr, B.t2, B.steps, B.afr, nhi, P.scr_ggam, true, mask);
+      }
+      __syncthreads();
+      DDNM_MARK(V, 2);
+    } else if (P.map_kind == MAP_AE && B.tiles) {
       // tensor-core sweep: warp per tile (interior tiles first, then interface)
       const int ntt = B.n_tiles, nti = B.n_tiles_in;
       for (int t = warp; t < ntt; t += nw) {
