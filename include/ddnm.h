@@ -39,6 +39,7 @@ extern "C" {
 #define DDNM_ECUDA (-2)        /* CUDA runtime failure                          */
 #define DDNM_EUNSUPPORTED (-3) /* latent dims / sizes without a compiled kernel */
 #define DDNM_ENOMEM (-4)
+#define DDNM_EFORMAT (-5)      /* malformed binio / instance file (reference: FormatError) */
 
 /* per-mu solve status (reference: SqpResult.failure_reason / exceptions) */
 #define DDNM_STATUS_OK 0           /* loop ended on tol or max_iter (sqp.py:255)   */
@@ -304,6 +305,36 @@ int ddnm_dd_step(ddnm_dd* dd, const double* d_gathered, int32_t nranks,
                  int32_t* n_active);
 
 int ddnm_dd_end(ddnm_dd* dd);
+
+
+/* ---- binio (binio.py:1-87) and instance files -------------------------------
+ * The reference's language-neutral matrix format: magic "DDNMROM1", then per
+ * record u32 name length, UTF-8 name, u64 rows, u64 cols, rows*cols float64
+ * in column-major order, all little-endian (binio.py:1-8).  Reading checks
+ * the magic, truncation and overruns as read_matrices does (binio.py:43-70);
+ * writing is byte-identical to write_matrices (binio.py:22-40). */
+typedef struct ddnm_binio ddnm_binio;
+
+int ddnm_binio_read(const char* path, ddnm_binio** out);
+int ddnm_binio_count(const ddnm_binio* b, int64_t* n);
+/* Record i: name (valid until ddnm_binio_free), shape, column-major data. */
+int ddnm_binio_entry(const ddnm_binio* b, int64_t i, const char** name, int64_t* rows,
+                     int64_t* cols, const double** data);
+/* Record by name (the last one if repeated, as the reference's dict). */
+int ddnm_binio_find(const ddnm_binio* b, const char* name, int64_t* rows, int64_t* cols,
+                    const double** data);
+int ddnm_binio_free(ddnm_binio* b);
+/* n records; data[k] column-major [rows[k] x cols[k]]. */
+int ddnm_binio_write(const char* path, int64_t n, const char* const* names,
+                     const int64_t* rows, const int64_t* cols, const double* const* data);
+
+/* A context straight from an instance file pair: `path` (binio, every
+ * artifact array of ddnm_artifacts as a record named as in the package's
+ * .npz artifacts, integer arrays stored as float64 like the reference stores
+ * CSR indices, save_net autoencoder.py:424-450) and the meta file next to it
+ * (same stem, ".txt", binio.py:73-87 format, "format = ddnm-instance-1").
+ * Also registers the full decoders when the file has them.  No Python. */
+int ddnm_ctx_create_binio(int32_t device, const char* path, int32_t slots, ddnm_ctx** out);
 
 #ifdef __cplusplus
 }

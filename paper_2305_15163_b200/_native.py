@@ -135,6 +135,16 @@ def lib():
     L.ddnm_dd_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _ip, C.c_int64, C.c_void_p,
                                _ip]
     L.ddnm_dd_end.argtypes = [C.c_void_p]
+    L.ddnm_binio_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    L.ddnm_binio_count.argtypes = [C.c_void_p, _lp]
+    L.ddnm_binio_entry.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_char_p), _lp, _lp,
+                                   C.POINTER(_dp)]
+    L.ddnm_binio_find.argtypes = [C.c_void_p, C.c_char_p, _lp, _lp, C.POINTER(_dp)]
+    L.ddnm_binio_free.argtypes = [C.c_void_p]
+    L.ddnm_binio_write.argtypes = [C.c_char_p, C.c_int64, C.POINTER(C.c_char_p), _lp, _lp,
+                                   C.POINTER(_dp)]
+    L.ddnm_ctx_create_binio.argtypes = [C.c_int32, C.c_char_p, C.c_int32,
+                                        C.POINTER(C.c_void_p)]
     if L.ddnm_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libddnm.so ABI version mismatch; rebuild")
     _lib = L
@@ -146,7 +156,9 @@ EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_
             "ddnm_eval_batch", "ddnm_last_counters", "ddnm_last_profile",
             "ddnm_ctx_set_full_decoders", "ddnm_ctx_state_len", "ddnm_decode_batch",
             "ddnm_decode_batch_device", "ddnm_dd_packet_len", "ddnm_dd_begin",
-            "ddnm_dd_eval", "ddnm_dd_step", "ddnm_dd_end")
+            "ddnm_dd_eval", "ddnm_dd_step", "ddnm_dd_end", "ddnm_binio_read",
+            "ddnm_binio_count", "ddnm_binio_entry", "ddnm_binio_find", "ddnm_binio_free",
+            "ddnm_binio_write", "ddnm_ctx_create_binio")
 
 
 def check(rc: int):
@@ -156,6 +168,9 @@ def check(rc: int):
             raise NotImplementedError(msg)
         if rc == -1:
             raise ValueError(msg)
+        if rc == -5:
+            from .errors import FormatError
+            raise FormatError(msg)
         raise NativeError(f"libddnm error {rc}: {msg}")
 
 

@@ -47,6 +47,14 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+namespace ddnm {
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace ddnm
+
+namespace {
+
 #define CUDA_TRY(x)                                                                   \
   do {                                                                                \
     cudaError_t e_ = (x);                                                             \

@@ -60,8 +60,19 @@ class RomInstance:
 
     @classmethod
     def load(cls, path: str) -> "RomInstance":
+        """From the ``.npz`` artifacts or a binio instance file pair
+        (``.bin`` + ``.txt``, see :mod:`binio`)."""
+        if str(path).endswith(".bin"):
+            from .binio import load_instance_arrays
+            return cls(load_instance_arrays(path))
         with np.load(path, allow_pickle=False) as z:
             return cls(dict(z))
+
+    def save_binio(self, path: str) -> None:
+        """Write the artifacts as a binio instance file pair, the input of
+        the C entry point ``ddnm_ctx_create_binio``."""
+        from .binio import save_instance
+        save_instance(self, path)
 
     def split_latent(self, x):
         out, off = [], 0
