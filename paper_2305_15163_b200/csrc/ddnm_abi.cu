@@ -669,15 +669,17 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // (tile spans 13 k-blocks for 8 outputs of 24 entries: 46% dense A), and
   // the A fragments (230 KB per block) stream from L2 every round.
   const char* swv = getenv("DDNM_SWEEP");
-  if (ae && ni <= 7 && ng <= 7 && swv && atoi(swv) == 1 && !getenv("DDNM_DMMA")) {
+  // DDNM_SWEEP=2: chains for the interface decoder only
+  if (ae && ni <= 7 && ng <= 7 && swv && (atoi(swv) == 1 || atoi(swv) == 2) && !getenv("DDNM_DMMA")) {
     constexpr int R = 4;
-    const int nw = c->threads / 32;
+    const bool gam_only = atoi(swv) == 2;
+    const int nw = gam_only ? 4 : c->threads / 32;
     for (int b = 0; b < P.nb; ++b) {
       if (hwin[2 * b].k0.empty() || hwin[2 * b + 1].k0.empty()) continue;
       std::vector<TileV2> tl;
       std::vector<int> which_of;
       std::vector<double> afr;
-      for (int which = 0; which < 2; ++which) {
+      for (int which = gam_only ? 1 : 0; which < 2; ++which) {
         const HostWindows& hw = hwin[2 * b + which];
         const ddnm_decoder& h = which == 0 ? a->blocks[b].interior : a->blocks[b].interface;
         const int n = (int)hw.k0.size();
@@ -787,6 +789,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
           (rc = upload(c, ch.data(), ch.size(), const_cast<ChainRec**>(&BD.chains))))
         return bail(rc);
       BD.n_chains = (int)ch.size();
+      BD.chain_gam_only = gam_only ? 1 : 0;
     }
   }
   P.G = kern->g;

@@ -119,6 +119,8 @@ struct BlockDev {
   const ChainRec* chains; // chains of tiles (null: per-output sweep)
   const StepRec* steps;   // their k-block walks
   int n_chains;
+  int chain_gam_only;     // 1: chains cover the interface decoder only (the
+                          //    interior runs the per-output sweep)
   StRows rows;
   const int* gio;
   const double* CA;       // WFPC: C A_i [n_c][ga.n_out]; SRPC: Ahat_i [n_c][ng]

@@ -639,6 +639,24 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
     }
     // ---- phase B: outputs (+ Jacobian rows) ----
     if (P.map_kind == MAP_AE && B.chains) {
+      if (B.chain_gam_only) {
+        // interior on the per-output sweep, interface chains on the warps
+        // that run fewer interior items
+        constexpr int NQ = 2;
+        const int niq = NQ * B.in.n_out, A = (niq + 31) & ~31;
+        for (int it = tid; it < A; it += T) {
+          const bool valid = it < niq;
+          sweep_output<G, NI, NQ>(V, B.in, valid ? it / NQ : 0, it % NQ, valid, 0, P.scr_gint,
+                                  false, mask);
+        }
+        for (int ci = nw - 1 - warp; ci < B.n_chains; ci += nw) {
+          const ChainRec cr = B.chains[ci];
+          if (cr.ns > 0)
+            sweep_chain<G, NG>(V, B.ga, cr, B.t2, B.steps, B.afr, nhi, P.scr_ggam, true, mask);
+        }
+        __syncthreads();
+        DDNM_MARK(V, 2);
+      } else {
       // chained tensor-core sweep: warp per chain (interior chains first)
       for (int ci = warp; ci < B.n_chains; ci += nw) {
         const ChainRec cr = B.chains[ci];
@@ -650,6 +668,7 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       }
       __syncthreads();
       DDNM_MARK(V, 2);
+      }
     } else if (P.map_kind == MAP_AE && B.tiles) {
       // tensor-core sweep: warp per tile (interior tiles first, then interface)
       const int ntt = B.n_tiles, nti = B.n_tiles_in;
