@@ -306,3 +306,22 @@ def test_device_sharded_matches_reference_goldens():
         r = O.solve(oi, *g["mu"][k])
         if min(r.margins) > 1e-13 * r.merit_history[0]:
             assert res.n_iter[k] == r.n_iter == g["n_iter"][k], k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [1, 7])
+def test_device_sharded_edge_cases(B):
+    """Given x0 / lam0, a short max_iter, batches that do not fill a CTA:
+    the round kernels still reproduce the persistent kernel bit for bit."""
+    import paper_2305_15163_b200 as P
+    inst = P.RomInstance.load(golden_path("c0_nm", "artifacts"))
+    mu = P.seeded_parameters(B, seed=21)
+    cfg = P.SqpConfig(max_iter=3)
+    base = P.solve_rom_batch(inst, mu, cfg)
+    x0 = base.x0 * (1.0 + 1e-3)
+    for kw in ({}, {"x0": x0}, {"x0": x0, "lam0": base.lam0}):
+        ref = P.solve_rom_batch(inst, mu, cfg, **kw)
+        res = P.solve_rom_batch_subdomain_sharded(inst, mu, cfg, **kw)
+        for k in ("x", "lam", "n_iter", "n_evals", "status", "x0", "lam0"):
+            np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=f"{k} {kw.keys()}")
+        assert np.all(res.n_iter <= 3)
