@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -51,6 +52,23 @@ int fail(int code, const std::string& msg) {
 
 namespace ddnm {
 void set_error(const std::string& msg) { g_err = msg; }
+
+// The dynamic shared-memory limit is an attribute of the kernel function,
+// shared by every context of the process that uses the same specialisation:
+// only ever raise it, so a context planned with less shared memory cannot
+// invalidate the launches of one planned with more.
+cudaError_t raise_smem_limit(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& v = cur[{dev, fn}];
+  if (bytes <= v) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) v = bytes;
+  return e;
+}
 }  // namespace ddnm
 
 namespace {
@@ -798,10 +816,10 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.sm_eb = P.sm_vec + P.G * 8 * P.nK;
   P.sm_scr = P.sm_eb + P.G * 2 * P.eb_size;
   c->smem = footprint(P.G, kern_level, kern->kkt_global);
-  if (cudaFuncSetAttribute(kern->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
-      cudaFuncSetAttribute(kern->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
-      cudaFuncSetAttribute(kern->dd_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess ||
-      cudaFuncSetAttribute(kern->dd_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess)
+  if (raise_smem_limit(kern->solve, c->smem) != cudaSuccess ||
+      raise_smem_limit(kern->eval, c->smem) != cudaSuccess ||
+      raise_smem_limit(kern->dd_eval, c->smem) != cudaSuccess ||
+      raise_smem_limit(kern->dd_step, c->smem) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cannot reserve dynamic shared memory"));
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern->solve, c->threads, c->smem) != cudaSuccess || occ < 1)

@@ -16,6 +16,9 @@
 
 namespace ddnm {
 
+cudaError_t raise_smem_limit(const void* fn, size_t bytes);   // ddnm_abi.cu
+
+
 constexpr int DEC_MU = 8;
 constexpr int DEC_THREADS = 256;
 
@@ -147,7 +150,7 @@ int decode_mu_tile(int max_hidden, size_t smem_cap) {
 cudaError_t launch_decode(const DecodeParams& p, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
   const size_t smem = decode_smem(p.linear ? 0 : p.mu_tile, p.max_hidden);
-  cudaError_t e = cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = raise_smem_limit((const void*)k_decode, smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((p.B + p.mu_tile - 1) / p.mu_tile, p.n_jobs);
   k_decode<<<grid, DEC_THREADS, smem, s>>>(p);

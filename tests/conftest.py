@@ -9,7 +9,8 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls"]
 # SRPC coupling and gappy HR variants
-VARIANTS = ["tiny_nmg", "tiny_srpc", "tiny_lsg", "tiny_lss", "c0_nmg", "c0_srpc", "c0_lsg"]
+VARIANTS = ["tiny_nmg", "tiny_srpc", "tiny_lsg", "tiny_lss", "c0_nmg", "c0_srpc", "c0_lsg",
+            "c0_lss"]
 ALL = NAMES + VARIANTS
 
 

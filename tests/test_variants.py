@@ -18,7 +18,11 @@ their solves through invariants: c0_lsg (gappy bases of 16-45 vectors for 28
 latents: H_b = R_b^T R_b is rank deficient, cond(K) ~ 1e18) and c0_srpc
 (every trajectory meets a KKT system the reference must regularize: the
 trained Sigmoid port nets saturate, leaving latent directions no decoder
-output depends on)."""
+output depends on) and c0_lss (SRPC LS-ROM, n = (20, 19), n_C = 40: the
+60x60 LS-ROM's H_b already has cond ~ 1e21, SURVEY §7 hard part 2; the
+oracle's and the reference's first KKT steps differ by 7% while both solve
+K to 1e-10).  c0_lss's 196 x 196 KKT workspace does not fit in shared
+memory: it runs the (20, 19) kernels with the KKT workspace in L2 (KG)."""
 
 import numpy as np
 import pytest
@@ -29,7 +33,7 @@ from oracle import ddnm_oracle as O
 from .conftest import VARIANTS, sensitivity
 from .test_oracle_golden import merit_noise, rel
 
-ILL_POSED = {"c0_lsg", "c0_srpc"}
+ILL_POSED = {"c0_lsg", "c0_srpc", "c0_lss"}
 STEP_TOL = {"tiny_lss": 1e-7, "c0_srpc": 1e-8}   # K amplifies the 1e-13 input round-off
 WELL_POSED = [n for n in VARIANTS if n not in ILL_POSED]
 MIN_DETERMINED = {"tiny_srpc": 4}
