@@ -521,6 +521,13 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.nK = P.n_D + P.n_C;
   P.b_lo = 0;
   P.b_hi = P.nb;
+  // block-structured KKT for block systems W + n_C <= 32 always; up to 96 for
+  // autoencoder ROMs (dd16: 478 -> 92 ms per 1024 mu).  The LS-ROMs' block
+  // factorisations lose pivots to multiplier rows at nearly every solve
+  // (c0_ls: 138 -> 150 ms with the attempt), so they go straight to the
+  // dense LU there.  DDNM_KKT_BLOCK_MAX overrides.
+  P.kkt_block_max = a->map_kind == DDNM_MAP_AUTOENCODER ? 96 : 32;
+  if (const char* kb = getenv("DDNM_KKT_BLOCK_MAX")) P.kkt_block_max = std::min(96, atoi(kb));
   P.total_rows = row_off;
   P.tot_iout = iout; P.tot_gout = gout; P.tot_R = Roff; P.tot_cjac = cjoff;
   P.tot_intJ = ijoff; P.tot_gamJ = gjoff;

@@ -207,6 +207,9 @@ struct Params {
   int pk_stride, dd_nranks, dd_init;
   int dd_bnd[MAXB + 1];   // block range of rank r: [dd_bnd[r], dd_bnd[r+1])
   int* dd_active;         // k_dd_step: count of slots still running
+  // largest block system (W + n_C) the block-structured KKT is tried on
+  // (<= 96); larger ones go straight to the dense LU
+  int kkt_block_max;
   // KKT workspace in global memory (kernels instantiated with KG = true)
   double* kkt_g;          // per global slot [kkt_stride]
   long long kkt_stride;

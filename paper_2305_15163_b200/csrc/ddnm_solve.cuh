@@ -1500,17 +1500,47 @@ __device__ void kkt_block_forward(const Params& P, int b, const double* M, const
   constexpr int W = NI + NG;
   const int lane = threadIdx.x & 31;
   const int nC = P.n_C, ld = W + nC + 1;
-  // lane i holds row i of [y_b; tE] (W + nC <= 32) across the steps; the
-  // block's row swaps are applied as a gather
   const int m = W + nC;
-  double yl = lane < W ? y[swap_source(piv, W, lane)] : 0.0;
+  if (m <= WARP) {
+    // lane i holds row i of [y_b; tE] across the steps; the block's row swaps
+    // are applied as a gather
+    double yl = lane < W ? y[swap_source(piv, W, lane)] : 0.0;
+    __syncwarp();
+    for (int k = 0; k < W; ++k) {
+      const double yk = __shfl_sync(0xffffffffu, yl, k);
+      if (lane > k && lane < m) yl = fma(-M[lane * ld + k], yk, yl);
+    }
+    if (lane < W) y[lane] = yl;
+    else if (lane < m) tE[lane - W] = yl;
+    __syncwarp();
+    return;
+  }
+  // m <= 3 * 32 (many multipliers, e.g. n_C = 40): lane i holds rows i,
+  // i + 32, i + 64; the same per-row update sequence as above
+  constexpr int MR = 3;
+  double yl[MR];
+#pragma unroll
+  for (int r = 0; r < MR; ++r) {
+    const int row = lane + WARP * r;
+    yl[r] = row < W ? y[swap_source(piv, W, row)] : 0.0;
+  }
   __syncwarp();
   for (int k = 0; k < W; ++k) {
-    const double yk = __shfl_sync(0xffffffffu, yl, k);
-    if (lane > k && lane < m) yl = fma(-M[lane * ld + k], yk, yl);
+    const int kr = k >> 5;                              // warp-uniform
+    const double src = kr == 0 ? yl[0] : (kr == 1 ? yl[1] : yl[2]);
+    const double yk = __shfl_sync(0xffffffffu, src, k & 31);
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int row = lane + WARP * r;
+      if (row > k && row < m) yl[r] = fma(-M[row * ld + k], yk, yl[r]);
+    }
   }
-  if (lane < W) y[lane] = yl;
-  else if (lane < m) tE[lane - W] = yl;
+#pragma unroll
+  for (int r = 0; r < MR; ++r) {
+    const int row = lane + WARP * r;
+    if (row < W) y[row] = yl[r];
+    else if (row < m) tE[row - W] = yl[r];
+  }
   __syncwarp();
 }
 
@@ -1518,6 +1548,7 @@ __device__ void kkt_block_forward(const Params& P, int b, const double* M, const
 template <int NI, int NG>
 __device__ void kkt_block_backward(const Params& P, const double* M, double* y, const double* xE) {
   constexpr int W = NI + NG;
+  constexpr int MW = (W + WARP - 1) / WARP;   // rows per lane (W <= 32: one)
   const int lane = threadIdx.x & 31;
   const int nC = P.n_C, ld = W + nC + 1;
   for (int i = lane; i < W; i += WARP) {
@@ -1528,13 +1559,24 @@ __device__ void kkt_block_backward(const Params& P, const double* M, double* y, 
   __syncwarp();
   // column-oriented back substitution; the diagonal division is done by every
   // lane from registers (no lane-0 round trip through shared memory)
-  double yl = lane < W ? y[lane] : 0.0;
+  double yl[MW];
+#pragma unroll
+  for (int r = 0; r < MW; ++r) yl[r] = lane + WARP * r < W ? y[lane + WARP * r] : 0.0;
   for (int k = W - 1; k >= 0; --k) {
-    const double xk = __shfl_sync(0xffffffffu, yl, k) * rcp_fast(M[k * ld + k]);
-    if (lane == k) yl = xk;
-    if (lane < k) yl = fma(-M[lane * ld + k], xk, yl);
+    double src = yl[0];
+#pragma unroll
+    for (int r = 1; r < MW; ++r) if ((k >> 5) == r) src = yl[r];   // warp-uniform
+    const double xk = __shfl_sync(0xffffffffu, src, k & 31) * rcp_fast(M[k * ld + k]);
+#pragma unroll
+    for (int r = 0; r < MW; ++r) {
+      const int row = lane + WARP * r;
+      if (row == k) yl[r] = xk;
+      if (row < k) yl[r] = fma(-M[row * ld + k], xk, yl[r]);
+    }
   }
-  if (lane < W) y[lane] = yl;
+#pragma unroll
+  for (int r = 0; r < MW; ++r)
+    if (lane + WARP * r < W) y[lane + WARP * r] = yl[r];
   __syncwarp();
 }
 
@@ -1549,8 +1591,9 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const KktLayout L = kkt_layout<NI, NG>(P);
   const int nC = P.n_C, nb = P.nb;
-  // the register-resident substitutions need one lane per block-system row
-  if (tid < G) kflag[tid] = (W + nC <= WARP) ? 1 : 0;
+  // the register-resident substitutions hold up to three block-system rows
+  // per lane; the planner caps the block size it is worth trying at
+  if (tid < G) kflag[tid] = (W + nC <= P.kkt_block_max) ? 1 : 0;
   __syncthreads();
   DDNM_MARK(V, 12);
   // 1. per-block elimination
