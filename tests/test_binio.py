@@ -135,3 +135,31 @@ def test_context_from_instance_file_solves_identically(tmp_path, name):
             np.testing.assert_array_equal(st, P.decode_batch(inst, ref.x).states)
     finally:
         L.ddnm_ctx_destroy(h)
+
+
+@pytest.mark.gpu
+def test_c_program_solves_from_instance_file(tmp_path):
+    """examples/solve_binio.c: a C caller with no Python (context from an
+    instance file, batched solve, binio output) agrees bitwise with the
+    Python API on the same parameters."""
+    import subprocess
+
+    import paper_2305_15163_b200 as P
+    from paper_2305_15163_b200 import binio
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "solve_binio"
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "solve_binio.c"),
+                    "-L", os.path.join(root, "paper_2305_15163_b200"), "-lddnm",
+                    "-Wl,-rpath," + os.path.join(root, "paper_2305_15163_b200"),
+                    "-o", str(exe)], check=True)
+    inst = P.RomInstance.load(golden_path("c0_nm", "artifacts"))
+    inst.save_binio(tmp_path / "c0.bin")
+    out = subprocess.run([str(exe), str(tmp_path / "c0.bin"), "48", str(tmp_path / "out.bin")],
+                         check=True, capture_output=True, text=True)
+    assert "solved 48 parameters" in out.stdout
+    m = binio.read_matrices(tmp_path / "out.bin")
+    mu = np.ascontiguousarray(m["mu"].T)
+    ref = P.solve_rom_batch(inst, mu)
+    np.testing.assert_array_equal(m["latent"].T, ref.x)
+    np.testing.assert_array_equal(m["multipliers"].T, ref.lam)
