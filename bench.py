@@ -305,6 +305,13 @@ def run_gpu(args):
         except Exception as exc:      # reported, never fatal for the headline line
             sub = {"error": f"{type(exc).__name__}: {exc}"}
 
+    others = None
+    if not args.no_subdomain:
+        try:
+            others = other_configs_bench(P, N, C, _cfg_struct, torch, dist, dev, stream, flush)
+        except Exception as exc:      # reported, never fatal for the headline line
+            others = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -353,11 +360,75 @@ def run_gpu(args):
         "clocks": clk.summary(),
         "decode": dec,
         "subdomain": sub,
+        "other_configs": others,
     }
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+# the other BASELINE configs on one GPU (per rank, mu-sharded like the headline)
+OTHER_CONFIGS = [
+    ("config1_ls", "c0_ls", 4096, "config1: 60x60 2x2 LS-ROM WFPC collocation HR, n=(20,8), "
+                                  "n_C=16, 180 rows/sub"),
+    ("config3_layout_120", "c3s_nm", 1024, "config 3's layout at 120x120: 2x2 NM-ROM, "
+                                           "n=(8,5), n_C=10, 2% collocation rows (144/sub)"),
+    ("config4_layout_dd16", "dd16_nm", 256, "config 4's layout at 60x60: 4x4 NM-ROM, "
+                                            "n=(8,5), n_C=40, 45 rows/sub (persistent kernel)"),
+]
+
+
+def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, reps=3):
+    """Device-timed solves/s of the other BASELINE configs (CUDA events on the
+    launching stream, L2 flushed between launches, max over ranks)."""
+    out = {}
+    for key, name, B, desc in OTHER_CONFIGS:
+        path = os.path.join(ROOT, "tests", "golden", f"{name}_artifacts.npz")
+        if not os.path.exists(path):
+            continue
+        inst = P.RomInstance.load(path)
+        ctx = inst.context(dev.index)
+        rank = dist.get_rank() if dist else 0
+        mu = torch.from_numpy(P.seeded_parameters(B, seed=3000 + rank)).to(dev)
+        nD, nC = inst.n_primal, inst.n_mult
+        x = torch.empty((B, nD), dtype=torch.float64, device=dev)
+        lam = torch.empty((B, nC), dtype=torch.float64, device=dev)
+        st = torch.empty(B, dtype=torch.int32, device=dev)
+        it = torch.empty(B, dtype=torch.int32, device=dev)
+        so = N.SolveOut()
+        so.x = C.cast(C.c_void_p(x.data_ptr()), C.POINTER(C.c_double))
+        so.lam = C.cast(C.c_void_p(lam.data_ptr()), C.POINTER(C.c_double))
+        so.status = C.cast(C.c_void_p(st.data_ptr()), C.POINTER(C.c_int32))
+        so.n_iter = C.cast(C.c_void_p(it.data_ptr()), C.POINTER(C.c_int32))
+        cs = cfg_struct(P.SqpConfig())
+
+        def launch():
+            N.check(N.lib().ddnm_solve_batch_device(ctx.h, B, C.c_void_p(mu.data_ptr()), None,
+                                                    None, C.byref(cs), C.byref(so),
+                                                    C.c_void_p(stream.cuda_stream)))
+        launch()
+        times = []
+        for _ in range(reps):
+            flush.fill_(3.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            launch()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = float(np.median(times))
+        if dist:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        world = dist.get_world_size() if dist else 1
+        out[key] = {"workload": desc, "batch_per_gpu": B, "solves_per_s": world * B / (ms / 1e3),
+                    "ms_per_batch": ms, "mean_n_iter": float(it.float().mean().item()),
+                    "status_counts": torch.bincount(st.long(), minlength=4).tolist(),
+                    "slots_per_cta": ctx.info.slots_per_cta}
+    return out
 
 
 def subdomain_bench(P, torch, dist, world, dev, stream, flush, reps=3):
@@ -405,7 +476,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-subdomain", action="store_true",
-                    help="skip the subdomain-sharded (dd16) measurement")
+                    help="skip the extra measurements (subdomain-sharded dd16, other configs)")
     ap.add_argument("--slots", type=int, default=0, help="mu slots per CTA (0 = largest that fits)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -115,7 +115,7 @@ def build(nx: int, ny: int, sx: int, sy: int, grid_n: int, snap_tol: float,
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c0", choices=["c0", "tiny", "dd16"])
+    ap.add_argument("--config", default="c0", choices=["c0", "tiny", "dd16", "c3", "c3s"])
     ap.add_argument("--out", default=os.path.join(
         os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
         "artifacts_cache"))
@@ -126,6 +126,17 @@ def main():
         # SURVEY.md §8(d1) config 0 (NM) + config 1 (LS) on the same snapshots
         build(60, 60, 2, 2, 6, 1e-7, 6, 4, 8, 1, a.epochs or 2000, 8, 16,
               180, (20, 8), a.out, a.procs, "c0")
+    elif a.config == "c3":
+        # 480x480, 2x2, 8x8 mu grid, n = (8, 5),
+        # band 8, 2% collocation rows (2304 per subdomain), n_C = 10
+        build(480, 480, 2, 2, 8, 1e-7, 8, 5, 8, 1, a.epochs or 2000, 10, 10,
+              2304, None, a.out, a.procs, "c3")
+    elif a.config == "c3s":
+        # config 3's layout at 120x120 (the reference's FOM Newton stagnates
+        # at |r| ~ 1e-6 > tol = 1e-7 from 240x240 up, measured): 2x2, 8x8 mu
+        # grid, n = (8, 5), band 8, 2% collocation rows (144), n_C = 10
+        build(120, 120, 2, 2, 8, 1e-7, 8, 5, 8, 1, a.epochs or 2000, 10, 10,
+              144, None, a.out, a.procs, "c3s")
     elif a.config == "dd16":
         # many-subdomain instance for subdomain sharding (config 4's layout at
         # a trainable size): 60x60 grid, 4x4 subdomains, n = (8, 5) and

@@ -279,15 +279,26 @@ def state_goldens(inst, g: dict, n: int) -> dict:
     from ddrom.driver import relative_error, restrict_blocks
     from ddrom.burgers import solve_monolithic
 
+    from ddrom.errors import ConvergenceError
     part = inst.partition
-    out = {"mu": g["mu"][:n], "x": g["x"][:n]}
-    for k in range(n):
-        states = inst.decode(g["x"][k])
-        out[f"s{k}"] = np.concatenate([np.concatenate([xi, xg]) for xi, xg in states])
+    rows = []
+    out = {}
+    for k in range(g["mu"].shape[0]):
+        if len(rows) == n:
+            break
         p = ParameterPoint(float(g["mu"][k, 0]), float(g["mu"][k, 1]))
-        fom, _ = solve_monolithic(part.grid, p)
-        out[f"fom{k}"] = np.asarray(fom, dtype=float)
-        out[f"err{k}"] = np.float64(relative_error(restrict_blocks(part, fom), states))
+        try:
+            fom, _ = solve_monolithic(part.grid, p)
+        except ConvergenceError:
+            continue          # the FOM Newton stagnates at this mu: take the next one
+        j = len(rows)
+        states = inst.decode(g["x"][k])
+        out[f"s{j}"] = np.concatenate([np.concatenate([xi, xg]) for xi, xg in states])
+        out[f"fom{j}"] = np.asarray(fom, dtype=float)
+        out[f"err{j}"] = np.float64(relative_error(restrict_blocks(part, fom), states))
+        rows.append(k)
+    out["mu"] = g["mu"][rows]
+    out["x"] = g["x"][rows]
     return out
 
 
