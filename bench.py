@@ -433,38 +433,45 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
 
 def subdomain_bench(P, torch, dist, world, dev, stream, flush, reps=3):
     """The subdomain-sharded path: the 16-block dd16
-    instance, DD_BATCH seeded mu, blocks sharded over the ranks with an NCCL
-    all-gather of the block packets every SQP round (strong scaling: the
-    same batch at every N).  Device-timed with CUDA events, max over ranks."""
+    instance, DD_BATCH seeded mu, blocks sharded over the ranks with an
+    exchange of the block packets every SQP round -- an NCCL all-gather after
+    the evaluation kernel, or the evaluation kernel storing the packets into
+    every rank's buffer over peer memory ("p2p", CUDA IPC) -- strong scaling
+    (the same batch at every N).  Device-timed with CUDA events, max over
+    ranks."""
     inst = P.RomInstance.load(DD_ARTIFACT)
     mu = P.seeded_parameters(DD_BATCH, seed=2000)
-    P.solve_rom_batch_subdomain_sharded(inst, mu)            # warm-up (plans, buffers)
-    times, res = [], None
-    for _ in range(reps):
-        flush.fill_(2.0)
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        res = P.solve_rom_batch_subdomain_sharded(inst, mu)
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
-    ms = float(np.median(times))
-    if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    return {"workload": "dd16: 60x60 4x4 NM-ROM WFPC collocation HR, n=(8,5), n_C=40, "
-                        "45 rows/sub (config 4's layout at a trainable grid)",
-            "batch": DD_BATCH, "parallelism": f"subdomain-shard x{world} (NCCL all-gather of "
-                                              "block packets every SQP round)",
-            "scaling": "strong", "solves_per_s": DD_BATCH / (ms / 1e3), "ms_per_batch": ms,
-            "rounds": int(res.rounds), "mean_n_iter": float(res.n_iter.mean()),
-            "status_counts": np.bincount(res.status, minlength=4).tolist(),
-            "kernels": "k_dd_eval + k_dd_step per round"}
+    out = {"workload": "dd16: 60x60 4x4 NM-ROM WFPC collocation HR, n=(8,5), n_C=40, "
+                       "45 rows/sub (config 4's layout at a trainable grid)",
+           "batch": DD_BATCH, "scaling": "strong", "ranks": world,
+           "kernels": "k_dd_eval + k_dd_step per SQP round"}
+    for transport in ("nccl", "p2p"):
+        try:
+            P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport)   # warm-up
+            times, res = [], None
+            for _ in range(reps):
+                flush.fill_(2.0)
+                if dist:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                res = P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport)
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+            ms = float(np.median(times))
+            if dist:
+                t = torch.tensor([ms], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            out[transport] = {"solves_per_s": DD_BATCH / (ms / 1e3), "ms_per_batch": ms,
+                              "rounds": int(res.rounds), "mean_n_iter": float(res.n_iter.mean()),
+                              "status_counts": np.bincount(res.status, minlength=4).tolist()}
+        except Exception as exc:      # reported per transport, never fatal
+            out[transport] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 def main():

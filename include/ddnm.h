@@ -304,7 +304,22 @@ int ddnm_dd_step(ddnm_dd* dd, const double* d_gathered, int32_t nranks,
                  const int32_t* bounds, int64_t pk_stride, void* stream,
                  int32_t* n_active);
 
+/* ddnm_dd_eval with the all-gather fused in: the kernel stores this rank's
+ * packets straight into every rank's gathered buffer, at
+ * peers[r] + (rank * B + mu) * pk_stride, over NVLink (peer stores; peers[r]
+ * valid on this device: same-process peer access or ddnm_ipc_open_handle).
+ * The caller then needs only a cross-rank barrier ordered on `stream` (e.g. a
+ * one-element NCCL all-reduce) before ddnm_dd_step on its own buffer. */
+int ddnm_dd_eval_p2p(ddnm_dd* dd, double* const* peers, int32_t nranks, int32_t rank,
+                     int64_t pk_stride, void* stream);
+
 int ddnm_dd_end(ddnm_dd* dd);
+
+/* CUDA IPC of a device buffer between the processes of one node (64-byte
+ * handles, exchanged by the caller), for ddnm_dd_eval_p2p's peer buffers. */
+int ddnm_ipc_get_handle(const void* dptr, unsigned char* handle);
+int ddnm_ipc_open_handle(const unsigned char* handle, void** dptr);
+int ddnm_ipc_close_handle(void* dptr);
 
 
 /* ---- binio (binio.py:1-87) and instance files -------------------------------

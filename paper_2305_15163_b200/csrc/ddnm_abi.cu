@@ -1332,6 +1332,51 @@ int ddnm_dd_eval(ddnm_dd* d, double* d_packets, int64_t pk_stride, void* stream)
   return dd_run(d, d->c->K.dd_eval, s, nullptr);
 }
 
+int ddnm_dd_eval_p2p(ddnm_dd* d, double* const* peers, int32_t nranks, int32_t rank,
+                     int64_t pk_stride, void* stream) {
+  if (!d || !peers) return fail(DDNM_EINVAL, "null argument");
+  if (nranks < 1 || nranks > MAXB || rank < 0 || rank >= nranks)
+    return fail(DDNM_EINVAL, "need 1..16 ranks and 0 <= rank < nranks");
+  int off = 0;
+  const int len = eb_span(d->c, d->P.b_lo, d->P.b_hi, &off);
+  if (pk_stride < len) return fail(DDNM_EINVAL, "packet stride shorter than this rank's packet");
+  for (int r = 0; r < nranks; ++r)
+    if (!peers[r]) return fail(DDNM_EINVAL, "null peer buffer");
+  CUDA_TRY(cudaSetDevice(d->c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  d->stream = s;
+  d->P.pk_stride = (int)pk_stride;
+  d->P.dd_npeers = nranks;
+  d->P.dd_rank = rank;
+  for (int r = 0; r < nranks; ++r) d->P.dd_peers[r] = peers[r];
+  const int rc = dd_run(d, d->c->K.dd_eval, s, nullptr);   // parameters copied at launch
+  d->P.dd_npeers = 0;
+  return rc;
+}
+
+int ddnm_ipc_get_handle(const void* dptr, unsigned char* handle) {
+  if (!dptr || !handle) return fail(DDNM_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  return 0;
+}
+
+int ddnm_ipc_open_handle(const unsigned char* handle, void** dptr) {
+  if (!handle || !dptr) return fail(DDNM_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int ddnm_ipc_close_handle(void* dptr) {
+  if (!dptr) return fail(DDNM_EINVAL, "null argument");
+  CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return 0;
+}
+
 int ddnm_dd_step(ddnm_dd* d, const double* d_gathered, int32_t nranks, const int32_t* bounds,
                  int64_t pk_stride, void* stream, int32_t* n_active) {
   if (!d || !d_gathered || !bounds) return fail(DDNM_EINVAL, "null argument");

@@ -207,6 +207,10 @@ struct Params {
   int pk_stride, dd_nranks, dd_init;
   int dd_bnd[MAXB + 1];   // block range of rank r: [dd_bnd[r], dd_bnd[r+1])
   int* dd_active;         // k_dd_step: count of slots still running
+  // peer-memory all-gather fused into k_dd_eval: when dd_npeers > 0 the
+  // packets go straight to every rank's gathered buffer (NVLink stores)
+  double* dd_peers[MAXB];
+  int dd_npeers, dd_rank;
   // largest block system (W + n_C) the block-structured KKT is tried on
   // (<= 96); larger ones go straight to the dense LU
   int kkt_block_max;

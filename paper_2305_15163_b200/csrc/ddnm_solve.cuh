@@ -2178,10 +2178,21 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_eval(const __grid_co
   const int len = (P.b_hi < P.nb ? P.blk[P.b_hi].eb_off : P.eb_rho) - off;
   for (int s = 0; s < G; ++s) {
     if (!((mask >> s) & 1u)) continue;
-    double* dst = P.dd_pk + (size_t)s_mu[s] * P.pk_stride;
     const double* e = V.eb(s, 0) + off;
-    for (int i = tid; i < len; i += T) dst[i] = e[i];
+    if (P.dd_npeers == 0) {
+      double* dst = P.dd_pk + (size_t)s_mu[s] * P.pk_stride;
+      for (int i = tid; i < len; i += T) dst[i] = e[i];
+    } else {
+      // fused all-gather: this rank's slice of every rank's gathered buffer
+      // [nranks][B][pk_stride], stored over NVLink while other CTAs evaluate
+      const size_t row = ((size_t)P.dd_rank * P.B + s_mu[s]) * P.pk_stride;
+      for (int r = 0; r < P.dd_npeers; ++r) {
+        double* dst = P.dd_peers[r] + row;
+        for (int i = tid; i < len; i += T) dst[i] = e[i];
+      }
+    }
   }
+  if (P.dd_npeers > 0) __threadfence_system();   // visible to the peers' step kernels
   if (tid == 0) atomicAdd(P.counters, (unsigned long long)__popc(mask) * (P.b_hi - P.b_lo));
 }
 

@@ -105,6 +105,10 @@ class DeviceRoundEngine:
         N.check(N.lib().ddnm_dd_eval(self.h, C.c_void_p(packets.data_ptr()), stride,
                                      self._stream()))
 
+    def eval_p2p(self, peers, rank: int, stride: int) -> None:
+        arr = (C.c_void_p * len(peers))(*[C.c_void_p(p) for p in peers])
+        N.check(N.lib().ddnm_dd_eval_p2p(self.h, arr, len(peers), rank, stride, self._stream()))
+
     def step(self, gathered, nranks: int, bounds, stride: int) -> int:
         bnd = (C.c_int32 * len(bounds))(*bounds)
         n = C.c_int32()
@@ -158,6 +162,12 @@ class ShardedSolve:
         self.eng.eval(self.packets, self.stride)
         return self.packets
 
+    def eval_p2p(self, peers):
+        """Evaluation with the all-gather fused in: the kernel stores this
+        rank's packets into every rank's gathered buffer (``peers[r]``, device
+        addresses valid on this GPU) over peer memory."""
+        self.eng.eval_p2p(peers, self.rank, self.stride)
+
     def step(self, gathered) -> int:
         self.active = self.eng.step(gathered, self.world, self.bounds, self.stride)
         self.rounds += 1
@@ -177,12 +187,48 @@ def _all_gather(gathered, packets, world, group):
         dist.all_gather(list(gathered.view(world, -1).unbind(0)), packets, group=group)
 
 
+class _PeerBuffers:
+    """Every rank's gathered buffer mapped on this GPU (CUDA IPC handles
+    exchanged over ``group``) for the fused peer-store all-gather."""
+
+    def __init__(self, gathered, rank, world, group):
+        import torch.distributed as dist
+        L = N.lib()
+        h = C.create_string_buffer(64)
+        N.check(L.ddnm_ipc_get_handle(C.c_void_p(gathered.data_ptr()), h))
+        handles = [None] * world
+        dist.all_gather_object(handles, h.raw, group=group)
+        self.opened = []
+        self.ptrs = []
+        for r, hr in enumerate(handles):
+            if r == rank:
+                self.ptrs.append(gathered.data_ptr())
+                continue
+            p = C.c_void_p()
+            N.check(L.ddnm_ipc_open_handle(hr, C.byref(p)))
+            self.opened.append(p)
+            self.ptrs.append(p.value)
+
+    def close(self):
+        for p in self.opened:
+            N.lib().ddnm_ipc_close_handle(p)
+        self.opened = []
+
+
 def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(), *,
                                       x0=None, lam0=None, group=None, device: int = -1,
-                                      engine=None):
+                                      engine=None, transport: str = "nccl"):
     """Batched ``solve_rom`` (driver.py:554-597, compute_error=False) with the
     subdomain blocks sharded over the ranks of ``group`` (every rank passes
-    the same ``mus``); every rank returns the same full ``BatchResult``."""
+    the same ``mus``); every rank returns the same full ``BatchResult``.
+
+    ``transport``: ``"nccl"`` -- evaluation kernel, then an NCCL all-gather of
+    the packets; ``"p2p"`` -- the evaluation kernel stores its packets into
+    every rank's gathered buffer over peer memory (CUDA IPC between the
+    processes of one node) and a one-element all-reduce orders the ranks
+    before the step (device engine only)."""
+    if transport not in ("nccl", "p2p"):
+        raise ValueError("transport must be 'nccl' or 'p2p'")
     import torch.distributed as dist
 
     from .driver import _mu_array
@@ -195,11 +241,25 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
                       device=device)
     gathered = sh.packets if world == 1 else sh.eng.buffer(world * sh.B * sh.stride)
     active = sh.active
-    while active:
-        packets = sh.eval()
-        if world > 1:
-            _all_gather(gathered, packets, world, group)
-        active = sh.step(gathered)
+    peers = None
+    if transport == "p2p":
+        peers = _PeerBuffers(gathered, rank, world, group) if world > 1 else None
+        ptrs = peers.ptrs if peers else [gathered.data_ptr()]
+        flag = sh.eng.buffer(1)
+    try:
+        while active:
+            if transport == "p2p":
+                sh.eval_p2p(ptrs)
+                if world > 1:
+                    dist.all_reduce(flag, group=group)     # orders every rank's stores
+            else:
+                packets = sh.eval()
+                if world > 1:
+                    _all_gather(gathered, packets, world, group)
+            active = sh.step(gathered)
+    finally:
+        if peers:
+            peers.close()
     res = sh.result()
     if hasattr(res, "seconds"):
         res.seconds = time.perf_counter() - t0

@@ -325,3 +325,54 @@ def test_device_sharded_edge_cases(B):
         for k in ("x", "lam", "n_iter", "n_evals", "status", "x0", "lam0"):
             np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=f"{k} {kw.keys()}")
         assert np.all(res.n_iter <= 3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_device_fused_peer_gather(world):
+    """The fused evaluation + all-gather (k_dd_eval storing every rank's slice
+    straight into every rank's gathered buffer): world rank states in one
+    process, one GPU, run one after another; results equal the one-rank
+    solve bitwise on every rank."""
+    import torch
+
+    import paper_2305_15163_b200 as P
+    from paper_2305_15163_b200.subdomain import ShardedSolve
+    inst = P.RomInstance.load(golden_path(DD, "artifacts"))
+    mu = P.seeded_parameters(20, seed=8)
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    if world == 1:
+        res = P.solve_rom_batch_subdomain_sharded(inst, mu, transport="p2p")
+        for k in ("x", "lam", "n_iter", "status"):
+            np.testing.assert_array_equal(getattr(res, k), getattr(one, k), err_msg=k)
+        return
+    cfg = P.SqpConfig()
+    ranks = [ShardedSolve(inst, mu, cfg, r, world) for r in range(world)]
+    n = world * ranks[0].B * ranks[0].stride
+    gathered = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+                for _ in ranks]
+    ptrs = [g.data_ptr() for g in gathered]
+    active = ranks[0].active
+    while active:
+        for sh in ranks:
+            sh.eval_p2p(ptrs)
+        counts = [sh.step(g) for sh, g in zip(ranks, gathered)]
+        assert len(set(counts)) == 1
+        active = counts[0]
+    for sh in ranks:
+        r = sh.result()
+        for k in ("x", "lam", "n_iter", "n_evals", "status"):
+            np.testing.assert_array_equal(getattr(r, k), getattr(one, k), err_msg=k)
+
+
+@pytest.mark.gpu
+def test_ipc_handle_of_a_device_buffer():
+    import ctypes as C
+
+    import torch
+
+    from paper_2305_15163_b200 import _native as N
+    t = torch.zeros(1024, dtype=torch.float64, device="cuda")
+    h = C.create_string_buffer(64)
+    N.check(N.lib().ddnm_ipc_get_handle(C.c_void_p(t.data_ptr()), h))
+    assert any(h.raw)
