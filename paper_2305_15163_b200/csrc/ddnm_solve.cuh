@@ -1228,9 +1228,8 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
   double* rhs = work + (size_t)n * ld + n;
   double* res = rhs + n;
   double* tmp = res + n;
-  double* lbuf = tmp + 2 * n;  // multipliers of the current column (sol is at tmp + n)
-  __shared__ double s_pval, s_kk, s_rp, s_rhsn, s_delta, s_wmax[32], s_red[32];
-  __shared__ int s_p, s_fin, s_widx[32];
+  __shared__ double s_rhsn, s_delta, s_red[32];
+  __shared__ int s_fin;
   for (int i = tid; i < n; i += T) rhs[i] = -(i < P.n_D ? e[P.eb_rho + i] : e[P.eb_con + i - P.n_D]);
   __syncthreads();
   if (warp == 0) {
@@ -1265,80 +1264,85 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
         K[i * ld + j] = v;
       }
     __syncthreads();
-    // column-0 pivot candidates: per-warp partial maxima
-    {
-      double best = -1.0;
-      int bi = n;
-      for (int i = warp; i < n; i += nw) {     // lane 0 of each warp scans its rows
-        if (lane == 0) {
-          const double a = fabs(K[i * ld]);
-          if (a > best || (a == best && i < bi)) { best = a; bi = i; }
-        }
-      }
-      if (lane == 0) { s_wmax[warp] = best; s_widx[warp] = bi; }
-    }
-    __syncthreads();
-    for (int k = 0; k < n; ++k) {
+    // right-looking LU with partial pivoting in panels of NB columns: warp 0
+    // factors the panel (pivot search, swaps, scaling and rank-1 updates
+    // inside the panel), then the CTA applies the panel's row swaps to the
+    // other columns, the unit-lower solve for the panel rows and the trailing
+    // update.  Every element sees the same fma(-l, u, a) sequence in the same
+    // k order as the column-by-column elimination, with 4 barriers per panel
+    // instead of 2 per column.
+    constexpr int NB = 8;
+    for (int j0 = 0; j0 < n; j0 += NB) {
+      const int j1 = min(n, j0 + NB);
       if (warp == 0) {
-        double best = lane < nw ? s_wmax[lane] : -1.0;
-        int bi = lane < nw ? s_widx[lane] : n;
+        for (int k = j0; k < j1; ++k) {
+          double best = -1.0;
+          int bi = n;
+          for (int i = k + lane; i < n; i += WARP) {
+            const double a = fabs(K[i * ld + k]);
+            if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        if (lane == 0) {
-          piv[k] = bi;
-          s_p = bi;
-          const double pv = K[bi * ld + k];
-          s_pval = pv;
-          s_kk = K[k * ld + k];
-          s_rp = pv != 0.0 && fabs(pv) >= 2.2250738585072014e-308 ? rcp_fast(pv) : 0.0;
-        }
-      }
-      __syncthreads();
-      const int p = s_p;
-      const double pv = s_pval, rp = s_rp;
-      // swap rows k and p (all columns but k), column k: pivot + multipliers
-      if (p != k)
-        for (int j = tid; j < n; j += T) {
-          if (j == k) continue;
-          const double t = K[k * ld + j];
-          K[k * ld + j] = K[p * ld + j];
-          K[p * ld + j] = t;
-        }
-      for (int i = k + tid; i < n; i += T) {
-        double v = i == p ? s_kk : K[i * ld + k];
-        if (i == k) v = pv;
-        if (i > k && pv != 0.0) v = rp != 0.0 ? v * rp : v / pv;
-        K[i * ld + k] = v;
-        lbuf[i] = v;
-      }
-      __syncthreads();
-      // rank-1 update; lane 0 of each warp owns column k+1 and tracks its
-      // pivot candidates (first max over its rows)
-      double best = -1.0;
-      int bi = n;
-      if (pv != 0.0) {
-        for (int j = k + 1 + lane; j < n; j += WARP) {
-          const double ukj = K[k * ld + j];
-          for (int i = k + 1 + warp; i < n; i += nw) {
-            const double v = fma(-lbuf[i], ukj, K[i * ld + j]);
-            K[i * ld + j] = v;
-            if (j == k + 1) {
-              const double a = fabs(v);
-              if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+          }
+          if (lane == 0) piv[k] = bi;
+          if (bi != k)
+            for (int j = j0 + lane; j < j1; j += WARP) {
+              const double t = K[k * ld + j];
+              K[k * ld + j] = K[bi * ld + j];
+              K[bi * ld + j] = t;
+            }
+          __syncwarp();
+          const double pv = K[k * ld + k];
+          if (pv != 0.0) {
+            const double rp = fabs(pv) >= 2.2250738585072014e-308 ? rcp_fast(pv) : 0.0;
+            for (int i = k + 1 + lane; i < n; i += WARP) {
+              const double v = K[i * ld + k];
+              K[i * ld + k] = rp != 0.0 ? v * rp : v / pv;
+            }
+            __syncwarp();
+            for (int i = k + 1 + lane; i < n; i += WARP) {
+              const double l = K[i * ld + k];
+              for (int j = k + 1; j < j1; ++j) K[i * ld + j] = fma(-l, K[k * ld + j], K[i * ld + j]);
             }
           }
-        }
-      } else if (lane == 0) {
-        for (int i = k + 1 + warp; i < n; i += nw) {
-          const double a = fabs(K[i * ld + k + 1]);
-          if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+          __syncwarp();
         }
       }
-      if (lane == 0) { s_wmax[warp] = best; s_widx[warp] = bi; }
+      __syncthreads();
+      // the panel's row swaps on the columns outside it, in pivot order
+      for (int c = tid; c < n; c += T) {
+        if (c >= j0 && c < j1) continue;
+        for (int k = j0; k < j1; ++k) {
+          const int p = piv[k];
+          if (p != k) {
+            const double t = K[k * ld + c];
+            K[k * ld + c] = K[p * ld + c];
+            K[p * ld + c] = t;
+          }
+        }
+      }
+      __syncthreads();
+      // panel rows of the trailing columns (unit-lower solve)
+      for (int c = j1 + tid; c < n; c += T)
+        for (int k = j0; k < j1; ++k) {
+          if (K[k * ld + k] == 0.0) continue;          // zero pivot: no update
+          const double u = K[k * ld + c];
+          for (int i = k + 1; i < j1; ++i) K[i * ld + c] = fma(-K[i * ld + k], u, K[i * ld + c]);
+        }
+      __syncthreads();
+      // trailing update A22 -= L21 U12, k in pivot order per element
+      const int m = n - j1;
+      for (int idx = tid; idx < m * m; idx += T) {
+        const int i = j1 + idx / m, c = j1 + idx % m;
+        double a = K[i * ld + c];
+        for (int k = j0; k < j1; ++k)
+          if (K[k * ld + k] != 0.0) a = fma(-K[i * ld + k], K[k * ld + c], a);
+        K[i * ld + c] = a;
+      }
       __syncthreads();
     }
     // solve, one refinement, check (sqp.py:175-189)
