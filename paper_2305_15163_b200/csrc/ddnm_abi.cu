@@ -1225,6 +1225,13 @@ struct ddnm_dd {
   double* vec = nullptr;
   double* ecur = nullptr;
   int* active = nullptr;
+  // per-solve copies of the context's per-slot scratch (boundary values,
+  // Jacobian rows, KKT workspace): a sharded solve never shares them with
+  // another solve on the same context
+  double* gbv = nullptr;
+  double* gJ = nullptr;
+  double* gJg = nullptr;
+  double* kkt_g = nullptr;
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
 };
 
@@ -1283,7 +1290,12 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   d->B = B;
   d->ctas = (B + c->P.G - 1) / c->P.G;
   auto bail = [&](int r) { ddnm_dd_end(d); return r; };
-  if ((rc = ensure_gbv(c, (size_t)d->ctas * c->P.G))) return bail(rc);
+  const size_t slots = (size_t)d->ctas * c->P.G;
+  if (cudaMalloc(&d->gbv, slots * std::max(c->tot_rows * 3, 1) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&d->gJ, slots * std::max(c->P.gJ_stride, 1) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&d->gJg, slots * std::max(c->P.gJg_stride, 1) * sizeof(double)) != cudaSuccess ||
+      (c->kkt_stride && cudaMalloc(&d->kkt_g, slots * c->kkt_stride * sizeof(double)) != cudaSuccess))
+    return bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve scratch"));
   if (cudaMalloc(&d->st, (size_t)B * sizeof(SlotState)) != cudaSuccess ||
       cudaMalloc(&d->vec, (size_t)B * 8 * c->P.nK * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&d->ecur, (size_t)B * c->P.eb_size * sizeof(double)) != cudaSuccess ||
@@ -1305,10 +1317,10 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   P.so.merit_hist = o->merit_hist; P.so.obj_hist = o->obj_hist; P.so.alpha_hist = o->alpha_hist;
   P.so.x0 = o->x0; P.so.lam0 = o->lam0;
   P.so.n_iter = o->n_iter; P.so.n_evals = o->n_evals; P.so.status = o->status; P.so.n_reg = o->n_reg;
-  P.gbv = c->gbv;
-  P.gJ = c->gJ;
-  P.gJg = c->gJg;
-  P.kkt_g = c->kkt_g;
+  P.gbv = d->gbv;
+  P.gJ = d->gJ;
+  P.gJg = d->gJg;
+  P.kkt_g = d->kkt_g;
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
@@ -1418,6 +1430,8 @@ int ddnm_dd_end(ddnm_dd* d) {
   if (d->vec) cudaFree(d->vec);
   if (d->ecur) cudaFree(d->ecur);
   if (d->active) cudaFree(d->active);
+  for (double* p : {d->gbv, d->gJ, d->gJg, d->kkt_g})
+    if (p) cudaFree(p);
   delete d;
   return 0;
 }
