@@ -892,6 +892,9 @@ int ddnm_ctx_info(const ddnm_ctx* c, ddnm_info* i) {
 
 static int ensure_gbv(ddnm_ctx* c, size_t slots) {
   if (c->gbv_slots >= slots) return 0;
+  // growing: work queued earlier (device entry points are asynchronous on
+  // the caller's stream) may still use the old buffers
+  if (c->gbv_slots) CUDA_TRY(cudaDeviceSynchronize());
   if (c->gbv) cudaFree(c->gbv);
   if (c->gJ) cudaFree(c->gJ);
   c->gbv = nullptr;
