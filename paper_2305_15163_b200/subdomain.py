@@ -192,22 +192,37 @@ class _PeerBuffers:
     exchanged over ``group``) for the fused peer-store all-gather."""
 
     def __init__(self, gathered, rank, world, group):
+        import torch
         import torch.distributed as dist
         L = N.lib()
         h = C.create_string_buffer(64)
-        N.check(L.ddnm_ipc_get_handle(C.c_void_p(gathered.data_ptr()), h))
+        err = None
+        if L.ddnm_ipc_get_handle(C.c_void_p(gathered.data_ptr()), h) != 0:
+            err = L.ddnm_last_error().decode(errors="replace")
         handles = [None] * world
-        dist.all_gather_object(handles, h.raw, group=group)
+        dist.all_gather_object(handles, None if err else h.raw, group=group)
         self.opened = []
         self.ptrs = []
         for r, hr in enumerate(handles):
             if r == rank:
                 self.ptrs.append(gathered.data_ptr())
                 continue
+            if err or hr is None:
+                err = err or f"rank {r} could not export its buffer"
+                continue
             p = C.c_void_p()
-            N.check(L.ddnm_ipc_open_handle(hr, C.byref(p)))
+            if L.ddnm_ipc_open_handle(hr, C.byref(p)) != 0:
+                err = L.ddnm_last_error().decode(errors="replace")
+                continue
             self.opened.append(p)
             self.ptrs.append(p.value)
+        # every rank learns whether all mappings succeeded, so a failure on
+        # one rank never leaves the others waiting in the round loop
+        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64, device=gathered.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() < 1.0:
+            self.close()
+            raise RuntimeError(f"peer-memory mapping failed: {err or 'on another rank'}")
 
     def close(self):
         for p in self.opened:
