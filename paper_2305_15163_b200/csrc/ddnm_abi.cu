@@ -597,7 +597,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // instantiated with KG = true), so it does not count against shared memory
   auto scr_total = [&](int level, bool kg = false) {
     int s0 = plan_scratch(level);
-    int t = std::max(std::max(s0, kg ? 0 : kkt_need), std::max(ls_need, rbf_need2));
+    // (kg: the Schur block, n_C x (n_C + 1), stays in this scratch)
+    int t = std::max(std::max(s0, kg ? P.n_C * (P.n_C + 1) : kkt_need), std::max(ls_need, rbf_need2));
     return (t + 1) & ~1;
   };
   auto footprint = [&](int G, int level, bool kg = false) {

@@ -1615,7 +1615,9 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   if (warp < G && ((kmask >> warp) & 1u) && kflag[warp]) {
     const int s = warp;
     double* sc = kws<KG>(V, s);
-    double* S = sc + L.off_S;
+    // KG: the Schur block lives in the slot's (idle) shared evaluation
+    // scratch, so its LU and solves do not pay L2 latency per step
+    double* S = KG ? V.scr(s) : sc + L.off_S;
     for (int idx = lane; idx < nC * nC; idx += WARP) {
       const int i = idx / nC, j = idx - i * nC;
       double v = 0.0;
@@ -1659,7 +1661,8 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
         y[c] = v;
       }
       __syncwarp();
-      warp_lu_solve(sc + L.off_S, L.ldS, nC, reinterpret_cast<const int*>(sc + L.off_pivS), y);
+      warp_lu_solve(KG ? V.scr(s) : sc + L.off_S, L.ldS, nC,
+                    reinterpret_cast<const int*>(sc + L.off_pivS), y);
     }
     __syncthreads();
     DDNM_MARK(V, 10);
