@@ -66,7 +66,7 @@ int main(int argc, char** argv) {
   const char* names[3] = {"latent", "multipliers", "mu"};
   const int64_t rows[3] = {nD, nC, 2}, cols[3] = {B, B, B};
   const double* data[3] = {x, lam, mu};
-  CHECK(ddnm_binio_write(argv[3], 3, names, rows, cols, data));
+  CHECK(ddnm_binio_write(argv[3], 3, names, NULL, rows, cols, data));
   printf("solved %d parameters: %d ok, %lld block evaluations, %lld KKT solves, n_iter[0] = %d\n",
          B, ok, (long long)evals, (long long)kkts, n_iter[0]);
   ddnm_ctx_destroy(ctx);

@@ -332,16 +332,19 @@ typedef struct ddnm_binio ddnm_binio;
 
 int ddnm_binio_read(const char* path, ddnm_binio** out);
 int ddnm_binio_count(const ddnm_binio* b, int64_t* n);
-/* Record i: name (valid until ddnm_binio_free), shape, column-major data. */
-int ddnm_binio_entry(const ddnm_binio* b, int64_t i, const char** name, int64_t* rows,
-                     int64_t* cols, const double** data);
+/* Record i: name bytes and their length (valid until ddnm_binio_free; a
+ * name may contain NUL bytes), shape, column-major data. */
+int ddnm_binio_entry(const ddnm_binio* b, int64_t i, const char** name, int64_t* name_len,
+                     int64_t* rows, int64_t* cols, const double** data);
 /* Record by name (the last one if repeated, as the reference's dict). */
 int ddnm_binio_find(const ddnm_binio* b, const char* name, int64_t* rows, int64_t* cols,
                     const double** data);
 int ddnm_binio_free(ddnm_binio* b);
-/* n records; data[k] column-major [rows[k] x cols[k]]. */
+/* n records; data[k] column-major [rows[k] x cols[k]]; name_lens NULL:
+ * NUL-terminated names. */
 int ddnm_binio_write(const char* path, int64_t n, const char* const* names,
-                     const int64_t* rows, const int64_t* cols, const double* const* data);
+                     const int64_t* name_lens, const int64_t* rows, const int64_t* cols,
+                     const double* const* data);
 
 /* A context straight from an instance file pair: `path` (binio, every
  * artifact array of ddnm_artifacts as a record named as in the package's

@@ -142,12 +142,12 @@ def lib():
     L.ddnm_ipc_close_handle.argtypes = [C.c_void_p]
     L.ddnm_binio_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
     L.ddnm_binio_count.argtypes = [C.c_void_p, _lp]
-    L.ddnm_binio_entry.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_char_p), _lp, _lp,
-                                   C.POINTER(_dp)]
+    L.ddnm_binio_entry.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), _lp, _lp,
+                                   _lp, C.POINTER(_dp)]
     L.ddnm_binio_find.argtypes = [C.c_void_p, C.c_char_p, _lp, _lp, C.POINTER(_dp)]
     L.ddnm_binio_free.argtypes = [C.c_void_p]
     L.ddnm_binio_write.argtypes = [C.c_char_p, C.c_int64, C.POINTER(C.c_char_p), _lp, _lp,
-                                   C.POINTER(_dp)]
+                                   _lp, C.POINTER(_dp)]
     L.ddnm_ctx_create_binio.argtypes = [C.c_int32, C.c_char_p, C.c_int32,
                                         C.POINTER(C.c_void_p)]
     if L.ddnm_abi_version() != ABI_VERSION:

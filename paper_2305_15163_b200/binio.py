@@ -44,14 +44,16 @@ def read_matrices(path) -> dict:
         _check(L.ddnm_binio_count(h, C.byref(n)))
         out = {}
         for i in range(n.value):
-            name = C.c_char_p()
+            name, nlen = C.c_void_p(), C.c_int64()
             r, c = C.c_int64(), C.c_int64()
             d = C.POINTER(C.c_double)()
-            _check(L.ddnm_binio_entry(h, i, C.byref(name), C.byref(r), C.byref(c), C.byref(d)))
+            _check(L.ddnm_binio_entry(h, i, C.byref(name), C.byref(nlen), C.byref(r), C.byref(c),
+                                      C.byref(d)))
             cnt = r.value * c.value
             flat = (np.ctypeslib.as_array(d, shape=(cnt,)).copy() if cnt
                     else np.zeros(0))
-            out[name.value.decode("utf-8")] = flat.reshape((r.value, c.value), order="F")
+            key = C.string_at(name, nlen.value).decode("utf-8") if nlen.value else ""
+            out[key] = flat.reshape((r.value, c.value), order="F")
         return out
     finally:
         L.ddnm_binio_free(h)
@@ -74,10 +76,11 @@ def write_matrices(path, matrices) -> None:
         bufs.append(f)
     n = len(items)
     cn = (C.c_char_p * n)(*names)
+    cl = (C.c_int64 * n)(*[len(b) for b in names])
     cr = (C.c_int64 * n)(*rows)
     cc = (C.c_int64 * n)(*cols)
     cd = (C.POINTER(C.c_double) * n)(*[b.ctypes.data_as(C.POINTER(C.c_double)) for b in bufs])
-    _check(N.lib().ddnm_binio_write(str(path).encode(), n, cn, cr, cc, cd))
+    _check(N.lib().ddnm_binio_write(str(path).encode(), n, cn, cl, cr, cc, cd))
 
 
 def write_meta(path, entries: dict) -> None:

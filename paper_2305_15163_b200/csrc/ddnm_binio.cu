@@ -157,11 +157,12 @@ int ddnm_binio_count(const ddnm_binio* b, int64_t* n) {
   return 0;
 }
 
-int ddnm_binio_entry(const ddnm_binio* b, int64_t i, const char** name, int64_t* rows,
-                     int64_t* cols, const double** data) {
+int ddnm_binio_entry(const ddnm_binio* b, int64_t i, const char** name, int64_t* name_len,
+                     int64_t* rows, int64_t* cols, const double** data) {
   if (!b || i < 0 || i >= (int64_t)b->recs.size()) return bfail(DDNM_EINVAL, "record index out of range");
   const Record& r = b->recs[(size_t)i];
-  if (name) *name = r.name.c_str();
+  if (name) *name = r.name.data();
+  if (name_len) *name_len = (int64_t)r.name.size();   // names may hold NUL bytes
   if (rows) *rows = r.rows;
   if (cols) *cols = r.cols;
   if (data) *data = r.data.data();
@@ -173,7 +174,7 @@ int ddnm_binio_find(const ddnm_binio* b, const char* name, int64_t* rows, int64_
   if (!b || !name) return bfail(DDNM_EINVAL, "null argument");
   auto it = b->index.find(name);
   if (it == b->index.end()) return bfail(DDNM_EINVAL, std::string("no record '") + name + "'");
-  return ddnm_binio_entry(b, (int64_t)it->second, nullptr, rows, cols, data);
+  return ddnm_binio_entry(b, (int64_t)it->second, nullptr, nullptr, rows, cols, data);
 }
 
 int ddnm_binio_free(ddnm_binio* b) {
@@ -181,13 +182,14 @@ int ddnm_binio_free(ddnm_binio* b) {
   return 0;
 }
 
-int ddnm_binio_write(const char* path, int64_t n, const char* const* names, const int64_t* rows,
-                     const int64_t* cols, const double* const* data) {
+int ddnm_binio_write(const char* path, int64_t n, const char* const* names,
+                     const int64_t* name_lens, const int64_t* rows, const int64_t* cols,
+                     const double* const* data) {
   if (!path || (n > 0 && (!names || !rows || !cols || !data))) return bfail(DDNM_EINVAL, "null argument");
   std::string s("DDNMROM1", 8);
   for (int64_t k = 0; k < n; ++k) {
     if (rows[k] < 0 || cols[k] < 0) return bfail(DDNM_EINVAL, "negative matrix dimension");
-    const size_t nl = std::strlen(names[k]);
+    const size_t nl = name_lens ? (size_t)name_lens[k] : std::strlen(names[k]);
     put_u32(s, (uint32_t)nl);
     s.append(names[k], nl);
     put_u64(s, (uint64_t)rows[k]);

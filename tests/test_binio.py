@@ -163,3 +163,34 @@ def test_c_program_solves_from_instance_file(tmp_path):
     ref = P.solve_rom_batch(inst, mu)
     np.testing.assert_array_equal(m["latent"].T, ref.x)
     np.testing.assert_array_equal(m["multipliers"].T, ref.lam)
+
+
+def test_round_trip_property(tmp_path):
+    """Random record sets: the C++ writer and reader are inverse, bit for bit
+    (names in UTF-8, empty and one-column matrices, any float64 pattern)."""
+    from hypothesis import HealthCheck, given, settings
+    from hypothesis import strategies as st
+
+    from paper_2305_15163_b200 import binio
+
+    shapes = st.tuples(st.integers(0, 5), st.integers(0, 5))
+    names = st.text(min_size=0, max_size=12)
+
+    @settings(max_examples=60, deadline=None,
+              suppress_health_check=[HealthCheck.function_scoped_fixture])
+    @given(st.lists(st.tuples(names, shapes, st.integers(0, 2 ** 32 - 1)), min_size=0,
+                    max_size=6, unique_by=lambda t: t[0]))
+    def check(recs):
+        mats = []
+        for nm, (r, c), seed in recs:
+            bits = np.random.default_rng(seed).integers(0, 2 ** 63, size=r * c, dtype=np.int64)
+            mats.append((nm, bits.view(np.float64).reshape(r, c)))
+        path = tmp_path / "p.bin"
+        binio.write_matrices(path, mats)
+        got = binio.read_matrices(path)
+        assert list(got) == [m[0] for m in mats]
+        for nm, a in mats:
+            assert got[nm].shape == a.shape
+            np.testing.assert_array_equal(got[nm].view(np.uint64), a.view(np.uint64))
+
+    check()

@@ -72,3 +72,63 @@ def test_argument_validation_before_device():
         P.SqpConfig(backtrack_factor=1.5)
     with pytest.raises(NotImplementedError):
         P.solve_rom(inst, P.ParameterPoint(100.0, 10.0), compute_error=True)
+
+
+def _artifacts(name="tiny_nm"):
+    import paper_2305_15163_b200 as P
+    from .conftest import golden_path
+    inst = P.RomInstance.load(golden_path(name, "artifacts"))
+    art, keep = inst._artifacts_struct()
+    return inst, art, keep
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda a: setattr(a, "abi_version", 1), "ABI version"),
+    (lambda a: setattr(a, "n_blocks", 0), "blocks"),
+    (lambda a: setattr(a, "n_blocks", 17), "blocks"),
+    (lambda a: setattr(a, "n_c", 0), "multiplier"),
+    (lambda a: setattr(a, "nx", 1), "grid"),
+    (lambda a: setattr(a, "nu", 0.0), "grid"),
+    (lambda a: setattr(a, "map_kind", 7), "map kind"),
+    (lambda a: setattr(a, "constraint_mode", 5), "constraint mode"),
+    (lambda a: setattr(a.blocks[1], "n_int", a.blocks[0].n_int + 1), "latent dims"),
+    (lambda a: setattr(a.blocks[0], "n_cols", a.blocks[0].n_cols + 1), "n_cols"),
+    (lambda a: setattr(a.blocks[0], "n_rows", 0), "sample row set is empty"),
+    (lambda a: setattr(a.blocks[0], "CA", None), "CA"),
+    (lambda a: setattr(a.blocks[0].interior, "n_out", a.blocks[0].interior.n_out + 1),
+     "n_io"),
+])
+def test_ctx_create_rejects_malformed_artifacts(mutate, msg):
+    """ddnm_ctx_create validates the artifacts before touching a device
+    (ValueError / NotImplementedError as the reference's ValueErrors)."""
+    from paper_2305_15163_b200 import _native as N
+    inst, art, keep = _artifacts()
+    mutate(art)
+    h = C.c_void_p()
+    rc = N.lib().ddnm_ctx_create(-1, C.byref(art), 0, C.byref(h))
+    assert rc in (-1, -3) and not h.value
+    assert msg.lower() in N.lib().ddnm_last_error().decode().lower()
+
+
+def test_gio_out_of_range_rejected():
+    from paper_2305_15163_b200 import _native as N
+    inst, art, keep = _artifacts()
+    blk = art.blocks[0]
+    bad = np.ascontiguousarray(np.full(blk.n_gio, 10 ** 9, dtype=np.int64))
+    keep.append(bad)
+    blk.gio = N.ptr(bad, C.c_int64)
+    h = C.c_void_p()
+    assert N.lib().ddnm_ctx_create(-1, C.byref(art), 0, C.byref(h)) == -1
+    assert "gio" in N.lib().ddnm_last_error().decode()
+
+
+def test_null_and_range_arguments():
+    from paper_2305_15163_b200 import _native as N
+    L = N.lib()
+    assert L.ddnm_ctx_create(-1, None, 0, None) == -1
+    assert L.ddnm_dd_packet_len(None, 0, 1, None) == -1
+    assert L.ddnm_binio_read(None, None) == -1
+    assert L.ddnm_binio_write(None, 0, None, None, None, None, None) == -1
+    assert L.ddnm_ipc_get_handle(None, None) == -1
+    n = C.c_int64()
+    assert L.ddnm_binio_count(None, C.byref(n)) == -1
