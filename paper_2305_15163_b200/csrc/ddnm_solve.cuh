@@ -47,6 +47,15 @@ struct View {
     }                                                        \
   } while (0)
 
+// every per-slot region (vectors, evaluation buffers, scratch) starts zeroed:
+// shared memory keeps the previous kernel's contents, and a slot must not see
+// them (c0_nmg once diverged on the first launch after other instances ran)
+__device__ __forceinline__ void zero_slots(const View& V) {
+  const Params& P = V.P;
+  const int n = P.sm_scr + P.G * P.scr_size - P.sm_vec;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ddnm_smem[P.sm_vec + i] = 0.0;
+}
+
 // block pieces inside an eval buffer
 __device__ __forceinline__ int tri_n(int w) { return w * (w + 1) / 2; }
 __device__ __forceinline__ double* eb_H(double* e, const BlockDev& B) { return e + B.eb_off; }
@@ -2068,7 +2077,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
   if (tid == 0) { s_evals = 0; s_kkts = 0; }
   if (tid < 16) s_prof[tid] = 0;
   if (P.prof) V.prof = s_prof;
-  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+  zero_slots(V);
   __syncthreads();
   if (tid == 0) s_prof[15] = clock64();
   for (;;) {
@@ -2172,7 +2181,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_eval(const __grid_co
   __shared__ int s_ebi[G];
   const unsigned mask = dd_load_state<G>(V, s_mu);
   if (mask == 0) return;
-  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+  zero_slots(V);
   if (tid < G) s_ebi[tid] = 0;
   for (int s = 0; s < G; ++s) {
     if (!((mask >> s) & 1u)) continue;
@@ -2221,7 +2230,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
       if (mu < P.B) slot_reset(st[tid], mu);
       else { st[tid].mu = -1; st[tid].phase = PH_IDLE; }
     }
-    for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+    zero_slots(V);
     __syncthreads();
     for (int s = 0; s < G; ++s)
       if (st[s].mu >= 0) slot_bvals(V, s, st[s].mu);
@@ -2241,7 +2250,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
   const unsigned mask = dd_load_state<G>(V, s_mu);
   if (mask == 0) return;
   if (tid == 0) s_kkts = 0;
-  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+  zero_slots(V);
   // state, current eval buffer (slot 0) and the gathered trial evaluation
   // (slot 1; slot 0 for the first evaluation of a new mu)
   for (int s = 0; s < G; ++s) {
@@ -2309,7 +2318,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS) k_eval(const __grid_constant
   __shared__ int s_ebi[G];
   __shared__ unsigned s_mask;
   // finite (zero) padding past n_hidden for the sweeps
-  for (int i = tid; i < G * P.scr_size; i += T) ddnm_smem[P.sm_scr + i] = 0.0;
+  zero_slots(V);
   if (tid == 0) {
     unsigned m = 0;
     for (int s = 0; s < G; ++s) {

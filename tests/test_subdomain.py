@@ -242,7 +242,8 @@ def _rel(a, b):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["c0_nm", DD])
+@pytest.mark.parametrize("name", ["c0_nm", DD, "tiny_srpc", "c0_nmg", "c0_ls", "c3s_nm",
+                                  "c0_lss"])
 def test_device_sharded_world1_equals_megakernel(name, gpu_instances):
     """One rank owning every block: the round kernels reproduce the
     persistent kernel bit for bit (same per-slot arithmetic)."""
