@@ -48,8 +48,10 @@ struct View {
   } while (0)
 
 // every per-slot region (vectors, evaluation buffers, scratch) starts zeroed:
-// shared memory keeps the previous kernel's contents, and a slot must not see
-// them (c0_nmg once diverged on the first launch after other instances ran)
+// shared memory keeps the previous kernel's contents.  (c0_nmg once diverged
+// at one mu on the first launch after other instances ran; the culprit was a
+// slot-state field read before it was set -- states are now value-initialised
+// -- and the zeroing keeps every slot region equally clean.)
 __device__ __forceinline__ void zero_slots(const View& V) {
   const Params& P = V.P;
   const int n = P.sm_scr + P.G * P.scr_size - P.sm_vec;
@@ -2073,7 +2075,10 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
   __shared__ unsigned long long s_evals, s_kkts;
   __shared__ int s_kres[G], s_kflag[G];
   __shared__ unsigned long long s_prof[16];
-  if (tid < G) { st[tid].mu = -1; st[tid].phase = PH_DONE; s_cur[tid] = 0; }
+  if (tid < G) {
+    st[tid] = SlotState{};
+    st[tid].mu = -1; st[tid].phase = PH_DONE; s_cur[tid] = 0; s_kres[tid] = 0; s_kflag[tid] = 0;
+  }
   if (tid == 0) { s_evals = 0; s_kkts = 0; }
   if (tid < 16) s_prof[tid] = 0;
   if (P.prof) V.prof = s_prof;
@@ -2227,6 +2232,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
     if (tid < G) {
       const int mu = blockIdx.x * G + tid;
       s_mu[tid] = mu;
+      st[tid] = SlotState{};
       if (mu < P.B) slot_reset(st[tid], mu);
       else { st[tid].mu = -1; st[tid].phase = PH_IDLE; }
     }
