@@ -49,9 +49,10 @@ struct View {
 
 // every per-slot region (vectors, evaluation buffers, scratch) starts zeroed:
 // shared memory keeps the previous kernel's contents.  (c0_nmg once diverged
-// at one mu on the first launch after other instances ran; the culprit was a
-// slot-state field read before it was set -- states are now value-initialised
-// -- and the zeroing keeps every slot region equally clean.)
+// at one mu on the first launch after other instances ran: value-initialising
+// the slot states and KKT flags alone removes it, so a state/flag was read
+// before being set; both are now initialised and the zeroing keeps every slot
+// region equally clean.)
 __device__ __forceinline__ void zero_slots(const View& V) {
   const Params& P = V.P;
   const int n = P.sm_scr + P.G * P.scr_size - P.sm_vec;
