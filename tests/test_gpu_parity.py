@@ -220,3 +220,23 @@ def test_single_mu_api(gpu_instances, oracle_instances, goldens):
     assert rel(Br, g["d0_b0_Br"]) < 1e-10
     cval, cjac = prob.blocks[0].constraint(prob.split(x0)[0][1])
     assert rel(cjac, g["d0_b0_con_jac"]) < 1e-12
+
+
+@pytest.mark.gpu
+def test_results_independent_of_launch_history():
+    """A context's solves do not depend on what ran on the GPU before
+    (leftover shared memory of other instances' kernels): the first solve of
+    c0_nmg after other instances equals its later solves and a fresh
+    instance's, bit for bit."""
+    import paper_2305_15163_b200 as P
+    from .conftest import golden_path
+    mu = P.seeded_parameters(64, seed=3)
+    for name in ("c0_nm", "dd16_nm", "tiny_srpc"):
+        P.solve_rom_batch(P.RomInstance.load(golden_path(name, "artifacts")), mu)
+    inst = P.RomInstance.load(golden_path("c0_nmg", "artifacts"))
+    runs = [P.solve_rom_batch(inst, mu) for _ in range(3)]
+    shard = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    for r in runs[1:] + [shard]:
+        np.testing.assert_array_equal(r.x, runs[0].x)
+        np.testing.assert_array_equal(r.lam, runs[0].lam)
+        np.testing.assert_array_equal(r.n_iter, runs[0].n_iter)
