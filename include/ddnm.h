@@ -316,7 +316,11 @@ int ddnm_dd_eval_p2p(ddnm_dd* dd, double* const* peers, int32_t nranks, int32_t 
 int ddnm_dd_end(ddnm_dd* dd);
 
 /* CUDA IPC of a device buffer between the processes of one node (64-byte
- * handles, exchanged by the caller), for ddnm_dd_eval_p2p's peer buffers. */
+ * handles, exchanged by the caller), for ddnm_dd_eval_p2p's peer buffers.
+ * A handle maps the start of the cudaMalloc allocation holding dptr, so the
+ * exported buffer must be a whole allocation: ddnm_dev_alloc (zeroed). */
+int ddnm_dev_alloc(int32_t device, int64_t bytes, void** out);
+int ddnm_dev_free(void* p);
 int ddnm_ipc_get_handle(const void* dptr, unsigned char* handle);
 int ddnm_ipc_open_handle(const unsigned char* handle, void** dptr);
 int ddnm_ipc_close_handle(void* dptr);

@@ -140,6 +140,8 @@ def lib():
     L.ddnm_ipc_get_handle.argtypes = [C.c_void_p, C.c_char_p]
     L.ddnm_ipc_open_handle.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
     L.ddnm_ipc_close_handle.argtypes = [C.c_void_p]
+    L.ddnm_dev_alloc.argtypes = [C.c_int32, C.c_int64, C.POINTER(C.c_void_p)]
+    L.ddnm_dev_free.argtypes = [C.c_void_p]
     L.ddnm_binio_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
     L.ddnm_binio_count.argtypes = [C.c_void_p, _lp]
     L.ddnm_binio_entry.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), _lp, _lp,
@@ -164,7 +166,8 @@ EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_
             "ddnm_dd_eval", "ddnm_dd_step", "ddnm_dd_end", "ddnm_binio_read",
             "ddnm_binio_count", "ddnm_binio_entry", "ddnm_binio_find", "ddnm_binio_free",
             "ddnm_binio_write", "ddnm_ctx_create_binio", "ddnm_dd_eval_p2p",
-            "ddnm_ipc_get_handle", "ddnm_ipc_open_handle", "ddnm_ipc_close_handle")
+            "ddnm_ipc_get_handle", "ddnm_ipc_open_handle", "ddnm_ipc_close_handle",
+            "ddnm_dev_alloc", "ddnm_dev_free")
 
 
 def check(rc: int):

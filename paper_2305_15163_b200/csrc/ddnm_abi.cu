@@ -1381,6 +1381,20 @@ int ddnm_dd_eval_p2p(ddnm_dd* d, double* const* peers, int32_t nranks, int32_t r
   return rc;
 }
 
+int ddnm_dev_alloc(int32_t device, int64_t bytes, void** out) {
+  if (!out || bytes <= 0) return fail(DDNM_EINVAL, "bad allocation request");
+  *out = nullptr;
+  if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaMalloc(out, (size_t)bytes));
+  CUDA_TRY(cudaMemset(*out, 0, (size_t)bytes));
+  return 0;
+}
+
+int ddnm_dev_free(void* p) {
+  if (p) CUDA_TRY(cudaFree(p));
+  return 0;
+}
+
 int ddnm_ipc_get_handle(const void* dptr, unsigned char* handle) {
   if (!dptr || !handle) return fail(DDNM_EINVAL, "null argument");
   cudaIpcMemHandle_t h;

@@ -187,6 +187,23 @@ def _all_gather(gathered, packets, world, group):
         dist.all_gather(list(gathered.view(world, -1).unbind(0)), packets, group=group)
 
 
+class _DevBuffer:
+    """A whole cudaMalloc allocation (CUDA IPC handles map allocations, not
+    sub-allocations of torch's caching allocator)."""
+
+    def __init__(self, nbytes: int, device: int):
+        self.p = C.c_void_p()
+        N.check(N.lib().ddnm_dev_alloc(device, nbytes, C.byref(self.p)))
+
+    def data_ptr(self) -> int:
+        return self.p.value
+
+    def close(self):
+        if self.p:
+            N.lib().ddnm_dev_free(self.p)
+            self.p = C.c_void_p()
+
+
 class _PeerBuffers:
     """Every rank's gathered buffer mapped on this GPU (CUDA IPC handles
     exchanged over ``group``) for the fused peer-store all-gather."""
@@ -218,7 +235,8 @@ class _PeerBuffers:
             self.ptrs.append(p.value)
         # every rank learns whether all mappings succeeded, so a failure on
         # one rank never leaves the others waiting in the round loop
-        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64, device=gathered.device)
+        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64,
+                          device=torch.device("cuda", torch.cuda.current_device()))
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
         if ok.item() < 1.0:
             self.close()
@@ -254,11 +272,21 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
     t0 = time.perf_counter()
     sh = ShardedSolve(instance, mu, cfg, rank, world, x0=x0, lam0=lam0, engine=engine,
                       device=device)
-    gathered = sh.packets if world == 1 else sh.eng.buffer(world * sh.B * sh.stride)
     active = sh.active
-    peers = None
+    peers = own = None
+    if transport == "p2p" and world > 1:
+        # the exported buffer is its own allocation (IPC maps allocations)
+        own = _DevBuffer(world * sh.B * sh.stride * 8, sh.eng.dev.index)
+        gathered = own
+    else:
+        gathered = sh.packets if world == 1 else sh.eng.buffer(world * sh.B * sh.stride)
     if transport == "p2p":
-        peers = _PeerBuffers(gathered, rank, world, group) if world > 1 else None
+        try:
+            peers = _PeerBuffers(gathered, rank, world, group) if world > 1 else None
+        except Exception:
+            if own:
+                own.close()
+            raise
         ptrs = peers.ptrs if peers else [gathered.data_ptr()]
         flag = sh.eng.buffer(1)
     try:
@@ -275,6 +303,11 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
     finally:
         if peers:
             peers.close()
+        if own:
+            torch_sync = getattr(sh.eng, "torch", None)
+            if torch_sync is not None:
+                torch_sync.cuda.current_stream(sh.eng.dev).synchronize()
+            own.close()
     res = sh.result()
     if hasattr(res, "seconds"):
         res.seconds = time.perf_counter() - t0

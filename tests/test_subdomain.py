@@ -368,12 +368,28 @@ def test_device_fused_peer_gather(world):
 
 @pytest.mark.gpu
 def test_ipc_handle_of_a_device_buffer():
+    """The exported gathered buffer is a whole allocation (a CUDA IPC handle
+    maps the start of the allocation holding the pointer) and the fused
+    exchange runs on it."""
     import ctypes as C
 
     import torch
 
+    import paper_2305_15163_b200 as P
     from paper_2305_15163_b200 import _native as N
-    t = torch.zeros(1024, dtype=torch.float64, device="cuda")
+    from paper_2305_15163_b200.subdomain import ShardedSolve, _DevBuffer
+    inst = P.RomInstance.load(golden_path(DD, "artifacts"))
+    mu = P.seeded_parameters(7, seed=2)
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    sh = ShardedSolve(inst, mu, P.SqpConfig(), 0, 1)
+    buf = _DevBuffer(sh.B * sh.stride * 8, torch.cuda.current_device())
     h = C.create_string_buffer(64)
-    N.check(N.lib().ddnm_ipc_get_handle(C.c_void_p(t.data_ptr()), h))
+    N.check(N.lib().ddnm_ipc_get_handle(C.c_void_p(buf.data_ptr()), h))
     assert any(h.raw)
+    active = sh.active
+    while active:
+        sh.eval_p2p([buf.data_ptr()])
+        active = sh.step(buf)
+    r = sh.result()
+    buf.close()
+    np.testing.assert_array_equal(r.x, one.x)
