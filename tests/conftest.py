@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "c3s_nm"]
+NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "c3s_nm", "dd16_nm"]
 # SRPC coupling and gappy HR variants
 VARIANTS = ["tiny_nmg", "tiny_srpc", "tiny_lsg", "tiny_lss", "c0_nmg", "c0_srpc", "c0_lsg",
             "c0_lss"]
