@@ -612,26 +612,32 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // config 0 with the tensor-core Gram: 4 slots with the Jacobian rows in L2
   // 35.7-37.1 ms per 4096 mu, vs 41.5 ms for 2 slots with them in shared memory)
   // kernels with the KKT workspace in global memory only when nothing else fits.
-  // A soft cap keeps >= ~36 KB of L1 next to the slots when the slots fit
-  // under it: at config 3's layout (c3s, 120^2, 1024 mu) 2 slots with the
-  // Jacobian rows in shared memory (205 KB) take 33.3 ms, 2 slots with them
-  // in L2 (146 KB) 29.9 ms (1 slot at 122 KB: 27.8 ms); config 0's 4 slots
-  // at 187 KB stay the best there (36 ms vs 41-45 ms for 2 slots).
-  // DDNM_SMEM_SOFT_CAP overrides (bytes).
+  // Slot count: the largest G that fits, even G first (odd G takes the
+  // slower reduce-scatter path of the decoder sweep: c0_nmg 45.1 ms at 2
+  // slots vs 47.7 ms at 3).  Level: for that G, the lowest Jacobian-row level
+  // whose footprint stays under a soft cap of 192 KB (>= ~36 KB of L1 left),
+  // else the lowest level that fits: at config 3's layout (c3s, 120^2, 1024
+  // mu) 2 slots with the rows in shared memory (205 KB) take 33.3 ms and with
+  // them in L2 (146 KB) 29.9 ms; c0_srpc keeps 2 slots at 219 KB (216 ms vs
+  // 243 ms for 1 slot).  DDNM_SMEM_SOFT_CAP overrides (bytes).
   size_t soft_cap = std::min<size_t>(smem_cap, 192 * 1024);
   if (const char* sc = getenv("DDNM_SMEM_SOFT_CAP")) soft_cap = std::min<size_t>(smem_cap, (size_t)atoll(sc));
-  for (int cap_pass = 0; cap_pass < 2 && !kern; ++cap_pass) {
-    const size_t cap = cap_pass == 0 ? soft_cap : smem_cap;
-    for (int pass = 0; pass < 2 && !kern; ++pass) {
-      for (const auto& k : kernel_table()) {
-        if (k.ni != ni || k.ng != ng || k.kkt_global != (pass == 1)) continue;
-        if (slots > 0 && k.g != slots) continue;
-        for (int level = lvl_lo; level <= lvl_hi; ++level) {
-          if (footprint(k.g, level, k.kkt_global) > cap) continue;
-          if (!kern || k.g > kern->g) { kern = &k; kern_level = level; }
-          break;
-        }
-      }
+  auto better = [](int g, int best) {   // even before odd, then larger
+    if (best < 0) return true;
+    if ((g % 2 == 0) != (best % 2 == 0)) return g % 2 == 0;
+    return g > best;
+  };
+  for (int pass = 0; pass < 2 && !kern; ++pass) {
+    for (const auto& k : kernel_table()) {
+      if (k.ni != ni || k.ng != ng || k.kkt_global != (pass == 1)) continue;
+      if (slots > 0 && k.g != slots) continue;
+      int lv = -1;
+      for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
+        if (footprint(k.g, level, k.kkt_global) <= soft_cap) lv = level;
+      for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
+        if (footprint(k.g, level, k.kkt_global) <= smem_cap) lv = level;
+      if (lv < 0) continue;
+      if (better(k.g, kern ? kern->g : -1)) { kern = &k; kern_level = lv; }
     }
   }
   if (!kern) {
