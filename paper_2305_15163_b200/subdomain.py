@@ -109,12 +109,14 @@ class DeviceRoundEngine:
         arr = (C.c_void_p * len(peers))(*[C.c_void_p(p) for p in peers])
         N.check(N.lib().ddnm_dd_eval_p2p(self.h, arr, len(peers), rank, stride, self._stream()))
 
-    def step(self, gathered, nranks: int, bounds, stride: int) -> int:
+    def step(self, gathered, nranks: int, bounds, stride: int, count: bool = True):
+        """One round; returns the running-mu count, or None without a host
+        synchronisation when ``count`` is False."""
         bnd = (C.c_int32 * len(bounds))(*bounds)
         n = C.c_int32()
         N.check(N.lib().ddnm_dd_step(self.h, C.c_void_p(gathered.data_ptr()), nranks, bnd,
-                                     stride, self._stream(), C.byref(n)))
-        return int(n.value)
+                                     stride, self._stream(), C.byref(n) if count else None))
+        return int(n.value) if count else None
 
     def finish(self, mu):
         from .driver import BatchResult
@@ -156,7 +158,7 @@ class ShardedSolve:
         self.rounds = 0
         # every round evaluates one trial point per running mu; a solve takes
         # at most max_iter KKT steps of at most max_halvings + 1 trials each
-        self.max_rounds = 2 + cfg.max_iter * (cfg.max_halvings + 1)
+        self.max_rounds = 2 + cfg.max_iter * (cfg.max_halvings + 1) + CHECK
 
     def eval(self):
         self.eng.eval(self.packets, self.stride)
@@ -168,8 +170,13 @@ class ShardedSolve:
         addresses valid on this GPU) over peer memory."""
         self.eng.eval_p2p(peers, self.rank, self.stride)
 
-    def step(self, gathered) -> int:
-        self.active = self.eng.step(gathered, self.world, self.bounds, self.stride)
+    def step(self, gathered, count: bool = True) -> int:
+        """One SQP round.  ``count=False`` skips the host read of the running
+        count (no stream synchronisation); rounds after every mu finished do
+        nothing, so a caller may check only every few rounds."""
+        n = self.eng.step(gathered, self.world, self.bounds, self.stride, count)
+        if n is not None:
+            self.active = n
         self.rounds += 1
         if self.active and self.rounds >= self.max_rounds:
             raise RuntimeError("sharded solve did not terminate within the SQP round bound")
@@ -177,6 +184,9 @@ class ShardedSolve:
 
     def result(self):
         return self.eng.finish(self.mu)
+
+
+CHECK = 4   # rounds between host reads of the running-mu count
 
 
 def _all_gather(gathered, packets, world, group):
@@ -299,7 +309,9 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
                 packets = sh.eval()
                 if world > 1:
                     _all_gather(gathered, packets, world, group)
-            active = sh.step(gathered)
+            # the running count is read (one host sync) every CHECK rounds;
+            # rounds after the last mu finished are empty launches
+            active = sh.step(gathered, count=sh.rounds % CHECK == CHECK - 1)
     finally:
         if peers:
             peers.close()

@@ -158,7 +158,7 @@ class OracleRoundEngine:
         Br, Ri, Rg, cv, cj = np.split(flat[:self.plen[b]], np.cumsum(sizes)[:-1])
         return Br, Ri.reshape(r, ni), Rg.reshape(r, ng), cv, cj.reshape(nc, ng)
 
-    def step(self, gathered, nranks, bounds, stride):
+    def step(self, gathered, nranks, bounds, stride, count=True):
         g = gathered.numpy().reshape(nranks, self.B, stride)
         active = 0
         for k in range(self.B):
