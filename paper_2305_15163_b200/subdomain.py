@@ -24,6 +24,7 @@ an oracle-backed engine into the same host loop.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 
 import numpy as np
@@ -186,7 +187,7 @@ class ShardedSolve:
         return self.eng.finish(self.mu)
 
 
-CHECK = 4   # rounds between host reads of the running-mu count
+CHECK = int(os.environ.get("DDNM_DD_CHECK", "4"))   # rounds between host reads of the running-mu count
 
 
 def _all_gather(gathered, packets, world, group):
@@ -283,26 +284,35 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
     sh = ShardedSolve(instance, mu, cfg, rank, world, x0=x0, lam0=lam0, engine=engine,
                       device=device)
     active = sh.active
-    peers = own = None
+    peers, own = [], []
     if transport == "p2p" and world > 1:
-        # the exported buffer is its own allocation (IPC maps allocations)
-        own = _DevBuffer(world * sh.B * sh.stride * 8, sh.eng.dev.index)
-        gathered = own
-    else:
-        gathered = sh.packets if world == 1 else sh.eng.buffer(world * sh.B * sh.stride)
-    if transport == "p2p":
+        # two whole allocations per rank (IPC maps allocations), alternating
+        # by round: a peer's evaluation of round t + 1 may start while this
+        # rank's step of round t still reads; the all-reduce of round t + 1
+        # orders every step of round t before any store of round t + 2
         try:
-            peers = _PeerBuffers(gathered, rank, world, group) if world > 1 else None
+            for _ in range(2):
+                own.append(_DevBuffer(world * sh.B * sh.stride * 8, sh.eng.dev.index))
+                peers.append(_PeerBuffers(own[-1], rank, world, group))
         except Exception:
-            if own:
-                own.close()
+            for pb in peers:
+                pb.close()
+            for b in own:
+                b.close()
             raise
-        ptrs = peers.ptrs if peers else [gathered.data_ptr()]
-        flag = sh.eng.buffer(1)
+        bufs = own
+        ptrs = [pb.ptrs for pb in peers]
+    else:
+        g1 = sh.packets if world == 1 else sh.eng.buffer(world * sh.B * sh.stride)
+        bufs = [g1, g1]
+        ptrs = [[g1.data_ptr()]] * 2
+    flag = sh.eng.buffer(1) if transport == "p2p" and world > 1 else None
+    done = False
     try:
         while active:
+            gathered = bufs[sh.rounds % 2]
             if transport == "p2p":
-                sh.eval_p2p(ptrs)
+                sh.eval_p2p(ptrs[sh.rounds % 2])
                 if world > 1:
                     dist.all_reduce(flag, group=group)     # orders every rank's stores
             else:
@@ -312,14 +322,16 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
             # the running count is read (one host sync) every CHECK rounds;
             # rounds after the last mu finished are empty launches
             active = sh.step(gathered, count=sh.rounds % CHECK == CHECK - 1)
+        done = True
     finally:
-        if peers:
-            peers.close()
+        for pb in peers:
+            pb.close()
         if own:
-            torch_sync = getattr(sh.eng, "torch", None)
-            if torch_sync is not None:
-                torch_sync.cuda.current_stream(sh.eng.dev).synchronize()
-            own.close()
+            sh.eng.torch.cuda.current_stream(sh.eng.dev).synchronize()
+            if done:
+                dist.barrier(group=group)   # every rank unmapped before the frees
+            for b in own:
+                b.close()
     res = sh.result()
     if hasattr(res, "seconds"):
         res.seconds = time.perf_counter() - t0
