@@ -424,10 +424,17 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         world = dist.get_world_size() if dist else 1
+        from paper_2305_15163_b200.workmodel import eval_flops
+        evals, _ = ctx.counters()            # block evaluations of the last launch
+        fl = eval_flops(inst.arrays, inst.meta)
+        peak, _ = fp64_peak()
+        # evaluation flops only (the KKT count depends on which LU path runs)
+        eval_tf = evals / inst.n_blocks * fl["per_eval"] / (ms / 1e3) / 1e12
         out[key] = {"workload": desc, "batch_per_gpu": B, "solves_per_s": world * B / (ms / 1e3),
                     "ms_per_batch": ms, "mean_n_iter": float(it.float().mean().item()),
                     "status_counts": torch.bincount(st.long(), minlength=4).tolist(),
-                    "slots_per_cta": ctx.info.slots_per_cta}
+                    "slots_per_cta": ctx.info.slots_per_cta,
+                    "eval_tflops": round(eval_tf, 3), "eval_frac_of_fp64_peak": round(eval_tf / peak, 4)}
     return out
 
 
