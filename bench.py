@@ -3,16 +3,19 @@
 Workload (BASELINE configs[2]): the 60x60, 2x2-subdomain
 NM-ROM WFPC instance with collocation HR (n = (6, 4), n_C = 8, 180 rows per
 subdomain; artifacts trained by the reference, tests/golden/c0_nm_*), a
-batch of 4096 seeded mu per GPU, FP64.  One "step" = one complete batched
-``solve_rom`` (device RBF init + least-squares multipliers + SQP loop) over
-the whole batch.  Multi-GPU: the mu batch is sharded across ranks (weak
-scaling, 4096 mu per GPU, no data-path collective).
+fixed batch of 4096 seeded mu (seed 1000), FP64.  One "step" = one complete
+batched ``solve_rom`` (device RBF init + least-squares multipliers + SQP
+loop) over the whole batch.  Multi-GPU (BASELINE config 2: "then with the
+batch sharded across 2, 4 and 8 GPUs"): the 4096 mu are split into
+contiguous shards, one per rank, no data-path collective -- strong scaling;
+weak scaling (4096 mu per GPU) is reported beside it.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-``--impl reference`` times the CPU implementation of the same path (the
-numpy oracle port, oracle/ddnm_oracle.py, all host cores) on a bounded sample
-of the same workload.
+``--gpus N`` without a torchrun environment launches N ranks itself
+(torch.distributed.run, 127.0.0.1).  ``--impl reference`` times the CPU
+implementation of the same path (the numpy oracle port,
+oracle/ddnm_oracle.py, all host cores) on a bounded sample of the workload.
 """
 
 from __future__ import annotations
@@ -35,6 +38,8 @@ ARTIFACT = os.path.join(ROOT, "tests", "golden", "c0_nm_artifacts.npz")
 DD_ARTIFACT = os.path.join(ROOT, "tests", "golden", "dd16_nm_artifacts.npz")
 DD_BATCH = 256
 METRIC = "DD NM-ROM-HR SQP solves/sec (batched mu)"
+WORKLOAD = ("config2: 60x60 2x2 NM-ROM WFPC collocation HR, n=(6,4), n_C=8, 180 rows/sub, "
+            "band 8 shift 1, 4096 seeded mu (seed 1000)")
 UNIT = "solves/s"
 BATCH = 4096
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peaks.json")
@@ -149,10 +154,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded mu, reference-trained artifacts)",
-        "config": {"workload": "config2: 60x60 2x2 NM-ROM WFPC collocation HR, n=(6,4), n_C=8, 180 rows/sub",
-                   "batch_per_gpu": BATCH, "sample_per_step": sample},
+        "config": {"workload": WORKLOAD, "global_batch": BATCH},
+        "run": {"sample_per_step": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,8 +188,11 @@ def run_gpu(args):
     ctx = inst.context(local, args.slots)
     info = ctx.info
     cfg = P.SqpConfig()
-    B = BATCH
-    mu_h = P.seeded_parameters(B, seed=1000 + rank)
+    # strong scaling: the fixed 4096-mu batch, contiguous shard per rank
+    mu_all = P.seeded_parameters(BATCH, seed=1000)
+    lo, hi = rank * BATCH // world, (rank + 1) * BATCH // world
+    B = hi - lo
+    mu_h = np.ascontiguousarray(mu_all[lo:hi])
     mu_d = torch.from_numpy(mu_h).to(dev)
     nD, nC = info.n_primal, info.n_mult
     outs = {
@@ -195,13 +203,16 @@ def run_gpu(args):
         "status": torch.empty(B, dtype=torch.int32, device=dev),
         "merit": torch.empty(B, dtype=torch.float64, device=dev),
     }
-    so = N.SolveOut()
-    so.x = C.cast(C.c_void_p(outs["x"].data_ptr()), C.POINTER(C.c_double))
-    so.lam = C.cast(C.c_void_p(outs["lam"].data_ptr()), C.POINTER(C.c_double))
-    so.n_iter = C.cast(C.c_void_p(outs["n_iter"].data_ptr()), C.POINTER(C.c_int32))
-    so.n_evals = C.cast(C.c_void_p(outs["n_evals"].data_ptr()), C.POINTER(C.c_int32))
-    so.status = C.cast(C.c_void_p(outs["status"].data_ptr()), C.POINTER(C.c_int32))
-    so.merit = C.cast(C.c_void_p(outs["merit"].data_ptr()), C.POINTER(C.c_double))
+    def so_for(o):
+        so = N.SolveOut()
+        so.x = C.cast(C.c_void_p(o["x"].data_ptr()), C.POINTER(C.c_double))
+        so.lam = C.cast(C.c_void_p(o["lam"].data_ptr()), C.POINTER(C.c_double))
+        so.n_iter = C.cast(C.c_void_p(o["n_iter"].data_ptr()), C.POINTER(C.c_int32))
+        so.n_evals = C.cast(C.c_void_p(o["n_evals"].data_ptr()), C.POINTER(C.c_int32))
+        so.status = C.cast(C.c_void_p(o["status"].data_ptr()), C.POINTER(C.c_int32))
+        so.merit = C.cast(C.c_void_p(o["merit"].data_ptr()), C.POINTER(C.c_double))
+        return so
+    so = so_for(outs)
     cs = _cfg_struct(cfg)
     stream = torch.cuda.Stream(dev)          # explicit (non-default) stream: events see the kernel
     L = N.lib()
@@ -243,7 +254,19 @@ def run_gpu(args):
         total_ms = float(t.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    value = world * B * args.steps / (total_ms / 1e3)
+    value = BATCH * args.steps / (total_ms / 1e3)
+
+    # parity of the timed batch (last timed step) against CPU goldens of its
+    # first mu (tests/golden/bench_c0_parity.npz: oracle and reference
+    # solve_rom on the same seed-1000 parameters, tools/make_bench_golden.py)
+    parity = None
+    if rank == 0:
+        parity = bench_parity(outs, lo)
+
+    # weak scaling beside it: 4096 mu per GPU (seed 1000 + rank)
+    weak = None
+    if not args.no_weak:
+        weak = weak_scaling(P, N, C, torch, dist, ctx, cs, so_for, dev, stream, flush, rank, world, args)
 
     # full decode of the batch's solutions (RomInstance.decode, driver.py:148-152):
     # reported beside the solve, not part of `value`
@@ -295,8 +318,8 @@ def run_gpu(args):
         e2e_t = float(t.item())
     K1 = cfg.max_iter + 1
     d2h = B * (nD * 8 * 2 + nC * 8 * 2 + 4 * 4 + 8 * 2 + K1 * 8 * 2 + cfg.max_iter * 8)
-    e2e = {"value": world * B / e2e_t, "unit": UNIT, "h2d_bytes_per_step": B * 2 * 8,
-           "d2h_bytes_per_step": d2h}
+    e2e = {"value": BATCH / e2e_t, "unit": UNIT, "h2d_bytes_per_step": BATCH * 2 * 8,
+           "d2h_bytes_per_step": d2h * world}
 
     sub = None
     if not args.no_subdomain:
@@ -345,12 +368,12 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded mu; artifacts trained by the reference on the 6x6 mu grid)",
-        "config": {"workload": "config2: 60x60 2x2 NM-ROM WFPC collocation HR, n=(6,4), n_C=8, "
-                               "180 rows/sub, band 8 shift 1",
-                   "batch_per_gpu": B, "global_batch": world * B,
-                   "parallelism": f"mu-shard x{world}", "l2": "flushed (256 MB write) between timed steps",
+        "config": {"workload": WORKLOAD, "global_batch": BATCH},
+        "run": {"batch_per_gpu": B,
+                   "parallelism": f"mu-shard x{world} (contiguous shards of the fixed batch)",
+                   "l2": "flushed (256 MB write) between timed steps",
                    "slots_per_cta": info.slots_per_cta, "ctas": info.ctas,
                    "mean_n_iter": float(n_iter.mean()), "status_counts": np.bincount(status, minlength=4).tolist()},
         "roofline": roof,
@@ -358,6 +381,8 @@ def run_gpu(args):
         "e2e": e2e,
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
+        "parity": parity,
+        "weak_scaling": weak,
         "decode": dec,
         "subdomain": sub,
         "other_configs": others,
@@ -368,7 +393,82 @@ def run_gpu(args):
     return 0
 
 
-# the other BASELINE configs on one GPU (per rank, mu-sharded like the headline)
+PARITY_FILE = os.path.join(ROOT, "tests", "golden", "bench_c0_parity.npz")
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def bench_parity(outs, lo):
+    """Rank 0's shard starts at mu `lo` = 0: compare its first mu with the
+    CPU goldens of the same seed-1000 parameters (north-star gate: x, lam to
+    1e-9 relative; identical iteration counts)."""
+    if not os.path.exists(PARITY_FILE) or lo != 0:
+        return None
+    z = dict(np.load(PARITY_FILE))
+    n = min(int(z["x"].shape[0]), outs["x"].shape[0])
+    x = outs["x"][:n].cpu().numpy()
+    lam = outs["lam"][:n].cpu().numpy()
+    it = outs["n_iter"][:n].cpu().numpy()
+    out = {"sample": n, "of_batch": "first mu of the timed seed-1000 batch", "tol": 1e-9}
+    for who in ("oracle", "reference"):
+        if f"{who}_x" not in z:
+            continue
+        ex = max(_rel(x[k], z[f"{who}_x"][k]) for k in range(n))
+        el = max(_rel(lam[k], z[f"{who}_lam"][k]) for k in range(n))
+        eq = int(np.sum(it == z[f"{who}_n_iter"][:n]))
+        out[who] = {"max_rel_x": ex, "max_rel_lam": el, "n_iter_equal": eq,
+                    "pass": bool(ex <= 1e-9 and el <= 1e-9)}
+    if "robust" in z:
+        rb = z["robust"][:n].astype(bool)
+        out["robust_mu"] = int(rb.sum())
+        out["n_iter_equal_on_robust"] = int(np.sum((it == z["oracle_n_iter"][:n])[rb]))
+    return out
+
+
+def weak_scaling(P, N, C, torch, dist, ctx, cs, so_for, dev, stream, flush, rank, world, args):
+    """4096 mu per GPU (seed 1000 + rank): the weak-scaling extra."""
+    B = BATCH
+    mu = torch.from_numpy(P.seeded_parameters(B, seed=1000 + rank)).to(dev)
+    nD, nC = ctx.info.n_primal, ctx.info.n_mult
+    o = {"x": torch.empty((B, nD), dtype=torch.float64, device=dev),
+         "lam": torch.empty((B, nC), dtype=torch.float64, device=dev),
+         "n_iter": torch.empty(B, dtype=torch.int32, device=dev),
+         "n_evals": torch.empty(B, dtype=torch.int32, device=dev),
+         "status": torch.empty(B, dtype=torch.int32, device=dev),
+         "merit": torch.empty(B, dtype=torch.float64, device=dev)}
+    so = so_for(o)
+
+    def launch():
+        N.check(N.lib().ddnm_solve_batch_device(ctx.h, B, C.c_void_p(mu.data_ptr()), None, None,
+                                                C.byref(cs), C.byref(so),
+                                                C.c_void_p(stream.cuda_stream)))
+    launch()
+    times = []
+    for _ in range(3):
+        flush.fill_(4.0)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launch()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"batch_per_gpu": B, "value": world * B / (ms / 1e3), "unit": UNIT, "ms_per_batch": ms,
+            "scaling": "weak"}
+
+
+# the other BASELINE configs (strong scaling: each config's fixed batch, sharded)
 OTHER_CONFIGS = [
     ("config1_ls", "c0_ls", 4096, "config1: 60x60 2x2 LS-ROM WFPC collocation HR, n=(20,8), "
                                   "n_C=16, 180 rows/sub"),
@@ -376,6 +476,10 @@ OTHER_CONFIGS = [
                                            "n=(8,5), n_C=10, 2% collocation rows (144/sub)"),
     ("config4_layout_dd16", "dd16_nm", 256, "config 4's layout at 60x60: 4x4 NM-ROM, "
                                             "n=(8,5), n_C=40, 45 rows/sub (persistent kernel)"),
+    ("config3", "c3_nm", 1024, "config3: 480x480 2x2 NM-ROM WFPC, n=(8,5), n_C=10, 2% collocation "
+                               "rows (2304/sub), blocks as evaluation units"),
+    ("config4", "c4_nm", 256, "config4: 960x960 4x4 NM-ROM WFPC, n=(8,5), n_C=40, 2% collocation "
+                              "rows (2304/sub), blocks as evaluation units"),
 ]
 
 
@@ -390,7 +494,11 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
         inst = P.RomInstance.load(path)
         ctx = inst.context(dev.index)
         rank = dist.get_rank() if dist else 0
-        mu = torch.from_numpy(P.seeded_parameters(B, seed=3000 + rank)).to(dev)
+        world = dist.get_world_size() if dist else 1
+        Bt = B
+        lo, hi = rank * Bt // world, (rank + 1) * Bt // world
+        B = hi - lo
+        mu = torch.from_numpy(np.ascontiguousarray(P.seeded_parameters(Bt, seed=3000)[lo:hi])).to(dev)
         nD, nC = inst.n_primal, inst.n_mult
         x = torch.empty((B, nD), dtype=torch.float64, device=dev)
         lam = torch.empty((B, nC), dtype=torch.float64, device=dev)
@@ -423,17 +531,21 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        world = dist.get_world_size() if dist else 1
         from paper_2305_15163_b200.workmodel import eval_flops
         evals, _ = ctx.counters()            # block evaluations of the last launch
         fl = eval_flops(inst.arrays, inst.meta)
         peak, _ = fp64_peak()
         # evaluation flops only (the KKT count depends on which LU path runs)
-        eval_tf = evals / inst.n_blocks * fl["per_eval"] / (ms / 1e3) / 1e12
-        out[key] = {"workload": desc, "batch_per_gpu": B, "solves_per_s": world * B / (ms / 1e3),
+        eval_tf = evals / inst.n_blocks * fl["per_eval"] / (ms / 1e3) / 1e12 / world
+        if dist:
+            ev_t = torch.tensor([float(evals)], device=dev, dtype=torch.float64)
+            dist.all_reduce(ev_t)
+            evals = int(ev_t.item())
+        out[key] = {"workload": desc, "batch": Bt, "scaling": "strong", "batch_per_gpu": B,
+                    "solves_per_s": Bt / (ms / 1e3),
                     "ms_per_batch": ms, "mean_n_iter": float(it.float().mean().item()),
                     "status_counts": torch.bincount(st.long(), minlength=4).tolist(),
-                    "slots_per_cta": ctx.info.slots_per_cta,
+                    "slots_per_cta": ctx.info.slots_per_cta, "eval_units": ctx.info.eval_units,
                     "eval_tflops": round(eval_tf, 3), "eval_frac_of_fp64_peak": round(eval_tf / peak, 4)}
     return out
 
@@ -492,7 +604,27 @@ def main():
     ap.add_argument("--no-subdomain", action="store_true",
                     help="skip the extra measurements (subdomain-sharded dd16, other configs)")
     ap.add_argument("--slots", type=int, default=0, help="mu slots per CTA (0 = largest that fits)")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling extra")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch the ranks ourselves (the driver may also
+        # launch us under torchrun, then WORLD_SIZE is set)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")            # init lines (ranks, transports) ...
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr, not in the JSON stream
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd, env=env)
+    if "WORLD_SIZE" in os.environ:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

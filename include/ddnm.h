@@ -153,6 +153,11 @@ typedef struct {
   int32_t ctas;              /* persistent grid size */
   int32_t smem_bytes;        /* dynamic shared memory per CTA */
   int32_t device;
+  int32_t eval_units;        /* evaluation units the blocks are split into (0: whole
+                                blocks); blocks too large for one CTA (configs 3/4)
+                                are evaluated as chunks of their sampled rows plus
+                                chunks of interface outputs; DDNM_UNIT_ROWS=<rows>
+                                forces the split (tests) */
 } ddnm_info;
 
 /* Per-mu solve results; every pointer may be NULL except x and lam. */
@@ -308,8 +313,14 @@ int ddnm_dd_step(ddnm_dd* dd, const double* d_gathered, int32_t nranks,
  * packets straight into every rank's gathered buffer, at
  * peers[r] + (rank * B + mu) * pk_stride, over NVLink (peer stores; peers[r]
  * valid on this device: same-process peer access or ddnm_ipc_open_handle).
- * The caller then needs only a cross-rank barrier ordered on `stream` (e.g. a
- * one-element NCCL all-reduce) before ddnm_dd_step on its own buffer. */
+ * Protocol: every rank owns TWO gathered buffers and round t uses buffer
+ * t % 2 on all ranks; after ddnm_dd_eval_p2p of round t, a cross-rank barrier
+ * ordered on `stream` (e.g. a one-element NCCL all-reduce), then
+ * ddnm_dd_step on this rank's buffer t % 2.  A faster peer's stores of round
+ * t + 1 go to the other buffer, and the barrier of round t + 1 orders every
+ * rank's step t before any store of round t + 2 into buffer t % 2.  With one
+ * buffer the protocol is racy: a peer's round-(t+1) stores could overwrite
+ * packets this rank's step t is still reading. */
 int ddnm_dd_eval_p2p(ddnm_dd* dd, double* const* peers, int32_t nranks, int32_t rank,
                      int64_t pk_stride, void* stream);
 

@@ -7,9 +7,10 @@ parameters mu and executed by hand-written sm_100a CUDA kernels behind the C
 ABI in ``include/ddnm.h`` (``libddnm.so``).  There is no CPU fallback.
 """
 
-from .burgers import A_RANGE, LAM_RANGE, Grid2D, ParameterPoint, seeded_parameters
-from .driver import (BatchResult, DecodeBatch, EvalBatch, RomInstance, RomSolution,
-                     build_problem, decode_batch, eval_gradients_batch, init_guess,
+from .burgers import (A_RANGE, LAM_RANGE, FomOperators, Grid2D, ParameterPoint, assemble,
+                      seeded_parameters)
+from .driver import (BatchResult, BenchmarkRecord, DecodeBatch, EvalBatch, RomInstance,
+                     RomSolution, build_problem, decode_batch, eval_gradients_batch, init_guess,
                      solve_rom, solve_rom_batch)
 from .errors import ConvergenceError, FormatError, SingularityError
 from .subdomain import (ShardedSolve, block_bounds,
@@ -19,8 +20,9 @@ from .sqp import SqpBlock, SqpConfig, SqpProblem, SqpResult, iterate
 __version__ = "0.1.0"
 
 __all__ = [
-    "A_RANGE", "LAM_RANGE", "Grid2D", "ParameterPoint", "seeded_parameters",
-    "BatchResult", "DecodeBatch", "EvalBatch", "RomInstance", "RomSolution",
+    "A_RANGE", "LAM_RANGE", "FomOperators", "Grid2D", "ParameterPoint", "assemble",
+    "seeded_parameters",
+    "BatchResult", "BenchmarkRecord", "DecodeBatch", "EvalBatch", "RomInstance", "RomSolution",
     "build_problem", "decode_batch",
     "eval_gradients_batch", "init_guess", "solve_rom", "solve_rom_batch",
     "ConvergenceError", "FormatError", "SingularityError",

@@ -74,7 +74,7 @@ class Info(C.Structure):
         "n_primal", "n_mult", "n_blocks", "total_rows", "total_out_rows", "total_out_R",
         "total_int_out", "total_gam_out",
         "total_R", "total_cjac", "total_int_J", "total_gam_J", "slots_per_cta", "ctas",
-        "smem_bytes", "device")]
+        "smem_bytes", "device", "eval_units")]
 
 
 class SolveOut(C.Structure):

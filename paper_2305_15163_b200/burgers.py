@@ -78,3 +78,22 @@ def seeded_parameters(B: int, seed: int = 0) -> np.ndarray:
     a = rng.uniform(A_RANGE[0], A_RANGE[1], B)
     lam = rng.uniform(LAM_RANGE[0], LAM_RANGE[1], B)
     return np.stack([a, lam], axis=1)
+
+
+@dataclass(frozen=True, eq=False)
+class FomOperators:
+    """``ddrom.burgers.FomOperators`` (burgers.py:143-157) for the online
+    path: the parameter and grid only.  The device evaluates the boundary
+    vectors (burgers.py:188-210) at the sampled rows itself and never
+    materialises the global sparse operators, so ``build_problem`` /
+    ``init_guess`` read just ``param`` -- a reference ``FomOperators`` is
+    accepted wherever this one is."""
+
+    grid: Grid2D
+    param: ParameterPoint
+
+
+def assemble(grid: Grid2D, p: ParameterPoint) -> FomOperators:
+    """``ddrom.burgers.assemble`` (burgers.py:174-213) signature; see
+    :class:`FomOperators` for what is kept."""
+    return FomOperators(grid=grid, param=p)

@@ -132,6 +132,7 @@ struct ddnm_ctx {
   std::map<std::string, std::pair<void*, size_t>> io;
   // full decode (ddnm_ctx_set_full_decoders)
   int map_kind = 0;
+  int n_units = 0;            // evaluation units (0: blocks evaluated whole)
   DecodeJob* d_jobs = nullptr;
   int state_len = 0, dec_max_hidden = 0, dec_mu_tile = 0;
 };
@@ -390,6 +391,203 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, int ac
   return 0;
 }
 
+// ---- evaluation units (large blocks) --------------------------------------
+// A block whose subnet, rows or interface decoder would not fit one CTA's
+// shared memory next to a few slots is evaluated as a sequence of units:
+//  * row units: a contiguous chunk of the block's sampled rows with the
+//    interior subnet restricted to the outputs those rows reference and the
+//    interface decoder restricted to the interface outputs they reference
+//    (extract_subnet, hyper.py:200-222, applied once more: every kept output
+//    is bitwise the full subnet's; test_hyper.py:194-201 pins that invariant);
+//    each adds its rows' Gram contribution R^T R, R^T r, r^T r to the block;
+//  * constraint units: a chunk of the full interface decoder's outputs and
+//    the matching columns of C A_i, adding C A_i g / C A_i J over the chunk
+//    (driver.py:371-373).
+// Sums over rows / interface outputs are then taken chunk by chunk (unit
+// order, deterministic) instead of in one pass: same terms, rounding only.
+
+struct HostDecoder {          // owning copy of a (restricted) decoder
+  std::vector<double> W1, b1, data, scale, shift;
+  std::vector<int64_t> indptr, indices;
+  ddnm_decoder d{};
+  void finish() {
+    d.n_out = (int32_t)scale.size();
+    d.n_hidden = (int32_t)b1.size();
+    d.W1 = W1.empty() ? nullptr : W1.data();
+    d.b1 = b1.data(); d.indptr = indptr.data(); d.indices = indices.data(); d.data = data.data();
+    d.scale = scale.data(); d.shift = shift.data();
+    if (d.n_out == 0) { static const double z = 0.0; d.W1 = &z; d.n_hidden = 0; }
+  }
+};
+
+// the decoder restricted to the outputs `outs` (in that order): hidden units
+// are the sorted union of their entries, entries keep storage order
+void restrict_decoder(const ddnm_decoder& h, int lat, const std::vector<int>& outs, HostDecoder& r) {
+  std::vector<int> hid;
+  for (int o : outs)
+    for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e) hid.push_back((int)h.indices[e]);
+  std::sort(hid.begin(), hid.end());
+  hid.erase(std::unique(hid.begin(), hid.end()), hid.end());
+  std::map<int, int> pos;
+  for (size_t k = 0; k < hid.size(); ++k) pos[hid[k]] = (int)k;
+  r.W1.resize(hid.size() * lat);
+  r.b1.resize(hid.size());
+  for (size_t k = 0; k < hid.size(); ++k) {
+    for (int d = 0; d < lat; ++d) r.W1[k * lat + d] = h.W1[(size_t)hid[k] * lat + d];
+    r.b1[k] = h.b1[hid[k]];
+  }
+  r.indptr.assign(1, 0);
+  r.indices.clear(); r.data.clear(); r.scale.clear(); r.shift.clear();
+  for (int o : outs) {
+    for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e) {
+      r.indices.push_back(pos[(int)h.indices[e]]);
+      r.data.push_back(h.data[e]);
+    }
+    r.indptr.push_back((int64_t)r.indices.size());
+    r.scale.push_back(h.scale[o]);
+    r.shift.push_back(h.shift[o]);
+  }
+  r.finish();
+}
+
+struct HostUnit {
+  HostDecoder in, ga;
+  std::vector<int64_t> rows, cols, gio;
+  std::vector<double> CA;
+  std::vector<int> iout_map, gout_map, row_map;
+  ddnm_block blk{};
+  int flags = 0;
+};
+
+struct UnitLimits { int rows, hidden, outs, grefs, gchunk; };
+
+// split block k into units (row chunks, then interface-output chunks)
+int split_block(const ddnm_artifacts* a, const ddnm_block& k, const HostRows& hr,
+                const UnitLimits& L, std::vector<HostUnit>& out) {
+  const int nr = k.n_rows, nio = k.n_io;
+  const ddnm_decoder& di = k.interior;
+  std::vector<int> omark(std::max(nio, 1), 0), hmark(std::max(di.n_hidden, 1), 0),
+      gmark(std::max(k.n_gio, 1), 0);
+  int stamp = 0;
+  // rows in node order (the u and v rows of a node and the rows of
+  // neighbouring nodes reference the same outputs and hidden units)
+  const int64_t nn = (int64_t)a->nx * a->ny;
+  std::vector<int> order(nr);
+  for (int r = 0; r < nr; ++r) order[r] = r;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    const int64_t px = k.res_rows[x] % nn, py = k.res_rows[y] % nn;
+    if (px != py) return px < py;
+    return k.res_rows[x] < k.res_rows[y];
+  });
+  int r0 = 0;
+  bool first_rows = true;
+  auto refs = [&](int r, std::vector<int>& io, std::vector<int>& gi) {
+    io.clear(); gi.clear();
+    for (int e = 0; e < hr.nent[r]; ++e) {
+      const int c = hr.col[(size_t)e * nr + r];
+      if (c < nio) io.push_back(c); else gi.push_back(c - nio);
+    }
+  };
+  auto flush = [&](int r1) {
+    if (r1 <= r0) return;
+    out.emplace_back();
+    HostUnit& u = out.back();
+    std::vector<int> io, gi, uo, ug;
+    for (int q = r0; q < r1; ++q) {
+      refs(order[q], io, gi);
+      uo.insert(uo.end(), io.begin(), io.end());
+      ug.insert(ug.end(), gi.begin(), gi.end());
+    }
+    std::sort(uo.begin(), uo.end()); uo.erase(std::unique(uo.begin(), uo.end()), uo.end());
+    std::sort(ug.begin(), ug.end()); ug.erase(std::unique(ug.begin(), ug.end()), ug.end());
+    restrict_decoder(k.interior, k.n_int, uo, u.in);
+    std::vector<int> gouts;
+    for (int g : ug) gouts.push_back((int)k.gio[g]);
+    restrict_decoder(k.interface, k.n_gam, gouts, u.ga);
+    for (int q = r0; q < r1; ++q) {
+      u.rows.push_back(k.res_rows[order[q]]);
+      u.row_map.push_back(order[q]);
+    }
+    for (int o : uo) u.cols.push_back(k.cols[o]);
+    for (int g : ug) u.cols.push_back(k.cols[nio + g]);
+    for (size_t g = 0; g < ug.size(); ++g) u.gio.push_back((int64_t)g);
+    u.iout_map = uo;
+    u.flags = UF_ROWS | (first_rows ? 0 : UF_ACC_GRAM);
+    first_rows = false;
+    r0 = r1;
+  };
+  int n_o = 0, n_h = 0, n_g = 0;
+  ++stamp;
+  std::vector<int> io, gi;
+  for (int q = 0; q < nr; ++q) {
+    const int r = order[q];
+    refs(r, io, gi);
+    // what this row would add to the current unit
+    int add_o = 0, add_h = 0, add_g = 0;
+    const int st2 = stamp + 1;
+    std::vector<int> newh;
+    for (int o : io) {
+      if (omark[o] == stamp || omark[o] == st2) continue;
+      omark[o] = st2; ++add_o;
+      for (int64_t e = di.indptr[o]; e < di.indptr[o + 1]; ++e) {
+        const int h = (int)di.indices[e];
+        if (hmark[h] == stamp || hmark[h] == st2) continue;
+        hmark[h] = st2; ++add_h; newh.push_back(h);
+      }
+    }
+    for (int g : gi) if (gmark[g] != stamp && gmark[g] != st2) { gmark[g] = st2; ++add_g; }
+    const bool over = q > r0 && (q - r0 + 1 > L.rows || n_o + add_o > L.outs ||
+                                 n_h + add_h > L.hidden || n_g + add_g > L.grefs);
+    if (over) {
+      flush(q);
+      stamp += 2;
+      n_o = n_h = n_g = 0;
+      --q;          // re-add this row to the fresh unit
+      continue;
+    }
+    // commit the row
+    for (int o : io) if (omark[o] == st2) omark[o] = stamp;
+    for (int h : newh) hmark[h] = stamp;
+    for (int g : gi) if (gmark[g] == st2) gmark[g] = stamp;
+    n_o += add_o; n_h += add_h; n_g += add_g;
+  }
+  flush(nr);
+  // constraint units: chunks of the full interface decoder (WFPC)
+  const int ngo = k.interface.n_out;
+  bool first_con = true;
+  for (int o0 = 0; o0 < ngo; o0 += L.gchunk) {
+    const int o1 = std::min(ngo, o0 + L.gchunk);
+    out.emplace_back();
+    HostUnit& u = out.back();
+    std::vector<int> gouts;
+    for (int o = o0; o < o1; ++o) gouts.push_back(o);
+    restrict_decoder(k.interface, k.n_gam, gouts, u.ga);
+    std::vector<int> none;
+    restrict_decoder(k.interior, k.n_int, none, u.in);
+    u.gout_map = gouts;
+    u.CA.resize((size_t)a->n_c * (o1 - o0));
+    for (int c = 0; c < a->n_c; ++c)
+      for (int o = o0; o < o1; ++o) u.CA[(size_t)c * (o1 - o0) + (o - o0)] = k.CA[(size_t)c * ngo + o];
+    u.flags = UF_CON | (first_con ? 0 : UF_ACC_CON);
+    first_con = false;
+  }
+  for (HostUnit& u : out) {
+    ddnm_block& b = u.blk;
+    b.n_int = k.n_int; b.n_gam = k.n_gam;
+    b.interior = u.in.d; b.interface = u.ga.d;
+    b.n_rows = (int32_t)u.rows.size();
+    b.res_rows = u.rows.empty() ? nullptr : u.rows.data();
+    b.n_cols = (int32_t)u.cols.size();
+    b.cols = u.cols.empty() ? nullptr : u.cols.data();
+    b.n_io = u.in.d.n_out;
+    b.n_gio = (int32_t)u.gio.size();
+    b.gio = u.gio.empty() ? nullptr : u.gio.data();
+    b.CA = u.CA.empty() ? nullptr : u.CA.data();
+    b.n_basis = 0; b.weights = nullptr;
+  }
+  return 0;
+}
+
 int64_t nnz_of(const ddnm_decoder& d, int kind) {
   return kind == DDNM_MAP_AUTOENCODER ? d.indptr[d.n_out] : 0;
 }
@@ -467,20 +665,21 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   int xoff = 0, row_off = 0, iout = 0, gout = 0, Roff = 0, cjoff = 0, ijoff = 0, gjoff = 0, eboff = 0;
   int max_nh = 0, max_io = 0, max_gam = 0, max_rows = 0, max_nbz = 0, out_off = 0, outR_off = 0;
   std::vector<HostWindows> hwin(2 * a->n_blocks);
-  for (int b = 0; b < P.nb; ++b) {
-    const ddnm_block& k = a->blocks[b];
-    BlockDev& B = P.blk[b];
+  // device tables of one block (or evaluation unit): decoders, stencil rows,
+  // gio, constraint matrix, gappy weights
+  auto setup = [&](const ddnm_block& k, BlockDev& B, HostWindows* hw2, HostRows& hr) -> int {
+    int rc2;
+    HostWindows tmp[2];
     B.ni = ni; B.ng = ng; B.w = W;
     B.nrows = k.n_rows; B.n_io = k.n_io; B.n_gio = k.n_gio;
-    B.xoff = xoff; B.row_off = row_off; B.iout_off = iout; B.gout_off = gout; B.R_off = Roff;
-    B.cjac_off = cjoff; B.intJ_off = ijoff; B.gamJ_off = gjoff; B.eb_off = eboff;
-    if ((rc = upload_decoder(c, k.interior, ni, a->map_kind, a->activation, B.in, hwin[2 * b])))
-      return bail(rc);
-    if ((rc = upload_decoder(c, k.interface, ng, a->map_kind, a->gam_activation, B.ga,
-                             hwin[2 * b + 1])))
-      return bail(rc);
-    HostRows hr;
-    if ((rc = build_stencil(a, k, hr))) return bail(rc);
+    B.uflags = UF_ROWS | UF_CON;
+    B.iout_map = nullptr; B.gout_map = nullptr; B.row_map = nullptr;
+    if ((rc2 = upload_decoder(c, k.interior, ni, a->map_kind, a->activation, B.in, hw2 ? hw2[0] : tmp[0])))
+      return rc2;
+    if ((rc2 = upload_decoder(c, k.interface, ng, a->map_kind, a->gam_activation, B.ga,
+                              hw2 ? hw2[1] : tmp[1])))
+      return rc2;
+    if ((rc2 = build_stencil(a, k, hr))) return rc2;
     StRows& R = B.rows;
     if ((rc = upload(c, hr.gu.data(), hr.gu.size(), const_cast<int**>(&R.gu))) ||
         (rc = upload(c, hr.gv.data(), hr.gv.size(), const_cast<int**>(&R.gv))) ||
@@ -495,15 +694,26 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
         (rc = upload(c, hr.cdc.data(), hr.cdc.size(), const_cast<double**>(&R.cdc))) ||
         (rc = upload(c, hr.xc.data(), hr.xc.size(), const_cast<double**>(&R.xc))) ||
         (rc = upload(c, hr.yc.data(), hr.yc.size(), const_cast<double**>(&R.yc))))
-      return bail(rc);
-    if ((rc = upload_i32(c, k.gio, (size_t)k.n_gio, const_cast<int**>(&B.gio)))) return bail(rc);
+      return rc;
+    if ((rc = upload_i32(c, k.gio, (size_t)k.n_gio, const_cast<int**>(&B.gio)))) return rc;
     const size_t ca_cols = a->constraint_mode == DDNM_CON_SRPC ? (size_t)ng : (size_t)k.interface.n_out;
-    if ((rc = upload(c, k.CA, (size_t)P.n_C * ca_cols, const_cast<double**>(&B.CA)))) return bail(rc);
+    B.CA = nullptr;
+    if (k.CA && (rc = upload(c, k.CA, (size_t)P.n_C * ca_cols, const_cast<double**>(&B.CA)))) return rc;
     B.nbz = k.n_basis;
     B.wts = nullptr;
     if (k.n_basis > 0 &&
         (rc = upload(c, k.weights, (size_t)k.n_basis * k.n_rows, const_cast<double**>(&B.wts))))
-      return bail(rc);
+      return rc;
+    return 0;
+  };
+  std::vector<HostRows> hrows(a->n_blocks);
+  for (int b = 0; b < P.nb; ++b) {
+    const ddnm_block& k = a->blocks[b];
+    BlockDev& B = P.blk[b];
+    if ((rc = setup(k, B, &hwin[2 * b], hrows[b]))) return bail(rc);
+    B.real = b;
+    B.xoff = xoff; B.row_off = row_off; B.iout_off = iout; B.gout_off = gout; B.R_off = Roff;
+    B.cjac_off = cjoff; B.intJ_off = ijoff; B.gamJ_off = gjoff; B.eb_off = eboff;
     B.out_off = out_off;
     B.outR_off = outR_off;
     out_off += k.n_basis > 0 ? k.n_basis : k.n_rows;
@@ -516,6 +726,67 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     max_io = std::max(max_io, k.n_io);
     max_gam = std::max(max_gam, k.interface.n_out);
     max_rows = std::max(max_rows, k.n_rows);
+  }
+  // evaluation units for blocks too large for one CTA (configs 3/4): every
+  // block becomes units when any block needs splitting (DDNM_UNIT_ROWS forces
+  // it, for tests on small instances)
+  {
+    UnitLimits L{256, 1536, 512, 128, 256};
+    const char* ur = getenv("DDNM_UNIT_ROWS");
+    if (ur) L.rows = std::max(1, atoi(ur));
+    if (const char* ug = getenv("DDNM_UNIT_GAM")) L.gchunk = std::max(8, atoi(ug));
+    bool need = false;
+    for (int b = 0; b < P.nb; ++b) {
+      const ddnm_block& k = a->blocks[b];
+      if (k.interior.n_hidden > 2048 || k.n_io > 512 || k.n_rows > 256 || k.interface.n_out > 512) need = true;
+    }
+    const bool can = a->map_kind == DDNM_MAP_AUTOENCODER && a->constraint_mode == DDNM_CON_WFPC;
+    bool nogappy = true;
+    for (int b = 0; b < P.nb; ++b) if (a->blocks[b].n_basis > 0) nogappy = false;
+    if ((need || ur) && can && nogappy && !getenv("DDNM_NO_UNITS")) {
+      std::vector<BlockDev> units;
+      max_nh = max_io = max_gam = max_rows = 0;
+      for (int b = 0; b < P.nb; ++b) {
+        const ddnm_block& k = a->blocks[b];
+        const BlockDev& RB = P.blk[b];
+        P.u_bnd[b] = (int)units.size();
+        std::vector<HostUnit> hu;
+        if ((rc = split_block(a, k, hrows[b], L, hu))) return bail(rc);
+        for (HostUnit& u : hu) {
+          BlockDev U;
+          std::memset(&U, 0, sizeof U);
+          HostRows uhr;
+          if ((rc = setup(u.blk, U, nullptr, uhr))) return bail(rc);
+          U.uflags = u.flags;
+          U.real = b;
+          U.xoff = RB.xoff; U.eb_off = RB.eb_off; U.cjac_off = RB.cjac_off;
+          U.iout_off = RB.iout_off; U.intJ_off = RB.intJ_off;
+          U.gout_off = RB.gout_off; U.gamJ_off = RB.gamJ_off;
+          U.row_off = RB.row_off;
+          U.out_off = RB.out_off;
+          U.outR_off = RB.outR_off;
+          U.R_off = RB.R_off;
+          if (!u.row_map.empty() &&
+              (rc = upload(c, u.row_map.data(), u.row_map.size(), const_cast<int**>(&U.row_map))))
+            return bail(rc);
+          if (!u.iout_map.empty() &&
+              (rc = upload(c, u.iout_map.data(), u.iout_map.size(), const_cast<int**>(&U.iout_map))))
+            return bail(rc);
+          if (!u.gout_map.empty() &&
+              (rc = upload(c, u.gout_map.data(), u.gout_map.size(), const_cast<int**>(&U.gout_map))))
+            return bail(rc);
+          max_nh = std::max(max_nh, U.in.n_hidden + U.ga.n_hidden);
+          max_io = std::max(max_io, U.in.n_out);
+          max_gam = std::max(max_gam, U.ga.n_out);
+          max_rows = std::max(max_rows, U.nrows);
+          units.push_back(U);
+        }
+      }
+      P.u_bnd[P.nb] = (int)units.size();
+      P.n_units = (int)units.size();
+      if ((rc = upload(c, units.data(), units.size(), const_cast<BlockDev**>(&P.units)))) return bail(rc);
+      c->n_units = P.n_units;
+    }
   }
   P.n_D = xoff;
   P.nK = P.n_D + P.n_C;
@@ -608,7 +879,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   int kern_level = 0;
   const char* jl = getenv("DDNM_JLEVEL");
   const int lvl_lo = jl ? atoi(jl) : 0, lvl_hi = jl ? atoi(jl) : (ae ? 2 : 0);
-  // largest G that fits wins, at the lowest level that fits it (measured at
+  // planner (see below: even G first, then the largest; measured at
   // config 0 with the tensor-core Gram: 4 slots with the Jacobian rows in L2
   // 35.7-37.1 ms per 4096 mu, vs 41.5 ms for 2 slots with them in shared memory)
   // kernels with the KKT workspace in global memory only when nothing else fits.
@@ -651,7 +922,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   c->kkt_stride = kern->kkt_global ? (size_t)((kkt_need + 31) & ~31) : 0;
   P.kkt_stride = (long long)c->kkt_stride;
   // tiles of consecutive outputs for the tensor-core sweep (P = 8 / G outputs each)
-  if (getenv("DDNM_DMMA") && ae && 8 % kern->g == 0) {
+  if (getenv("DDNM_DMMA") && ae && 8 % kern->g == 0 && !P.units) {
     const int Pt = 8 / kern->g;
     for (int b = 0; b < P.nb; ++b) {
       if (hwin[2 * b].k0.empty() || hwin[2 * b + 1].k0.empty()) continue;
@@ -713,7 +984,7 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // the A fragments (230 KB per block) stream from L2 every round.
   const char* swv = getenv("DDNM_SWEEP");
   // DDNM_SWEEP=2: chains for the interface decoder only
-  if (ae && ni <= 7 && ng <= 7 && swv && (atoi(swv) == 1 || atoi(swv) == 2) && !getenv("DDNM_DMMA")) {
+  if (ae && ni <= 7 && ng <= 7 && swv && (atoi(swv) == 1 || atoi(swv) == 2) && !getenv("DDNM_DMMA") && !P.units) {
     constexpr int R = 4;
     const bool gam_only = atoi(swv) == 2;
     const int nw = gam_only ? 4 : c->threads / 32;
@@ -894,6 +1165,7 @@ int ddnm_ctx_info(const ddnm_ctx* c, ddnm_info* i) {
   i->ctas = c->ctas;
   i->smem_bytes = (int32_t)c->smem;
   i->device = c->device;
+  i->eval_units = c->n_units;
   return 0;
 }
 

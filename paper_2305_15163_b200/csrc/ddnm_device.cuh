@@ -127,7 +127,19 @@ struct BlockDev {
   int nbz;                // gappy HR: residual basis size (0: collocation)
   const double* wts;      // gappy HR: weights [nbz][nrows] (hyper.py:153-160)
   int out_off, outR_off;  // offsets of the weighted rows in the Br / R dumps
+  // evaluation units (large blocks split into row chunks, see Params::units):
+  int uflags;             // UF_* below
+  int real;               // real block of this unit
+  const int* iout_map;    // [in.n_out] real-block interior output of each unit output (null: identity)
+  const int* gout_map;    // [ga.n_out] real-block interface output (null: identity)
+  const int* row_map;     // [nrows] real-block row of each unit row (null: identity)
 };
+
+// evaluation-unit flags: a unit with rows evaluates its stencil rows and adds
+// its Gram contribution to its real block; a constraint unit evaluates
+// C A_i g over its interface outputs.  ACC_*: add into the real block's
+// pieces (a later unit of the same block) instead of writing them.
+enum UnitFlags { UF_ROWS = 1, UF_CON = 2, UF_ACC_GRAM = 4, UF_ACC_CON = 8 };
 
 struct SlotState {
   int mu, phase, n_iter, n_trials, n_evals, n_reg, status, need_kkt;
@@ -217,6 +229,14 @@ struct Params {
   // KKT workspace in global memory (kernels instantiated with KG = true)
   double* kkt_g;          // per global slot [kkt_stride]
   long long kkt_stride;
+  // evaluation units: when non-null, eval_blocks walks units[u_bnd[b]] ..
+  // units[u_bnd[b + 1] - 1] for real block b instead of blk[b] (blocks too
+  // large for one CTA's shared memory are split into chunks of their sampled
+  // rows, each with the decoder subnet restricted to the outputs its rows
+  // reference, plus chunks of interface outputs for the WFPC constraint)
+  const BlockDev* units;
+  int n_units;
+  int u_bnd[MAXB + 1];
 };
 
 // RomInstance.decode (driver.py:148-152): one full decoder of one block.

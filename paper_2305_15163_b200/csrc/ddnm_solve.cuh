@@ -608,28 +608,31 @@ __device__ void gram_dmma(const View& V, const BlockDev& B, unsigned mask, const
     double c0[2] = {c[0][0] + c[2][0], c[0][1] + c[2][1]};
     double c1[2] = {c[1][0] + c[3][0], c[1][1] + c[3][1]};
     double* e = V.eb(s, ebi[s]);
+    // later units of a split block add to the block's pieces (unit order)
+    const bool acc = (B.uflags & UF_ACC_GRAM) != 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3) + h;
       if (i > j || j > W) continue;
       const double v = c0[h] + c1[h];
-      if (j < W) eb_H(e, B)[tri_idx(W, i, j)] = v;
-      else if (i < W) eb_proj(e, B)[i] = v;
-      else *eb_rr(e, B, P.n_C) = v;
+      double* dst = j < W ? eb_H(e, B) + tri_idx(W, i, j) : i < W ? eb_proj(e, B) + i : eb_rr(e, B, P.n_C);
+      *dst = acc ? *dst + v : v;
     }
   }
 }
 
+// one block (or evaluation unit) of eval_gradients for every slot in mask
 template <int G, int NI, int NG>
-__device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gslot0,
-                            bool dump) {
+__device__ __forceinline__ void eval_unit(const View& V, const BlockDev& B, unsigned mask,
+                                          const int* ebi, int gslot0, bool dump) {
   const Params& P = V.P;
   const int tid = threadIdx.x, T = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  const int warp = tid >> 5, nw = T >> 5;
   SlotState* st = V.st();
   constexpr int W = NI + NG;
-  for (int b = P.b_lo; b < P.b_hi; ++b) {
-    const BlockDev& B = P.blk[b];
+  {
+    const bool has_con = (B.uflags & UF_CON) != 0;
+    const bool acc_con = (B.uflags & UF_ACC_CON) != 0;
     const int nhi = P.map_kind == MAP_AE ? B.in.n_hidden : 0;
     // ---- phase A: hidden layer of both decoders ----
     if (P.map_kind == MAP_AE) {
@@ -729,8 +732,8 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
       const int ngo = B.ga.n_out;
       // 8-lane group per (slot, constraint row): cval = CA g, cjac = CA J
       // (driver.py:371-373); the remaining threads start on stencil rows
-      const int nct = P.con_mode == 1 ? 0 : 8 * G * P.n_C, nct32 = (nct + 31) & ~31;
-      if (P.con_mode == 1) {
+      const int nct = (P.con_mode == 1 || !has_con) ? 0 : 8 * G * P.n_C, nct32 = (nct + 31) & ~31;
+      if (P.con_mode == 1 && has_con) {
         // SRPC (driver.py:374-378): value Ahat x_Gamma, constant Jacobian Ahat
         for (int t = tid; t < G * P.n_C; t += T) {
           const int s = t / P.n_C, c = t - s * P.n_C;
@@ -774,16 +777,19 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         }
         if (act && q == 0) {
           double* e = V.eb(s, ebi[s]);
-          eb_cval(e, B)[c] = a0;
+          double* cv = eb_cval(e, B) + c;
+          double* cj = eb_cjac(e, B, P.n_C) + c * NG;
+          *cv = acc_con ? *cv + a0 : a0;
 #pragma unroll
-          for (int d = 0; d < NG; ++d) eb_cjac(e, B, P.n_C)[c * NG + d] = aj[d];
+          for (int d = 0; d < NG; ++d) cj[d] = acc_con ? cj[d] + aj[d] : aj[d];
         }
       }
       for (int it = tid - nct32; it < G * B.nrows; it += T) {
         if (it < 0) continue;
         const int s = it / B.nrows, row = it - s * B.nrows;
         if (!((mask >> s) & 1u)) continue;
-        const double* bv = P.gbv + ((size_t)(gslot0 + s) * P.total_rows + B.row_off + row) * 3;
+        const int rr = B.row_map ? __ldg(B.row_map + row) : row;   // real-block row
+        const double* bv = P.gbv + ((size_t)(gslot0 + s) * P.total_rows + B.row_off + rr) * 3;
         stencil_row<NI, NG>(V, B, s, row, bv);
       }
       __syncthreads();
@@ -803,36 +809,75 @@ __device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gs
         const bool lin = P.map_kind == MAP_LINEAR;
         const double* Jint = lin ? B.in.W1 : V.jint(s);
         const double* Jgam = lin ? B.ga.W1 : V.jgam(s);
+        // units: outputs go to their real-block positions (a unit's subnet
+        // values equal the full subnet's bit for bit, hyper.py:200-222)
+        auto imap = [&](int i) { return B.iout_map ? __ldg(B.iout_map + i) : i; };
+        auto gmap = [&](int i) { return B.gout_map ? __ldg(B.gout_map + i) : i; };
+        auto rmap = [&](int i) { return B.row_map ? __ldg(B.row_map + i) : i; };
         if (o.int_g)
-          for (int i = tid; i < B.in.n_out; i += T) o.int_g[mu * P.tot_iout + B.iout_off + i] = sc[P.scr_gint + i];
+          for (int i = tid; i < B.in.n_out; i += T) o.int_g[mu * P.tot_iout + B.iout_off + imap(i)] = sc[P.scr_gint + i];
         if (o.int_J)
-          for (int i = tid; i < B.in.n_out * NI; i += T) o.int_J[mu * P.tot_intJ + B.intJ_off + i] = Jint[i];
-        if (o.gam_g)
-          for (int i = tid; i < B.ga.n_out; i += T) o.gam_g[mu * P.tot_gout + B.gout_off + i] = sc[P.scr_ggam + i];
-        if (o.gam_J)
-          for (int i = tid; i < B.ga.n_out * NG; i += T) o.gam_J[mu * P.tot_gamJ + B.gamJ_off + i] = Jgam[i];
+          for (int i = tid; i < B.in.n_out * NI; i += T)
+            o.int_J[mu * P.tot_intJ + B.intJ_off + imap(i / NI) * NI + i % NI] = Jint[i];
+        if (o.gam_g && has_con)
+          for (int i = tid; i < B.ga.n_out; i += T) o.gam_g[mu * P.tot_gout + B.gout_off + gmap(i)] = sc[P.scr_ggam + i];
+        if (o.gam_J && has_con)
+          for (int i = tid; i < B.ga.n_out * NG; i += T)
+            o.gam_J[mu * P.tot_gamJ + B.gamJ_off + gmap(i / NG) * NG + i % NG] = Jgam[i];
         const int nz = B.nbz > 0 ? B.nbz : B.nrows;
         const double* Rs = sc + (B.nbz > 0 ? P.scr_RB : P.scr_R);
         const double* rs = B.nbz > 0 ? Rs + nz * W : sc + P.scr_r;
         if (o.Br)
-          for (int i = tid; i < nz; i += T) o.Br[mu * P.tot_out + B.out_off + i] = rs[i];
+          for (int i = tid; i < nz; i += T) o.Br[mu * P.tot_out + B.out_off + rmap(i)] = rs[i];
         if (o.R)
-          for (int i = tid; i < nz * W; i += T) o.R[mu * P.tot_outR + B.outR_off + i] = Rs[i];
+          for (int i = tid; i < nz * W; i += T) o.R[mu * P.tot_outR + B.outR_off + rmap(i / W) * W + i % W] = Rs[i];
         if (o.bvals)
           for (int i = tid; i < B.nrows * 3; i += T)
-            o.bvals[(mu * P.total_rows + B.row_off) * 3 + i] =
-                P.gbv[((size_t)(gslot0 + s) * P.total_rows + B.row_off) * 3 + i];
-        const double* e = V.eb(s, ebi[s]);
-        if (o.cval)
-          for (int i = tid; i < P.n_C; i += T) o.cval[(mu * P.nb + b) * P.n_C + i] = eb_cval(const_cast<double*>(e), B)[i];
-        if (o.cjac)
-          for (int i = tid; i < P.n_C * NG; i += T) o.cjac[mu * P.tot_cjac + B.cjac_off + i] = eb_cjac(const_cast<double*>(e), B, P.n_C)[i];
+            o.bvals[(mu * P.total_rows + B.row_off + rmap(i / 3)) * 3 + i % 3] =
+                P.gbv[((size_t)(gslot0 + s) * P.total_rows + B.row_off + rmap(i / 3)) * 3 + i % 3];
       }
     }
     // ---- phase D: Gram block, projections, r^T r on FP64 tensor cores ----
-    gram_dmma<G, W>(V, B, mask, ebi);
-    __syncthreads();
+    if (B.uflags & UF_ROWS) {
+      gram_dmma<G, W>(V, B, mask, ebi);
+      __syncthreads();
+    }
     DDNM_MARK(V, 4);
+  }
+}
+
+template <int G, int NI, int NG>
+__device__ void eval_blocks(const View& V, unsigned mask, const int* ebi, int gslot0,
+                            bool dump) {
+  const Params& P = V.P;
+  const int tid = threadIdx.x, T = blockDim.x;
+  SlotState* st = V.st();
+  constexpr int NGc = NG;
+  // real blocks [b_lo, b_hi) (parameter space), or their evaluation units
+  // (Params::units, global memory): two instantiations of the body so the
+  // whole-block path keeps its constant-bank operands
+  if (!P.units) {
+    for (int b = P.b_lo; b < P.b_hi; ++b) eval_unit<G, NI, NG>(V, P.blk[b], mask, ebi, gslot0, dump);
+  } else {
+    for (int u = P.u_bnd[P.b_lo]; u < P.u_bnd[P.b_hi]; ++u)
+      eval_unit<G, NI, NG>(V, P.units[u], mask, ebi, gslot0, dump);
+  }
+  // constraint pieces of every block (complete once all its units ran)
+  if (dump) {
+    const EvalOut& o = P.eo;
+    for (int s = 0; s < G; ++s) {
+      if (!((mask >> s) & 1u)) continue;
+      const size_t mu = (size_t)st[s].mu;
+      double* e = V.eb(s, ebi[s]);
+      for (int b = P.b_lo; b < P.b_hi; ++b) {
+        const BlockDev& R = P.blk[b];
+        if (o.cval)
+          for (int i = tid; i < P.n_C; i += T) o.cval[(mu * P.nb + b) * P.n_C + i] = eb_cval(e, R)[i];
+        if (o.cjac)
+          for (int i = tid; i < P.n_C * NGc; i += T) o.cjac[mu * P.tot_cjac + R.cjac_off + i] = eb_cjac(e, R, P.n_C)[i];
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -59,6 +59,13 @@ class RomInstance:
         self._keep = []
 
     @classmethod
+    def from_ddrom(cls, ref_instance, full_maps: bool = True) -> "RomInstance":
+        """From the reference's ``ddrom.driver.RomInstance`` (driver.py:93-152)
+        after ``attach_hr``/``fit_initializer`` -- see :mod:`.intake`."""
+        from .intake import arrays_from_ddrom
+        return cls(arrays_from_ddrom(ref_instance, full_maps=full_maps))
+
+    @classmethod
     def load(cls, path: str) -> "RomInstance":
         """From the ``.npz`` artifacts or a binio instance file pair
         (``.bin`` + ``.txt``, see :mod:`binio`)."""
@@ -450,19 +457,74 @@ class RomSolution:
     error: float = np.nan
 
 
-def solve_rom(instance: RomInstance, p: ParameterPoint, cfg: SqpConfig = SqpConfig(), *,
-              x0=None, lam0=None, fom_state=None, compute_error: bool = False,
-              label: str = ""):
-    """Solve the ROM at ``p`` (driver.py:554-597) on the GPU.
+@dataclass(eq=False)
+class BenchmarkRecord:
+    """driver.py:522-551 (same fields, CSV header and row)."""
 
-    Returns ``(RomSolution, record_dict)``.  ``states`` is the device decode
-    of the solution (driver.py:589) when the artifacts carry the full maps.
-    ``fom_state`` (a global FOM state) gives ``error`` = relative_error
-    (driver.py:590-592); computing the FOM itself (``compute_error`` without
-    ``fom_state``) is outside the online GPU path and is rejected."""
+    label: str
+    config: dict
+    a: float
+    lam: float
+    error: float = np.nan
+    fom_seconds: float = np.nan
+    rom_seconds: float = np.nan
+    parallel_seconds: float = np.nan
+    per_iter_seconds: float = np.nan
+    speedup: float = np.nan
+    n_iter: int = 0
+    converged: bool = False
+    final_merit: float = np.nan
+    status: str = "ok"
+
+    HEADER = ["label", "rom", "constraint", "hr", "n_int", "n_gam", "a",
+              "lambda", "error", "fom_seconds", "rom_seconds",
+              "parallel_seconds", "per_iter_seconds", "speedup", "n_iter",
+              "converged", "final_merit", "status"]
+
+    def row(self):
+        c = self.config
+        return [self.label, c.get("rom", ""), c.get("constraint", ""),
+                c.get("hr", ""), c.get("n_int", ""), c.get("n_gam", ""),
+                self.a, self.lam, self.error, self.fom_seconds,
+                self.rom_seconds, self.parallel_seconds,
+                self.per_iter_seconds, self.speedup, self.n_iter,
+                int(self.converged), self.final_merit, self.status]
+
+
+def _param_of(ops_or_p) -> ParameterPoint:
+    """The parameter of a ``FomOperators`` (ours or the reference's:
+    burgers.py:143-157 carries ``param``) or a ``ParameterPoint``."""
+    if isinstance(ops_or_p, ParameterPoint):
+        return ops_or_p
+    p = getattr(ops_or_p, "param", None)
+    if p is None or not hasattr(p, "a") or not hasattr(p, "lam"):
+        raise ValueError("expected FomOperators (assemble(grid, p)) or a ParameterPoint")
+    return p if isinstance(p, ParameterPoint) else ParameterPoint(float(p.a), float(p.lam))
+
+
+def solve_rom(instance: RomInstance, p: ParameterPoint, cfg: SqpConfig = SqpConfig(), *,
+              x0=None, lam0=None, fom_state=None, fom_seconds: float = np.nan,
+              compute_error: bool = True, label: str = ""):
+    """Solve the ROM at ``p`` (driver.py:554-597) on the GPU; returns
+    ``(RomSolution, BenchmarkRecord)`` like the reference.
+
+    ``compute_error`` (default True, as the reference): without ``fom_state``
+    the full-order solution is computed first on the host (``fom.py``, the
+    reference's own ``solve_monolithic`` path, driver.py:566-569; not part of
+    the ROM solve and not in ``rom_seconds``), then ``error`` =
+    ``relative_error`` of the device decode (driver.py:589-592).  The record's
+    ``parallel_seconds`` is the device time of the solve (every block of an
+    evaluation runs concurrently on the GPU, the execution model the
+    reference emulates with its max-over-blocks charge, driver.py:580)."""
+    part_fom = None
     if compute_error and fom_state is None:
-        raise NotImplementedError("compute_error needs the full-order solve, which is "
-                                  "not part of the online GPU path; pass fom_state")
+        from .fom import solve_monolithic
+        t0 = time.perf_counter()
+        part_fom = solve_monolithic(instance.grid, p)
+        fom_seconds = time.perf_counter() - t0
+        fom_state = part_fom
+    if compute_error and not instance.has_full_decoders:
+        raise ValueError("compute_error needs the full decoders (artifacts with *_intf_* maps)")
     mu = np.array([[p.a, p.lam]], dtype=float)
     res = solve_rom_batch(instance, mu, cfg,
                           x0=None if x0 is None else np.asarray(x0, float)[None, :],
@@ -471,20 +533,31 @@ def solve_rom(instance: RomInstance, p: ParameterPoint, cfg: SqpConfig = SqpConf
     states, error = None, np.nan
     if instance.has_full_decoders:
         dec = decode_batch(instance, r.x[None, :],
-                           fom_states=None if fom_state is None else np.asarray(fom_state)[None])
+                           fom_states=(None if not compute_error or fom_state is None
+                                       else np.asarray(fom_state)[None]))
         states = dec.blocks(0)
         if dec.error is not None:
             error = float(dec.error[0])
-    rec = {"label": label or instance.provenance.get("rom", "rom"), "a": p.a, "lam": p.lam,
-           "error": error, "rom_seconds": res.seconds, "n_iter": r.n_iter,
-           "converged": r.converged, "final_merit": r.final_merit,
-           "status": "ok" if r.failure_reason is None else r.failure_reason}
+    parallel = float(res.seconds)
+    rec = BenchmarkRecord(
+        label=label or instance.provenance.get("rom", "rom"), config=dict(instance.provenance),
+        a=p.a, lam=p.lam, error=error, fom_seconds=fom_seconds, rom_seconds=parallel,
+        parallel_seconds=parallel, per_iter_seconds=parallel / max(r.n_iter, 1),
+        speedup=fom_seconds / parallel if parallel > 0 else np.nan,
+        n_iter=r.n_iter, converged=r.converged, final_merit=r.final_merit,
+        status="ok" if r.failure_reason is None else r.failure_reason)
     return RomSolution(x_latent=r.x, lam=r.lam, states=states, sqp=r, error=error), rec
 
 
-def init_guess(instance: RomInstance, p: ParameterPoint):
+def init_guess(instance: RomInstance, p: ParameterPoint, *, ops=None, prob=None):
     """RBF latents plus least-squares multipliers (driver.py:442-458),
-    evaluated on the device."""
+    evaluated on the device.  ``ops`` / ``prob`` are accepted as in the
+    reference (they only let it reuse assembled operators); the device reads
+    the parameter alone."""
+    if ops is not None and _param_of(ops) != p:
+        raise ValueError("ops were assembled at a different parameter")
+    if prob is not None and getattr(prob, "param", p) != p:
+        raise ValueError("problem was built at a different parameter")
     mu = np.array([[p.a, p.lam]], dtype=float)
     res = solve_rom_batch(instance, mu, SqpConfig(max_iter=1, tol=1e300))
     return res.x0[0].copy(), res.lam0[0].copy()
@@ -572,10 +645,13 @@ def eval_gradients_batch(instance: RomInstance, mus, x, lam, *, reg_scale: float
     return EvalBatch(layout=layout, **o)
 
 
-def build_problem(instance: RomInstance, p: ParameterPoint) -> SqpProblem:
-    """``build_problem`` (driver.py:356-436) at one parameter: blocks whose
+def build_problem(instance: RomInstance, ops) -> SqpProblem:
+    """``build_problem(instance, ops)`` (driver.py:356-436): blocks whose
     residual/constraint closures evaluate on the GPU (one eval per call), so
-    the reference's own ``sqp.iterate`` can drive them."""
+    the reference's own ``sqp.iterate`` can drive them.  ``ops`` is
+    ``assemble(grid, p)`` (ours or the reference's); a ``ParameterPoint`` is
+    accepted too."""
+    p = _param_of(ops)
     mu = np.array([[p.a, p.lam]], dtype=float)
     offs = np.cumsum([0] + [a + b for a, b in instance.latent_layout])
     nD, nC = instance.n_primal, instance.n_mult

@@ -187,7 +187,7 @@ class ShardedSolve:
         return self.eng.finish(self.mu)
 
 
-CHECK = int(os.environ.get("DDNM_DD_CHECK", "4"))   # rounds between host reads of the running-mu count
+CHECK = max(1, int(os.environ.get("DDNM_DD_CHECK", "4")))   # rounds between host reads of the running-mu count
 
 
 def _all_gather(gathered, packets, world, group):
@@ -324,14 +324,17 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
             active = sh.step(gathered, count=sh.rounds % CHECK == CHECK - 1)
         done = True
     finally:
+        if own:
+            # no evaluation kernel may still store through a peer mapping
+            sh.eng.torch.cuda.current_stream(sh.eng.dev).synchronize()
         for pb in peers:
             pb.close()
-        if own:
-            sh.eng.torch.cuda.current_stream(sh.eng.dev).synchronize()
-            if done:
-                dist.barrier(group=group)   # every rank unmapped before the frees
+        if own and done:
+            dist.barrier(group=group)   # every rank unmapped before the frees
             for b in own:
                 b.close()
+        # on the error path the exported buffers are leaked rather than freed:
+        # a peer may still have them mapped
     res = sh.result()
     if hasattr(res, "seconds"):
         res.seconds = time.perf_counter() - t0

@@ -8,7 +8,10 @@ against its monolithic FOM solve (``solve_monolithic``) for three mu."""
 import numpy as np
 import pytest
 
-from tests.conftest import ALL, golden_path
+from tests.conftest import ALL, BIG, golden_path
+
+# the 480^2 / 960^2 instances carry no full maps (decode is off their solve path)
+DEC = [n for n in ALL if n not in BIG]
 
 
 def _states(name):
@@ -21,7 +24,7 @@ def _flat(blocks):
 
 # -- CPU: oracle pinned to the reference, host-side index helpers ---------------
 
-@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("name", DEC)
 def test_oracle_decode_matches_reference(name, oracle_instances):
     from oracle import ddnm_oracle as O
     inst, s = oracle_instances[name], _states(name)
@@ -62,7 +65,7 @@ def test_restrict_and_assemble_host_helpers(name, oracle_instances):
 # -- GPU: device decode ----------------------------------------------------------
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("name", DEC)
 def test_decode_matches_reference_golden(name, gpu_instances):
     import paper_2305_15163_b200 as P
     inst, s = gpu_instances[name], _states(name)
@@ -106,11 +109,17 @@ def test_solve_rom_returns_states_and_error(gpu_instances, oracle_instances):
         np.testing.assert_allclose(a, c, rtol=1e-12, atol=1e-13)
         np.testing.assert_allclose(b, d, rtol=1e-12, atol=1e-13)
     e = O.relative_error(oinst.restrict_blocks(s["fom1"]), ref)
-    assert abs(sol.error - e) <= 1e-12 * e and rec["error"] == sol.error
+    assert abs(sol.error - e) <= 1e-12 * e and rec.error == sol.error
     # the device solution is the reference's to 1e-9, so is its error
     assert abs(sol.error - float(s["err1"])) <= 1e-6 * float(s["err1"])
-    with pytest.raises(NotImplementedError):
-        P.solve_rom(inst, p, compute_error=True)
+    # the reference's default (compute_error=True, no fom_state): the FOM is
+    # solved first (host, burgers.solve_monolithic semantics), then the error
+    sol2, rec2 = P.solve_rom(inst, p)
+    assert abs(sol2.error - float(s["err1"])) <= 1e-6 * float(s["err1"])
+    assert rec2.fom_seconds > 0 and rec2.speedup == rec2.fom_seconds / rec2.parallel_seconds
+    assert len(rec2.row()) == len(P.BenchmarkRecord.HEADER)
+    _, rec3 = P.solve_rom(inst, p, compute_error=False)
+    assert np.isnan(rec3.error) and np.isnan(rec3.fom_seconds)
 
 
 @pytest.mark.gpu

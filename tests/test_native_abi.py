@@ -70,8 +70,11 @@ def test_argument_validation_before_device():
         P.solve_rom_batch(inst, np.array([[np.nan, 10.0]]))
     with pytest.raises(ValueError):
         P.SqpConfig(backtrack_factor=1.5)
-    with pytest.raises(NotImplementedError):
-        P.solve_rom(inst, P.ParameterPoint(100.0, 10.0), compute_error=True)
+    with pytest.raises(ValueError):
+        P.build_problem(inst, object())        # neither FomOperators nor ParameterPoint
+    with pytest.raises(ValueError):
+        P.init_guess(inst, P.ParameterPoint(100.0, 10.0),
+                     ops=P.assemble(inst.grid, P.ParameterPoint(200.0, 10.0)))
 
 
 def _artifacts(name="tiny_nm"):

@@ -8,7 +8,7 @@ import pytest
 
 from oracle import ddnm_oracle as O
 
-from .conftest import NAMES
+from .conftest import BIG, N_BIG, NAMES
 
 
 def rel(a, b):
@@ -82,7 +82,7 @@ def test_solve_matches_reference(name, oracle_instances, goldens):
     identical whenever no tol/Armijo decision on the path was within the merit
     noise floor (SURVEY §7 hard part 1: the margin-aware gate)."""
     inst, g = oracle_instances[name], goldens[name]
-    B = g["mu"].shape[0]
+    B = N_BIG if name in BIG else g["mu"].shape[0]
     robust = 0
     for k in range(B):
         a, lam = g["mu"][k]

@@ -41,131 +41,30 @@ import numpy as np  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def extract(inst) -> dict:
-    from ddrom.autoencoder import Autoencoder
-    from ddrom.hyper import extract_subnet, hr_rows_for_subdomain
-    from ddrom.pod import LinearMap
+def extract(inst, full_maps: bool = True) -> dict:
+    """The package's own intake (paper_2305_15163_b200/intake.py)."""
+    sys.path.insert(0, ROOT)
+    from paper_2305_15163_b200.intake import arrays_from_ddrom
+    return arrays_from_ddrom(inst, full_maps=full_maps)
 
-    part = inst.partition
-    grid = part.grid
+
+def _golden_one(inst, mu, k, detail, dense_jd):
+    """One mu of ``goldens`` (process-pool worker): batch rows as
+    (index, value) pairs, detail arrays as-is."""
+    sub = goldens(inst, 1, 0, 1 if detail else 0, mu=mu[k:k + 1], dense_jd=dense_jd)
     out = {}
-    kind = "nm" if isinstance(inst.interior_maps[0], Autoencoder) else "ls"
-    srpc = inst.constraint_mode == "srpc"
-    n_int = [m.latent_dim for m in inst.interior_maps]
-    n_gam = [g.latent_dim for g in inst.interface_maps]
-    act = inst.interior_maps[0].activation if kind == "nm" else "linear"
-    gam_act = inst.interface_maps[0].activation if kind == "nm" else "linear"
-    for i, sub in enumerate(part.subdomains):
-        hr = inst.hr[i]
-        rows = hr.apply_B_rows()
-        io, gio = hr_rows_for_subdomain(part, i, rows)
-        cols = np.concatenate([sub.interior_cols[io], sub.interface_cols[gio]])
-        p = f"b{i}_"
-        out[p + "res_rows"] = sub.res_rows[rows].astype(np.int64)
-        out[p + "cols"] = cols.astype(np.int64)
-        out[p + "io"] = io.astype(np.int64)
-        out[p + "gio"] = gio.astype(np.int64)
-        out[p + "n_interior"] = np.int64(sub.n_interior)
-        out[p + "n_interface"] = np.int64(sub.n_interface)
-        if srpc:   # driver.py:374-378
-            out[p + "Ahat"] = inst.rom_constraints.blocks[i].toarray()
-        else:      # driver.py:366-373
-            out[p + "CA"] = inst.wfpc_C @ inst.fom_constraints.blocks[i].toarray()
-        if hr.mode == "gappy":   # hyper.py:107-118,153-160
-            out[p + "weights"] = np.ascontiguousarray(hr.weights)
-        # global dof columns of the block (Partition.restrict, partition.py:232-235)
-        out[p + "int_cols"] = sub.interior_cols.astype(np.int64)
-        out[p + "gam_cols"] = sub.interface_cols.astype(np.int64)
-        im, gm = inst.interior_maps[i], inst.interface_maps[i]
-        # the full interior map for RomInstance.decode (driver.py:148-152)
-        if kind == "nm":
-            W2f = im.W2g.tocsr()
-            out[p + "intf_W1"] = np.ascontiguousarray(im.W1g)
-            out[p + "intf_b1"] = im.b1g.copy()
-            out[p + "intf_W2_indptr"] = W2f.indptr.astype(np.int64)
-            out[p + "intf_W2_indices"] = W2f.indices.astype(np.int64)
-            out[p + "intf_W2_data"] = W2f.data.copy()
-            out[p + "intf_scale"] = im.norm.scale.copy()
-            out[p + "intf_shift"] = im.norm.shift.copy()
+    for key, v in sub.items():
+        if key in ("mu", "seed"):
+            continue
+        if key.startswith("d0_"):
+            out[f"d{k}_" + key[3:]] = v
         else:
-            out[p + "intf_Phi"] = np.ascontiguousarray(im.Phi)
-        if srpc:
-            # the residual uses the interface map restricted to gio
-            # (driver.py:400-402); the full map is kept for the decode
-            if kind == "nm":
-                W2f = gm.W2g.tocsr()
-                out[p + "gamf_W1"] = np.ascontiguousarray(gm.W1g)
-                out[p + "gamf_b1"] = gm.b1g.copy()
-                out[p + "gamf_W2_indptr"] = W2f.indptr.astype(np.int64)
-                out[p + "gamf_W2_indices"] = W2f.indices.astype(np.int64)
-                out[p + "gamf_W2_data"] = W2f.data.copy()
-                out[p + "gamf_scale"] = gm.norm.scale.copy()
-                out[p + "gamf_shift"] = gm.norm.shift.copy()
-            else:
-                out[p + "gamf_Phi"] = np.ascontiguousarray(gm.Phi)
-        if kind == "nm":
-            sn = extract_subnet(im, io)
-            out[p + "int_W1"] = np.ascontiguousarray(sn.W1)
-            out[p + "int_b1"] = sn.b1.copy()
-            out[p + "int_W2_indptr"] = sn.W2.indptr.astype(np.int64)
-            out[p + "int_W2_indices"] = sn.W2.indices.astype(np.int64)
-            out[p + "int_W2_data"] = sn.W2.data.copy()
-            out[p + "int_scale"] = sn.scale.copy()
-            out[p + "int_shift"] = sn.shift.copy()
-            out[p + "int_hidden_idx"] = sn.hidden_idx.astype(np.int64)
-            if srpc:
-                sg = extract_subnet(gm, gio) if gio.size else None
-                H = sg.W1.shape[0] if sg is not None else 0
-                out[p + "gam_W1"] = (np.ascontiguousarray(sg.W1) if sg is not None
-                                     else np.zeros((0, gm.latent_dim)))
-                out[p + "gam_b1"] = sg.b1.copy() if sg is not None else np.zeros(0)
-                out[p + "gam_W2_indptr"] = (sg.W2.indptr.astype(np.int64) if sg is not None
-                                            else np.zeros(1, np.int64))
-                out[p + "gam_W2_indices"] = (sg.W2.indices.astype(np.int64) if sg is not None
-                                             else np.zeros(0, np.int64))
-                out[p + "gam_W2_data"] = sg.W2.data.copy() if sg is not None else np.zeros(0)
-                out[p + "gam_scale"] = sg.scale.copy() if sg is not None else np.zeros(0)
-                out[p + "gam_shift"] = sg.shift.copy() if sg is not None else np.zeros(0)
-                del H
-            else:
-                W2g = gm.W2g.tocsr()
-                out[p + "gam_W1"] = np.ascontiguousarray(gm.W1g)
-                out[p + "gam_b1"] = gm.b1g.copy()
-                out[p + "gam_W2_indptr"] = W2g.indptr.astype(np.int64)
-                out[p + "gam_W2_indices"] = W2g.indices.astype(np.int64)
-                out[p + "gam_W2_data"] = W2g.data.copy()
-                out[p + "gam_scale"] = gm.norm.scale.copy()
-                out[p + "gam_shift"] = gm.norm.shift.copy()
-        else:
-            assert isinstance(im, LinearMap) and isinstance(gm, LinearMap)
-            out[p + "int_Phi"] = np.ascontiguousarray(im.restrict_outputs(io).Phi)
-            out[p + "gam_Phi"] = np.ascontiguousarray(
-                gm.restrict_outputs(gio).Phi if srpc else gm.Phi)
-    ini = inst.initializer
-    rbf = ini._rbf
-    meta = {
-        "kind": kind, "activation": act, "gam_activation": gam_act,
-        "constraint": inst.constraint_mode, "hr": inst.hr[0].mode,
-        "nx": grid.nx, "ny": grid.ny,
-        "nu": grid.nu, "nsub_x": part.nsub_x, "nsub_y": part.nsub_y,
-        "nblocks": len(part.subdomains), "n_int": n_int, "n_gam": n_gam,
-        "n_c": int(inst.n_mult), "ndof": int(grid.ndof), "rbf_kernel": rbf.kernel,
-        "rbf_epsilon": float(rbf.epsilon),
-        "provenance": {k: (v if isinstance(v, (int, float, str)) else str(v))
-                       for k, v in inst.provenance.items()},
-    }
-    out["rbf_lo"] = ini.lo.copy()
-    out["rbf_hi"] = ini.hi.copy()
-    out["rbf_y"] = np.ascontiguousarray(rbf.y)
-    out["rbf_coeffs"] = np.ascontiguousarray(rbf._coeffs)
-    out["rbf_shift"] = np.asarray(rbf._shift, dtype=float)
-    out["rbf_scale"] = np.asarray(rbf._scale, dtype=float)
-    out["rbf_powers"] = np.asarray(rbf.powers, dtype=np.int64)
-    out["meta_json"] = np.array(json.dumps(meta))
+            out[key] = (k, v[0])
     return out
 
 
-def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
+def goldens(inst, B: int, seed: int, n_detail: int, mu=None, dense_jd: bool = True,
+            procs: int = 1) -> dict:
     from ddrom.burgers import ParameterPoint, assemble
     from ddrom.driver import build_problem, init_guess, solve_rom
     from ddrom.errors import ConvergenceError
@@ -174,10 +73,13 @@ def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
     from ddrom.sqp import SqpConfig, assemble_and_solve_kkt, eval_gradients
 
     cfg = SqpConfig()
-    rng = np.random.default_rng(seed)
-    a = rng.uniform(1.0, 1.0e4, B)
-    lam = rng.uniform(5.0, 25.0, B)
-    mu = np.stack([a, lam], axis=1)
+    if mu is None:
+        rng = np.random.default_rng(seed)
+        a = rng.uniform(1.0, 1.0e4, B)
+        lam = rng.uniform(5.0, 25.0, B)
+        mu = np.stack([a, lam], axis=1)
+    else:
+        a, lam = mu[:, 0], mu[:, 1]
     n_D = sum(ni + ng for ni, ng in inst.latent_layout)
     n_C = inst.n_mult
     K = cfg.max_iter
@@ -192,6 +94,18 @@ def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
         "alpha_hist": np.full((B, K), np.nan),
     }
     part = inst.partition
+    if procs > 1:
+        from multiprocessing import get_context
+        with get_context("fork").Pool(procs) as pool:
+            parts = pool.starmap(_golden_one, [(inst, mu, k, k < n_detail, dense_jd)
+                                               for k in range(B)], chunksize=1)
+        for part_g in parts:
+            for key, v in part_g.items():
+                if isinstance(v, tuple):      # (row index, value) of a batch array
+                    g[key][v[0]] = v[1]
+                else:
+                    g[key] = v
+        return g
     for k in range(B):
         p = ParameterPoint(float(a[k]), float(lam[k]))
         ops = assemble(part.grid, p)
@@ -259,7 +173,8 @@ def goldens(inst, B: int, seed: int, n_detail: int) -> dict:
                 v = np.concatenate([g[q + "int_g"],
                                     g[q + "gam_g"] if srpc else g[q + "gam_g"][gio]])
                 g[q + "stencil_r"] = rr.residual(v)
-                g[q + "stencil_Jd"] = rr.jacobian(v).toarray()
+                if dense_jd:
+                    g[q + "stencil_Jd"] = rr.jacobian(v).toarray()
                 n = part.grid.nnode
                 rws = sub.res_rows[rows]
                 node = np.where(rws < n, rws, rws - n)
@@ -313,6 +228,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--detail", type=int, default=3)
     ap.add_argument("--states", type=int, default=3, help="mu with decoded-state goldens")
+    ap.add_argument("--procs", type=int, default=1, help="mu solved in parallel")
+    ap.add_argument("--big", action="store_true",
+                    help="480^2 / 960^2 instances: no full maps, no dense Jd, no states")
     ap.add_argument("--artifacts-only", action="store_true",
                     help="rewrite the artifacts and state goldens, keep *_golden.npz")
     a = ap.parse_args()
@@ -320,16 +238,17 @@ def main():
     for name in a.names:
         with open(os.path.join(a.cache, f"{name}.pkl"), "rb") as f:
             inst = pickle.load(f)
-        art = extract(inst)
+        art = extract(inst, full_maps=not a.big)
         np.savez_compressed(os.path.join(a.out, f"{name}_artifacts.npz"), **art)
         gpath = os.path.join(a.out, f"{name}_golden.npz")
         if a.artifacts_only:
             gd = dict(np.load(gpath))
         else:
-            gd = goldens(inst, a.B, a.seed, a.detail)
+            gd = goldens(inst, a.B, a.seed, a.detail, dense_jd=not a.big, procs=a.procs)
             np.savez_compressed(gpath, **gd)
-        st = state_goldens(inst, gd, a.states)
-        np.savez_compressed(os.path.join(a.out, f"{name}_states.npz"), **st)
+        if not a.big:
+            st = state_goldens(inst, gd, a.states)
+            np.savez_compressed(os.path.join(a.out, f"{name}_states.npz"), **st)
         print(name, "n_iter", gd["n_iter"].tolist(), "failure",
               gd["failure"].tolist(), flush=True)
 
