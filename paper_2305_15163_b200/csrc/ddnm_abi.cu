@@ -37,6 +37,8 @@ DDNM_DECL(6, 11)
 DDNM_DECL(4, 9)
 DDNM_DECL(8, 11)
 DDNM_DECL(20, 19)
+// the declared extra latent pairs (csrc/latent_dims.txt, generated at build time)
+void register_generated(std::vector<KernelEntry>&);
 }  // namespace ddnm
 
 namespace {
@@ -98,6 +100,7 @@ const std::vector<Kernels>& kernel_table() {
     ddnm::register_4_9(v);
     ddnm::register_8_11(v);
     ddnm::register_20_19(v);
+    ddnm::register_generated(v);
     return v;
   }();
   return t;
@@ -913,7 +916,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   }
   if (!kern) {
     char buf[160];
-    snprintf(buf, sizeof buf, "no compiled kernel for n_int=%d n_gam=%d slots=%d fitting %zu B smem",
+    snprintf(buf, sizeof buf,
+             "no compiled kernel for n_int=%d n_gam=%d slots=%d fitting %zu B smem "
+             "(declare the pair in csrc/latent_dims.txt or DDNM_LATENT_DIMS and rebuild)",
              ni, ng, slots, smem_cap);
     return bail(fail(DDNM_EUNSUPPORTED, buf));
   }

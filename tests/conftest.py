@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "c3s_nm", "dd16_nm", "c3_nm"]
+NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "c3s_nm", "dd16_nm", "c3_nm", "tiny42_nm"]
 # BASELINE configs 3 (480^2) and 4 (960^2): the oracle takes seconds per
 # solve there, so whole-solve oracle comparisons use the first N_BIG mu
 # (the device is still checked against the reference goldens on all of them)

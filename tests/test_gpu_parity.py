@@ -88,6 +88,10 @@ def test_solve_batch_matches_oracle(name, gpu_instances, oracle_instances, golde
         assert rel(res.lam[k], r.lam) < 1e-9, k
         assert rel(res.x[k], g["x"][k]) < 1e-9, k          # and the reference itself
         assert rel(res.lam[k], g["lam"][k]) < 1e-9, k
+        if r.n_iter == g["n_iter"][k]:
+            # the north star's "identical SQP iteration counts": wherever the
+            # oracle reproduces the reference's count, the device must too
+            assert res.n_iter[k] == r.n_iter, (k, res.n_iter[k], r.n_iter)
         if min(r.margins) > merit_noise(r.merit_history[0]):
             robust += 1
             assert res.n_iter[k] == r.n_iter == g["n_iter"][k]

@@ -70,6 +70,11 @@ def test_kkt_step_matches_reference(name, oracle_instances, goldens):
         assert rel(sl, g[f"d{k}_step_lam"]) < 1e-9
 
 
+# oracle-vs-reference iteration-count agreement where it is not every mu
+# (decided by round-off at the merit floor, SURVEY §7 hard part 1)
+ITER_AGREEMENT = {"c0_ls": 7, "c3s_nm": 15}
+
+
 def merit_noise(merit0):
     """Absolute round-off floor of the merit: ~1e-13 * merit0 (SURVEY §0
     finding 2: ~1e-3 absolute at 60x60 where merit0 ~ 1e10)."""
@@ -83,7 +88,7 @@ def test_solve_matches_reference(name, oracle_instances, goldens):
     noise floor (SURVEY §7 hard part 1: the margin-aware gate)."""
     inst, g = oracle_instances[name], goldens[name]
     B = N_BIG if name in BIG else g["mu"].shape[0]
-    robust = 0
+    robust = same_iters = 0
     for k in range(B):
         a, lam = g["mu"][k]
         r = O.solve(inst, a, lam)
@@ -96,6 +101,11 @@ def test_solve_matches_reference(name, oracle_instances, goldens):
             np.testing.assert_allclose(r.merit_history, g["merit_hist"][k, :r.n_iter + 1],
                                        rtol=1e-9, atol=merit_noise(r.merit_history[0]))
             assert (r.failure_reason is not None) == bool(g["failure"][k] == 1)
+        same_iters += int(r.n_iter == g["n_iter"][k])
     # c0_ls: every trajectory touches the noise floor (cond(H_i) ~ 1e21,
     # SURVEY §7 hard part 2) -- only the 1e-9 state gate applies there
     assert robust >= (0 if name == "c0_ls" else 1)
+    # iteration counts equal to the reference's on every mu, except where a
+    # tol/Armijo decision sits at the merit round-off floor (measured: c0_ls
+    # 7/16 -- config 1 claims no iteration-count parity -- and c3s_nm 15/16)
+    assert same_iters >= ITER_AGREEMENT.get(name, B), (name, same_iters)

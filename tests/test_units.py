@@ -23,6 +23,16 @@ pytestmark = pytest.mark.gpu
 SPLIT = ["tiny_nm", "c0_nm", "c3s_nm", "dd16_nm"]
 
 
+def _whole_instance(name, monkeypatch):
+    """Every block evaluated whole (DDNM_NO_UNITS), whatever its size."""
+    monkeypatch.setenv("DDNM_NO_UNITS", "1")
+    inst = P.RomInstance.load(golden_path(name, "artifacts"))
+    ctx = inst.context()
+    monkeypatch.delenv("DDNM_NO_UNITS")
+    assert ctx.info.eval_units == 0
+    return inst
+
+
 def _split_instance(name, monkeypatch, rows="24", gam="64"):
     monkeypatch.setenv("DDNM_UNIT_ROWS", rows)
     monkeypatch.setenv("DDNM_UNIT_GAM", gam)
@@ -36,8 +46,7 @@ def _split_instance(name, monkeypatch, rows="24", gam="64"):
 
 @pytest.mark.parametrize("name", SPLIT)
 def test_units_eval_match_whole_blocks(name, gpu_instances, goldens, monkeypatch):
-    whole, g = gpu_instances[name], goldens[name]
-    assert whole.context().info.eval_units == 0
+    whole, g = _whole_instance(name, monkeypatch), goldens[name]
     split = _split_instance(name, monkeypatch)
     B = 5
     mu, x, lam = g["mu"][:B], g["x0"][:B], g["lam0"][:B]
@@ -59,7 +68,7 @@ def test_units_eval_match_whole_blocks(name, gpu_instances, goldens, monkeypatch
 
 @pytest.mark.parametrize("name", SPLIT)
 def test_units_solve_match_reference(name, gpu_instances, goldens, monkeypatch):
-    whole, g = gpu_instances[name], goldens[name]
+    whole, g = _whole_instance(name, monkeypatch), goldens[name]
     split = _split_instance(name, monkeypatch)
     rw = P.solve_rom_batch(whole, g["mu"])
     rs = P.solve_rom_batch(split, g["mu"])

@@ -147,18 +147,25 @@ def test_variant_eval_matches_oracle(name, gpu_instances, oracle_instances, gold
 def test_variant_solve_matches_oracle(name, gpu_instances, oracle_instances, goldens):
     inst, oi, g = gpu_instances[name], oracle_instances[name], goldens[name]
     res = P.solve_rom_batch(inst, g["mu"])
+    undetermined = 0
     for k in range(g["mu"].shape[0]):
         assert rel(res.x0[k], g["x0"][k]) < 1e-13
         sig, r = sensitivity(name, oi, g["mu"][k], g["x0"][k], k)
-        if r is None or sig > 1e-3:
-            continue              # not determined by the problem at all (diverging)
-        tol = max(1e-9, 1e3 * sig)
+        if r is None or 1e3 * sig > 1e-6:
+            # the problem does not determine x to 1e-6 at this mu (the oracle
+            # moves by more under a 1e-14 start perturbation or another valid
+            # KKT solve): no parity claim, counted
+            undetermined += 1
+            continue
+        tol = max(1e-9, 1e3 * sig)          # capped: <= 1e-6
         assert rel(res.x[k], r.x) < tol, (k, sig)
         assert rel(res.lam[k], r.lam) < tol, (k, sig)
         if sig <= 1e-10 and min(r.margins, default=np.inf) > merit_noise(r.merit_history[0]):
             assert res.n_iter[k] == r.n_iter
             np.testing.assert_array_equal(res.alpha_hist[k, :r.n_iter], r.alpha_history)
             assert res.failure_reason(k) == r.failure_reason
+    print(f"{name}: {undetermined} of {g['mu'].shape[0]} mu undetermined at 1e-6")
+    assert g["mu"].shape[0] - undetermined >= MIN_DETERMINED.get(name, 8)
 
 
 @pytest.mark.gpu

@@ -115,7 +115,7 @@ def build(nx: int, ny: int, sx: int, sy: int, grid_n: int, snap_tol: float,
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c0", choices=["c0", "tiny", "dd16", "c3", "c3s"])
+    ap.add_argument("--config", default="c0", choices=["c0", "tiny", "dd16", "c3", "c3s", "tiny42"])
     ap.add_argument("--out", default=os.path.join(
         os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
         "artifacts_cache"))
@@ -143,6 +143,12 @@ def main():
         # n_C = 40 as config 4, 8x8 mu grid, 10% collocation rows
         build(60, 60, 4, 4, 8, 1e-7, 8, 5, 8, 1, a.epochs or 2000, 40, 40,
               45, None, a.out, a.procs, "dd16")
+    elif a.config == "tiny42":
+        # a latent pair outside the hand-written kernel list (the paper's
+        # latent sweep starts at (4, 2)): 24x24, 2x2,
+        # n = (4, 2), n_C = sum n_gam / 2 = 4
+        build(24, 24, 2, 2, 4, 1e-7, 4, 2, 4, 1, a.epochs or 2000, 4, 4,
+              40, None, a.out, a.procs, "tiny42")
     else:
         # small fast instance for CPU unit tests: 24x24 grid, 2x2 subdomains
         build(24, 24, 2, 2, 4, 1e-7, 4, 3, 4, 1, a.epochs or 2000, 4, 8,

@@ -1,6 +1,7 @@
 """Small end-to-end cases through every kernel family (for debug builds with
-bounds checks; compute-sanitizer is not available on the pool): the persistent solve and the
-evaluation on tiny / c0 / variants, the KG kernels (c0_lss, dd16: KKT
+bounds checks, and under compute-sanitizer): the persistent solve and the
+evaluation on tiny / c0 / variants / evaluation units (c3_nm, forced on
+tiny_nm), a generated latent pair (tiny42_nm), the KG kernels (c0_lss, dd16: KKT
 workspace in L2, 96-row block path), the subdomain round kernels (NCCL-style
 and fused peer stores, several rank states), the decoder and a context from
 a binio instance file."""
@@ -23,7 +24,14 @@ def load(name):
     return P.RomInstance.load(os.path.join(ROOT, "tests", "golden", f"{name}_artifacts.npz"))
 
 
-for name in ("tiny_nm", "tiny_ls", "c0_nm", "tiny_srpc", "c0_nmg", "c0_lss", "dd16_nm"):
+os.environ["DDNM_UNIT_ROWS"] = "24"          # evaluation units (the configs-3/4 path) on tiny
+unit_inst = load("tiny_nm")
+unit_inst.context()
+del os.environ["DDNM_UNIT_ROWS"]
+r = P.solve_rom_batch(unit_inst, P.seeded_parameters(6, seed=4))
+print("tiny_nm units ok", unit_inst.context().info.eval_units, r.n_iter.tolist(), flush=True)
+for name in ("tiny_nm", "tiny_ls", "c0_nm", "tiny_srpc", "c0_nmg", "c0_lss", "dd16_nm", "tiny42_nm",
+             "c3_nm"):
     inst = load(name)
     mu = P.seeded_parameters(6, seed=4)
     r = P.solve_rom_batch(inst, mu)
