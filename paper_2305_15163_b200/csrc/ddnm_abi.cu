@@ -310,6 +310,17 @@ int upload_decoder(ddnm_ctx* c, const ddnm_decoder& h, int lat, int kind, int ac
     if ((rc = upload(c, w1t.data(), w1t.size(), const_cast<double**>(&d.W1t)))) return rc;
     d.W1 = nullptr;
     if ((rc = upload(c, h.b1, (size_t)h.n_hidden, const_cast<double**>(&d.b1)))) return rc;
+    {   // A fragments of the tensor-core hidden layer (hidden_group)
+      const int nt = (h.n_hidden + 7) / 8, ks = (lat + 3) / 4;
+      std::vector<double> wa((size_t)nt * ks * 32, 0.0);
+      for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < ks; ++k)
+          for (int l = 0; l < 32; ++l) {
+            const int u = 8 * t + (l >> 2), dd = 4 * k + (l & 3);
+            if (u < h.n_hidden && dd < lat) wa[((size_t)t * ks + k) * 32 + l] = h.W1[(size_t)u * lat + dd];
+          }
+      if ((rc = upload(c, wa.data(), wa.size(), const_cast<double**>(&d.w1a)))) return rc;
+    }
     if ((rc = upload_i32(c, h.indptr, (size_t)h.n_out + 1, const_cast<int**>(&d.indptr)))) return rc;
     if ((rc = upload_i32(c, h.indices, nnz, const_cast<int**>(&d.indices)))) return rc;
     if ((rc = upload(c, h.data, nnz, const_cast<double**>(&d.data)))) return rc;
@@ -801,6 +812,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // (c0_ls: 138 -> 150 ms with the attempt), so they go straight to the
   // dense LU there.  DDNM_KKT_BLOCK_MAX overrides.
   P.kkt_block_max = a->map_kind == DDNM_MAP_AUTOENCODER ? 96 : 32;
+  // hidden layer on the FP64 tensor cores unless DDNM_HIDDEN_SCALAR=1
+  P.hid_dmma = getenv("DDNM_HIDDEN_SCALAR") ? 0 : 1;
   if (const char* kb = getenv("DDNM_KKT_BLOCK_MAX")) P.kkt_block_max = std::min(96, atoi(kb));
   P.total_rows = row_off;
   P.tot_iout = iout; P.tot_gout = gout; P.tot_R = Roff; P.tot_cjac = cjoff;

@@ -60,6 +60,10 @@ struct DecDev {
   // chained tensor-core sweep: W1 as the B operand, [ceil(n_hidden/4)][32]:
   // lane -> k = 4kb + (lane&3), n = lane>>2: W1[k][n] (n < lat), 1 (n == lat), 0
   const double* wbfrag;
+  // hidden pre-activation on the FP64 tensor cores (hidden_group): W1 as the
+  // m8n8k4 A operand, [ceil(n_hidden/8)][ceil(lat/4)][32]:
+  // lane -> W1[8t + (lane>>2)][4ks + (lane&3)] (0 outside)
+  const double* w1a;
 };
 
 // Chained tensor-core sweep (sweep_chain): a tile is 8 consecutive outputs of
@@ -226,6 +230,8 @@ struct Params {
   // largest block system (W + n_C) the block-structured KKT is tried on
   // (<= 96); larger ones go straight to the dense LU
   int kkt_block_max;
+  // hidden layer: 1 = FP64 tensor-core tiles (hidden_group), 0 = per-unit DFMA
+  int hid_dmma;
   // KKT workspace in global memory (kernels instantiated with KG = true)
   double* kkt_g;          // per global slot [kkt_stride]
   long long kkt_stride;

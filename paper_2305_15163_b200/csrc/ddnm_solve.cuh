@@ -103,6 +103,61 @@ __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int 
   }
 }
 
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+// phase A on the FP64 tensor cores (north-star kernel (1)): the hidden
+// pre-activation of 8 consecutive units for every slot of the CTA as one
+// m8n8k4 chain, Z[unit][slot] = b1[unit] + sum_d W1[unit][d] x_slot[d]
+// (A = the units' W1 rows, B = the slots' latent vectors, K = latent dim in
+// steps of 4, C initialised with b1: hyper.py:184-188 / autoencoder.py:134-140
+// with the products summed by the tensor core), written to the sigma array;
+// then swish / swish' (autoencoder.py:31-45) of the group's 8 x G
+// (unit, slot) pairs, one per lane, by the same warp.  A group is ntile
+// consecutive tiles of one decoder (32 / (8 G) tiles, so every lane has an
+// activation to compute).
+template <int G, int L>
+__device__ __forceinline__ void hidden_group(const View& V, const DecDev& D, int t0, int ntile,
+                                             int xo, int sig_off, unsigned mask) {
+  constexpr int KS = (L + 3) / 4;
+  const Params& P = V.P;
+  const int lane = threadIdx.x & 31;
+  const int nh = D.n_hidden;
+  const int bs = lane >> 2, kq = lane & 3;
+  double bfr[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int d = 4 * ks + kq;
+    bfr[ks] = (bs < G && d < L) ? V.vec(bs, 4)[xo + d] : 0.0;
+  }
+  const int s0 = 2 * (lane & 3);
+  for (int t = t0; t < t0 + ntile; ++t) {
+    const int u = 8 * t + (lane >> 2);
+    const double b = u < nh ? __ldg(D.b1 + u) : 0.0;
+    double c[2] = {b, b};
+    const double* a = D.w1a + (size_t)t * KS * 32 + lane;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dmma_884(c, __ldg(a + ks * 32), bfr[ks]);
+    if (u < nh) {
+      if (s0 < G && ((mask >> s0) & 1u)) V.scr(s0)[P.scr_sig + sig_off + u] = c[0];
+      if (s0 + 1 < G && ((mask >> (s0 + 1)) & 1u)) V.scr(s0 + 1)[P.scr_sig + sig_off + u] = c[1];
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < ntile * 8 * G; it += WARP) {
+    const int s = it % G, u = 8 * t0 + it / G;
+    if (u >= nh || !((mask >> s) & 1u)) continue;
+    double* sc = V.scr(s);
+    double av, dv;
+    act_pair(D.act, sc[P.scr_sig + sig_off + u], av, dv, k_exp2_32);
+    sc[P.scr_sig + sig_off + u] = av;
+    sc[P.scr_dsig + sig_off + u] = dv;
+  }
+  __syncwarp();
+}
+
 // phase B: one decoder output (value + latent Jacobian row) for all slots.
 // Row sweep in CSR storage order (hyper.py:190-197), read from the
 // ELL-transposed copy of W2 (entry e of output o at [e][o]: a warp's lanes
@@ -271,10 +326,6 @@ __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int
 // K = 4 hidden units per mma, over the tile's k-block range; g = W2 sigma
 // accumulates on the FP64 pipe from the same B-operand loads.  Same sums as
 // hyper.py:190-197 in a different association order.
-__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
-}
 
 // Lean tensor-core tile: the host expands each tile's B-operand W2 values in
 // fragment order (vt[i][lane] = W2[o(lane)][4(kb_lo+i)+tig-k0(o)] or 0), the
@@ -643,11 +694,26 @@ __device__ __forceinline__ void eval_unit(const View& V, const BlockDev& B, unsi
         const int s = it >> 6, z = it & 63;
         if ((mask >> s) & 1u) V.scr(s)[(z < 32 ? P.scr_sig : P.scr_dsig) + nht + (z & 31)] = 0.0;
       }
-      for (int it = tid; it < nht; it += T) {
-        if (it < nhi)
-          hidden_unit<G, NI>(V, B.in, it, B.xoff, 0, mask);
-        else
-          hidden_unit<G, NG>(V, B.ga, it - nhi, B.xoff + NI, nhi, mask);
+      if (P.hid_dmma && (nhi == 0 || B.in.w1a) && (B.ga.n_hidden == 0 || B.ga.w1a)) {
+        // tensor-core tiles: groups of TPW tiles (32 activations per warp)
+        constexpr int TPW = G >= 4 ? 1 : 4 / G;
+        const int gi = ((nhi + 7) / 8 + TPW - 1) / TPW;
+        const int ti = (nhi + 7) / 8, tg = (B.ga.n_hidden + 7) / 8;
+        const int gg = (tg + TPW - 1) / TPW;
+        for (int q = warp; q < gi + gg; q += nw) {
+          if (q < gi)
+            hidden_group<G, NI>(V, B.in, q * TPW, min(TPW, ti - q * TPW), B.xoff, 0, mask);
+          else
+            hidden_group<G, NG>(V, B.ga, (q - gi) * TPW, min(TPW, tg - (q - gi) * TPW),
+                                B.xoff + NI, nhi, mask);
+        }
+      } else {
+        for (int it = tid; it < nht; it += T) {
+          if (it < nhi)
+            hidden_unit<G, NI>(V, B.in, it, B.xoff, 0, mask);
+          else
+            hidden_unit<G, NG>(V, B.ga, it - nhi, B.xoff + NI, nhi, mask);
+        }
       }
       __syncthreads();
       DDNM_MARK(V, 1);

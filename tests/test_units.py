@@ -60,7 +60,7 @@ def test_units_eval_match_whole_blocks(name, gpu_instances, goldens, monkeypatch
             assert rel(ds["con_val"], dw["con_val"]) < 1e-13
             assert rel(ds["con_jac"], dw["con_jac"]) < 1e-13
         assert rel(es.rho[k], ew.rho[k]) < 1e-12
-        assert rel(es.con[k], ew.con[k]) < 1e-13
+        assert rel(es.con[k], ew.con[k]) < 1e-12          # sum over blocks: cancellation
         assert abs(es.merit[k] - ew.merit[k]) <= 1e-12 * ew.merit[k]
         assert rel(es.step[k], ew.step[k]) < 1e-8
         assert rel(es.rho[k], g[f"d{k}_rho"]) < 1e-11 if f"d{k}_rho" in g else True

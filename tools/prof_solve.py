@@ -13,10 +13,11 @@ B = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 slots = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 inst = P.RomInstance.load(os.path.join(ROOT, "tests", "golden", f"{name}_artifacts.npz"))
 mu = P.seeded_parameters(B, seed=1000)
-for _ in range(2):
+for _ in range(3):
     r = P.solve_rom_batch(inst, mu, slots=slots)
 ctx = inst.context(-1, slots)
-print(f"slots/CTA {ctx.info.slots_per_cta}, CTAs {ctx.info.ctas}, smem {ctx.info.smem_bytes} B")
+print(f"slots/CTA {ctx.info.slots_per_cta}, CTAs {ctx.info.ctas}, smem {ctx.info.smem_bytes} B, "
+      f"units {ctx.info.eval_units}")
 prof = ctx.profile()
 tot = sum(prof.values()) or 1
 print({k: f"{100 * v / tot:.1f}%" for k, v in prof.items()})
