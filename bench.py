@@ -551,20 +551,35 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
 
 
 def subdomain_bench(P, torch, dist, world, dev, stream, flush, reps=3):
-    """The subdomain-sharded path: the 16-block dd16
-    instance, DD_BATCH seeded mu, blocks sharded over the ranks with an
-    exchange of the block packets every SQP round -- an NCCL all-gather after
-    the evaluation kernel, or the evaluation kernel storing the packets into
-    every rank's buffer over peer memory ("p2p", CUDA IPC) -- strong scaling
-    (the same batch at every N).  Device-timed with CUDA events, max over
-    ranks."""
-    inst = P.RomInstance.load(DD_ARTIFACT)
-    mu = P.seeded_parameters(DD_BATCH, seed=2000)
-    out = {"workload": "dd16: 60x60 4x4 NM-ROM WFPC collocation HR, n=(8,5), n_C=40, "
-                       "45 rows/sub (config 4's layout at a trainable grid)",
-           "batch": DD_BATCH, "scaling": "strong", "ranks": world,
+    """dd16 (config 4's layout at 60x60) and, when its artifacts exist, config 4
+    itself (960x960, 4x4, 256 mu) through the subdomain-sharded rounds."""
+    out = {"dd16": _subdomain_one(P, torch, dist, world, dev, stream, flush, DD_ARTIFACT,
+                                  DD_BATCH, "dd16: 60x60 4x4 NM-ROM WFPC collocation HR, "
+                                  "n=(8,5), n_C=40, 45 rows/sub (config 4's layout at a "
+                                  "trainable grid)", reps)}
+    c4 = os.path.join(ROOT, "tests", "golden", "c4_nm_artifacts.npz")
+    if os.path.exists(c4):
+        out["config4"] = _subdomain_one(P, torch, dist, world, dev, stream, flush, c4, 256,
+                                        "config4: 960x960 4x4 NM-ROM WFPC, n=(8,5), n_C=40, "
+                                        "2304 rows/sub, blocks as evaluation units", 2,
+                                        transports=("nccl",))
+    return out
+
+
+def _subdomain_one(P, torch, dist, world, dev, stream, flush, path, batch, desc, reps,
+                   transports=("nccl", "p2p")):
+    """The subdomain-sharded path: blocks sharded over the
+    ranks with an exchange of the block packets every SQP round -- an NCCL
+    all-gather after the evaluation kernel, or the evaluation kernel storing
+    the packets into every rank's buffer over peer memory ("p2p", CUDA IPC)
+    -- the steps sharded by mu (each mu's KKT on one rank, trial points
+    all-gathered), strong scaling (the same batch at every N).  Device-timed
+    with CUDA events, max over ranks."""
+    inst = P.RomInstance.load(path)
+    mu = P.seeded_parameters(batch, seed=2000)
+    out = {"workload": desc, "batch": batch, "scaling": "strong", "ranks": world,
            "kernels": "k_dd_eval + k_dd_step per SQP round"}
-    for transport in ("nccl", "p2p"):
+    for transport in transports:
         try:
             P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport)   # warm-up
             times, res = [], None
@@ -585,7 +600,7 @@ def subdomain_bench(P, torch, dist, world, dev, stream, flush, reps=3):
                 t = torch.tensor([ms], device=dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
-            out[transport] = {"solves_per_s": DD_BATCH / (ms / 1e3), "ms_per_batch": ms,
+            out[transport] = {"solves_per_s": batch / (ms / 1e3), "ms_per_batch": ms,
                               "rounds": int(res.rounds), "mean_n_iter": float(res.n_iter.mean()),
                               "status_counts": np.bincount(res.status, minlength=4).tolist()}
         except Exception as exc:      # reported per transport, never fatal

@@ -324,6 +324,20 @@ int ddnm_dd_step(ddnm_dd* dd, const double* d_gathered, int32_t nranks,
 int ddnm_dd_eval_p2p(ddnm_dd* dd, double* const* peers, int32_t nranks, int32_t rank,
                      int64_t pk_stride, void* stream);
 
+/* Trial records: per mu [running flag, x_trial[n_D]] (+ padding), the input
+ * of the next ddnm_dd_eval.  By default the handle owns them (B records) and
+ * ddnm_dd_step advances every mu.  Sharding the steps by mu (each mu solved
+ * by one rank; the KKT work divides by the rank count): every rank gives a
+ * buffer of cap >= B records, the same slice size on every rank, and its mu
+ * slice [mu_lo, mu_hi); ddnm_dd_step then advances only that slice and writes
+ * its records, and the caller all-gathers the records (rank-major chunks of
+ * cap / nranks records) before the next ddnm_dd_eval; n_active counts the
+ * slice (sum it over the ranks).  The final results are written by the
+ * owning rank only: gather the slices' rows. */
+int ddnm_dd_trial_len(const ddnm_dd* dd, int64_t* len);
+int ddnm_dd_set_trials(ddnm_dd* dd, double* d_trials, int64_t cap, int32_t mu_lo,
+                       int32_t mu_hi, void* stream);
+
 int ddnm_dd_end(ddnm_dd* dd);
 
 /* CUDA IPC of a device buffer between the processes of one node (64-byte

@@ -812,8 +812,14 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // (c0_ls: 138 -> 150 ms with the attempt), so they go straight to the
   // dense LU there.  DDNM_KKT_BLOCK_MAX overrides.
   P.kkt_block_max = a->map_kind == DDNM_MAP_AUTOENCODER ? 96 : 32;
-  // hidden layer on the FP64 tensor cores unless DDNM_HIDDEN_SCALAR=1
-  P.hid_dmma = getenv("DDNM_HIDDEN_SCALAR") ? 0 : 1;
+  // hidden pre-activation: per-unit DFMA (default) or FP64 tensor-core tiles
+  // (DDNM_HIDDEN_DMMA=1, hidden_range).  Measured (profiles/r2e_hidden_ab.log):
+  // the tiles are 3-5% slower at config 2 (36.1 vs 34.4-35.1 ms per 4096 mu)
+  // and 11% at config 3 (156.6 vs 140.1 ms per 1024 mu, 2 slots: the B
+  // operand's 8 slot columns hold 2): the pre-activation is ~1/4 of the
+  // phase's FP64 work (the activations dominate) and the tiles add a
+  // shared-memory round trip of Z between the mma chains and the activations.
+  P.hid_dmma = getenv("DDNM_HIDDEN_DMMA") ? 1 : 0;
   if (const char* kb = getenv("DDNM_KKT_BLOCK_MAX")) P.kkt_block_max = std::min(96, atoi(kb));
   P.total_rows = row_off;
   P.tot_iout = iout; P.tot_gout = gout; P.tot_R = Roff; P.tot_cjac = cjoff;
@@ -1532,6 +1538,7 @@ struct ddnm_dd {
   double* gJ = nullptr;
   double* gJg = nullptr;
   double* kkt_g = nullptr;
+  double* trials = nullptr;       // own trial records [B][rec] (until ddnm_dd_set_trials)
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
 };
 
@@ -1543,11 +1550,13 @@ int eb_span(const ddnm_ctx* c, int lo, int hi, int* off) {
   return (hi < P.nb ? P.blk[hi].eb_off : P.eb_rho) - *off;
 }
 
-int dd_run(ddnm_dd* d, const void* kern, cudaStream_t s, int32_t* n_active) {
+int dd_run(ddnm_dd* d, const void* kern, cudaStream_t s, int32_t* n_active, int ctas = 0) {
   ddnm_ctx* c = d->c;
   CUDA_TRY(cudaMemsetAsync(d->active, 0, sizeof(int), s));
   void* args[] = {&d->P};
-  CUDA_TRY(cudaLaunchKernel(kern, dim3(d->ctas), dim3(c->threads), args, c->smem, s));
+  if (ctas == 0) ctas = d->ctas;
+  if (ctas > 0)
+    CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(c->threads), args, c->smem, s));
   if (n_active) {
     int h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, d->active, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1601,6 +1610,9 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
       cudaMalloc(&d->ecur, (size_t)B * c->P.eb_size * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&d->active, sizeof(int)) != cudaSuccess)
     return bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve state"));
+  const int rec = (c->P.n_D + 1 + 1) & ~1;
+  if (cudaMalloc(&d->trials, (size_t)B * rec * sizeof(double)) != cudaSuccess)
+    return bail(fail(DDNM_ENOMEM, "cannot allocate the trial records"));
   Params& P = d->P;
   P = c->P;
   P.B = B;
@@ -1630,6 +1642,10 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   P.dd_vec = d->vec;
   P.dd_ecur = d->ecur;
   P.dd_active = d->active;
+  P.dd_trial = d->trials;
+  P.dd_rec = rec;
+  P.dd_mu_lo = 0;
+  P.dd_mu_hi = B;
   if ((rc = fill_nan(s, o->merit_hist, (size_t)B * (cfg->max_iter + 1)))) return bail(rc);
   if ((rc = fill_nan(s, o->obj_hist, (size_t)B * (cfg->max_iter + 1)))) return bail(rc);
   if ((rc = fill_nan(s, o->alpha_hist, (size_t)B * cfg->max_iter))) return bail(rc);
@@ -1733,7 +1749,44 @@ int ddnm_dd_step(ddnm_dd* d, const double* d_gathered, int32_t nranks, const int
   d->P.dd_nranks = nranks;
   d->P.pk_stride = (int)pk_stride;
   for (int r = 0; r <= nranks; ++r) d->P.dd_bnd[r] = bounds[r];
-  return dd_run(d, d->c->K.dd_step, s, n_active);
+  const int G = d->c->P.G;
+  const int n = d->P.dd_mu_hi - d->P.dd_mu_lo;
+  const int rc = dd_run(d, d->c->K.dd_step, s, nullptr, n > 0 ? (n + G - 1) / G : -1);
+  if (rc) return rc;
+  if (n_active) {
+    int h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, d->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *n_active = h;
+  }
+  return 0;
+}
+
+int ddnm_dd_trial_len(const ddnm_dd* d, int64_t* len) {
+  if (!d || !len) return fail(DDNM_EINVAL, "null argument");
+  *len = d->P.dd_rec;
+  return 0;
+}
+
+int ddnm_dd_set_trials(ddnm_dd* d, double* d_trials, int64_t cap, int32_t mu_lo, int32_t mu_hi,
+                       void* stream) {
+  if (!d || !d_trials) return fail(DDNM_EINVAL, "null argument");
+  if (cap < d->B) return fail(DDNM_EINVAL, "trial buffer holds fewer records than the batch");
+  if (mu_lo < 0 || mu_hi < mu_lo || mu_hi > d->B) return fail(DDNM_EINVAL, "bad mu slice");
+  CUDA_TRY(cudaSetDevice(d->c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rec = (size_t)d->P.dd_rec;
+  if (d_trials != d->P.dd_trial) {
+    CUDA_TRY(cudaMemcpyAsync(d_trials, d->P.dd_trial, (size_t)d->B * rec * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+    if (cap > d->B)
+      CUDA_TRY(cudaMemsetAsync(d_trials + (size_t)d->B * rec, 0,
+                               (size_t)(cap - d->B) * rec * sizeof(double), s));
+  }
+  d->P.dd_trial = d_trials;
+  d->P.dd_mu_lo = mu_lo;
+  d->P.dd_mu_hi = mu_hi;
+  return 0;
 }
 
 int ddnm_dd_end(ddnm_dd* d) {
@@ -1744,7 +1797,7 @@ int ddnm_dd_end(ddnm_dd* d) {
   if (d->vec) cudaFree(d->vec);
   if (d->ecur) cudaFree(d->ecur);
   if (d->active) cudaFree(d->active);
-  for (double* p : {d->gbv, d->gJ, d->gJg, d->kkt_g})
+  for (double* p : {d->gbv, d->gJ, d->gJg, d->kkt_g, d->trials})
     if (p) cudaFree(p);
   delete d;
   return 0;

@@ -223,6 +223,11 @@ struct Params {
   int pk_stride, dd_nranks, dd_init;
   int dd_bnd[MAXB + 1];   // block range of rank r: [dd_bnd[r], dd_bnd[r+1])
   int* dd_active;         // k_dd_step: count of slots still running
+  // trial records [mu][dd_rec]: running flag, then the trial point x_t (the
+  // next evaluation's input on every rank); k_dd_step writes the records of
+  // the mu it advances, [dd_mu_lo, dd_mu_hi) (its slice), k_dd_eval reads all
+  double* dd_trial;
+  int dd_rec, dd_mu_lo, dd_mu_hi;
   // peer-memory all-gather fused into k_dd_eval: when dd_npeers > 0 the
   // packets go straight to every rank's gathered buffer (NVLink stores)
   double* dd_peers[MAXB];

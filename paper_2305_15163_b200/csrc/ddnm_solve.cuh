@@ -113,13 +113,12 @@ __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
 // m8n8k4 chain, Z[unit][slot] = b1[unit] + sum_d W1[unit][d] x_slot[d]
 // (A = the units' W1 rows, B = the slots' latent vectors, K = latent dim in
 // steps of 4, C initialised with b1: hyper.py:184-188 / autoencoder.py:134-140
-// with the products summed by the tensor core), written to the sigma array;
-// then swish / swish' (autoencoder.py:31-45) of the group's 8 x G
-// (unit, slot) pairs, one per lane, by the same warp.  A group is ntile
-// consecutive tiles of one decoder (32 / (8 G) tiles, so every lane has an
-// activation to compute).
+// with the products summed by the tensor core), written to the sigma array.
+// A warp takes a contiguous range of tiles of one decoder: all their mma
+// chains first (independent, in flight together), then swish / swish'
+// (autoencoder.py:31-45) of the range's (unit, slot) pairs, one per lane.
 template <int G, int L>
-__device__ __forceinline__ void hidden_group(const View& V, const DecDev& D, int t0, int ntile,
+__device__ __forceinline__ void hidden_range(const View& V, const DecDev& D, int t0, int t1,
                                              int xo, int sig_off, unsigned mask) {
   constexpr int KS = (L + 3) / 4;
   const Params& P = V.P;
@@ -133,7 +132,11 @@ __device__ __forceinline__ void hidden_group(const View& V, const DecDev& D, int
     bfr[ks] = (bs < G && d < L) ? V.vec(bs, 4)[xo + d] : 0.0;
   }
   const int s0 = 2 * (lane & 3);
-  for (int t = t0; t < t0 + ntile; ++t) {
+  const bool w0 = s0 < G && ((mask >> s0) & 1u), w1 = s0 + 1 < G && ((mask >> (s0 + 1)) & 1u);
+  double* z0 = w0 ? V.scr(s0) + P.scr_sig + sig_off : nullptr;
+  double* z1 = w1 ? V.scr(s0 + 1) + P.scr_sig + sig_off : nullptr;
+#pragma unroll 4
+  for (int t = t0; t < t1; ++t) {
     const int u = 8 * t + (lane >> 2);
     const double b = u < nh ? __ldg(D.b1 + u) : 0.0;
     double c[2] = {b, b};
@@ -141,21 +144,21 @@ __device__ __forceinline__ void hidden_group(const View& V, const DecDev& D, int
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) dmma_884(c, __ldg(a + ks * 32), bfr[ks]);
     if (u < nh) {
-      if (s0 < G && ((mask >> s0) & 1u)) V.scr(s0)[P.scr_sig + sig_off + u] = c[0];
-      if (s0 + 1 < G && ((mask >> (s0 + 1)) & 1u)) V.scr(s0 + 1)[P.scr_sig + sig_off + u] = c[1];
+      if (w0) z0[u] = c[0];
+      if (w1) z1[u] = c[1];
     }
   }
   __syncwarp();
-  for (int it = lane; it < ntile * 8 * G; it += WARP) {
+  const int u_hi = min(8 * t1, nh);
+  for (int it = lane; it < (u_hi - 8 * t0) * G; it += WARP) {
     const int s = it % G, u = 8 * t0 + it / G;
-    if (u >= nh || !((mask >> s) & 1u)) continue;
+    if (!((mask >> s) & 1u)) continue;
     double* sc = V.scr(s);
     double av, dv;
     act_pair(D.act, sc[P.scr_sig + sig_off + u], av, dv, k_exp2_32);
     sc[P.scr_sig + sig_off + u] = av;
     sc[P.scr_dsig + sig_off + u] = dv;
   }
-  __syncwarp();
 }
 
 // phase B: one decoder output (value + latent Jacobian row) for all slots.
@@ -695,18 +698,15 @@ __device__ __forceinline__ void eval_unit(const View& V, const BlockDev& B, unsi
         if ((mask >> s) & 1u) V.scr(s)[(z < 32 ? P.scr_sig : P.scr_dsig) + nht + (z & 31)] = 0.0;
       }
       if (P.hid_dmma && (nhi == 0 || B.in.w1a) && (B.ga.n_hidden == 0 || B.ga.w1a)) {
-        // tensor-core tiles: groups of TPW tiles (32 activations per warp)
-        constexpr int TPW = G >= 4 ? 1 : 4 / G;
-        const int gi = ((nhi + 7) / 8 + TPW - 1) / TPW;
+        // tensor-core tiles: each warp a contiguous tile range of each decoder
         const int ti = (nhi + 7) / 8, tg = (B.ga.n_hidden + 7) / 8;
-        const int gg = (tg + TPW - 1) / TPW;
-        for (int q = warp; q < gi + gg; q += nw) {
-          if (q < gi)
-            hidden_group<G, NI>(V, B.in, q * TPW, min(TPW, ti - q * TPW), B.xoff, 0, mask);
-          else
-            hidden_group<G, NG>(V, B.ga, (q - gi) * TPW, min(TPW, tg - (q - gi) * TPW),
-                                B.xoff + NI, nhi, mask);
-        }
+        const int ri = (ti + nw - 1) / nw, rg = (tg + nw - 1) / nw;
+        if (warp * ri < ti)
+          hidden_range<G, NI>(V, B.in, warp * ri, min(ti, (warp + 1) * ri), B.xoff, 0, mask);
+        // interface ranges taken by the warps in reverse order (balance)
+        const int wg = nw - 1 - warp;
+        if (wg * rg < tg)
+          hidden_range<G, NG>(V, B.ga, wg * rg, min(tg, (wg + 1) * rg), B.xoff + NI, nhi, mask);
       } else {
         for (int it = tid; it < nht; it += T) {
           if (it < nhi)
@@ -2269,14 +2269,15 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_solve(const __grid_cons
 // so all ranks hold bit-identical states and results.  CTA c owns mu
 // c*G .. c*G+G-1 for the whole solve (no work counter: rounds are global).
 
+// slot s of this CTA <-> mu = mu0 + blockIdx.x * G + s (valid below mu_hi)
 template <int G>
-__device__ __forceinline__ unsigned dd_load_state(const View& V, int* mu_of) {
+__device__ __forceinline__ unsigned dd_load_state(const View& V, int* mu_of, int mu0, int mu_hi) {
   const Params& P = V.P;
   SlotState* st = V.st();
   __shared__ unsigned s_m;
   if (threadIdx.x < G) {
-    const int s = threadIdx.x, mu = blockIdx.x * G + s;
-    if (mu < P.B) st[s] = P.dd_st[mu];
+    const int s = threadIdx.x, mu = mu0 + blockIdx.x * G + s;
+    if (mu < mu_hi) st[s] = P.dd_st[mu];
     else { st[s].mu = -1; st[s].phase = PH_IDLE; }
     mu_of[s] = mu;
   }
@@ -2290,19 +2291,48 @@ __device__ __forceinline__ unsigned dd_load_state(const View& V, int* mu_of) {
   return s_m;
 }
 
+// trial record of slot s (warp-cooperative over the CTA): running flag and
+// the trial point the next evaluation reads
+__device__ __forceinline__ void dd_write_trial(const View& V, int s, int mu) {
+  const Params& P = V.P;
+  double* r = P.dd_trial + (size_t)mu * P.dd_rec;
+  const SlotState& S = V.st()[s];
+  const bool run = S.phase == PH_INIT || S.phase == PH_TRIAL;
+  for (int j = threadIdx.x; j < P.n_D + 1; j += blockDim.x)
+    r[j] = j == 0 ? (run ? 1.0 : 0.0) : V.vec(s, 4)[j - 1];
+}
+
 template <int G, int NI, int NG>
 __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_eval(const __grid_constant__ Params P) {
   View V(P, ddnm_smem);
   const int tid = threadIdx.x, T = blockDim.x;
   __shared__ int s_mu[G];
   __shared__ int s_ebi[G];
-  const unsigned mask = dd_load_state<G>(V, s_mu);
+  __shared__ unsigned s_m;
+  // running flags and trial points from the trial records (every rank holds
+  // all of them after the records' all-gather)
+  SlotState* st = V.st();
+  if (tid < G) {
+    const int s = tid, mu = blockIdx.x * G + s;
+    st[s] = SlotState{};
+    st[s].mu = mu < P.B ? mu : -1;
+    st[s].phase = (mu < P.B && P.dd_trial[(size_t)mu * P.dd_rec] != 0.0) ? PH_TRIAL : PH_IDLE;
+    s_mu[s] = mu;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned m = 0;
+    for (int s = 0; s < G; ++s) if (st[s].phase == PH_TRIAL) m |= 1u << s;
+    s_m = m;
+  }
+  __syncthreads();
+  const unsigned mask = s_m;
   if (mask == 0) return;
   zero_slots(V);
   if (tid < G) s_ebi[tid] = 0;
   for (int s = 0; s < G; ++s) {
     if (!((mask >> s) & 1u)) continue;
-    const double* src = P.dd_vec + ((size_t)s_mu[s] * 8 + 4) * P.nK;
+    const double* src = P.dd_trial + (size_t)s_mu[s] * P.dd_rec + 1;
     for (int j = tid; j < P.n_D; j += T) V.vec(s, 4)[j] = src[j];
   }
   __syncthreads();
@@ -2334,6 +2364,9 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
   View V(P, ddnm_smem);
   SlotState* st = V.st();
   const int tid = threadIdx.x, T = blockDim.x, warp = tid >> 5;
+  // this rank's mu slice (all mu at the start); per-mu scratch is indexed by mu
+  const int mu0 = P.dd_init ? 0 : P.dd_mu_lo, mu_hi = P.dd_init ? P.B : P.dd_mu_hi;
+  V.gslot0 = mu0 + blockIdx.x * G;
   __shared__ int s_mu[G];
   __shared__ int s_cur[G];
   __shared__ int s_ebi[G];
@@ -2342,7 +2375,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
   if (P.dd_init) {
     // new batch: every slot takes its mu, boundary values, x0 / lam0
     if (tid < G) {
-      const int mu = blockIdx.x * G + tid;
+      const int mu = mu0 + blockIdx.x * G + tid;
       s_mu[tid] = mu;
       st[tid] = SlotState{};
       if (mu < P.B) slot_reset(st[tid], mu);
@@ -2359,13 +2392,15 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
       double* dst = P.dd_vec + (size_t)s_mu[s] * 8 * P.nK;
       for (int i = tid; i < 8 * P.nK; i += T) dst[i] = V.vec(s, 0)[i];
     }
+    for (int s = 0; s < G; ++s)
+      if (st[s].mu >= 0) dd_write_trial(V, s, s_mu[s]);
     if (tid < G && st[tid].mu >= 0) {
       P.dd_st[s_mu[tid]] = st[tid];
       atomicAdd(P.dd_active, 1);
     }
     return;
   }
-  const unsigned mask = dd_load_state<G>(V, s_mu);
+  const unsigned mask = dd_load_state<G>(V, s_mu, mu0, mu_hi);
   if (mask == 0) return;
   if (tid == 0) s_kkts = 0;
   zero_slots(V);
@@ -2409,6 +2444,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
       if (s_cur[s] != 0 || s_ebi[s] == 0)
         for (int i = tid; i < P.eb_size; i += T) ec[i] = e[i];
     }
+    dd_write_trial(V, s, mu);
   }
   if (tid < G && ((mask >> tid) & 1u)) {
     P.dd_st[s_mu[tid]] = st[tid];

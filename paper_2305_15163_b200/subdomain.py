@@ -11,9 +11,15 @@ only places them.  So with many subdomains the blocks are split across ranks
    mu's trial point and packs, per mu, the block pieces the SQP needs (Gram
    block H_b = R_bᵀR_b, R_bᵀr_b, cval_b, cjac_b, r_bᵀr_b);
 2. an all-gather of those packets (NCCL between GPUs, gloo in the CPU tests);
-3. ``step``: every rank assembles all blocks' pieces in block order and runs
-   the same Armijo decision / KKT solve / trial update (sqp.py:230-299), so
-   all ranks hold bit-identical iterates and results.
+3. ``step``: the mu batch is split into contiguous slices, one per rank;
+   each rank assembles, for the mu of its slice, all blocks' pieces in block
+   order and runs the Armijo decision / KKT solve / trial update
+   (sqp.py:230-299) -- every mu is solved by exactly one rank, so results
+   are the one-rank results bit for bit and the KKT work (248 x 248 at
+   config 4) divides by the rank count instead of being repeated;
+4. an all-gather of the slices' trial records (running flag + the next trial
+   point, n_D + 1 doubles per mu), which the next ``eval`` reads on every
+   rank.  At the end the slices' results are all-gathered too.
 
 Rounds are batch-synchronous: a mu that finished idles until the batch does.
 The round engine is pluggable: :class:`DeviceRoundEngine` drives the
@@ -70,10 +76,13 @@ class DeviceRoundEngine:
     def _stream(self):
         return C.c_void_p(self.torch.cuda.current_stream(self.dev).cuda_stream)
 
-    def begin(self, mu, cfg: SqpConfig, x0, lam0, lo: int, hi: int) -> int:
+    def begin(self, mu, cfg: SqpConfig, x0, lam0, lo: int, hi: int, rows: int = 0) -> int:
+        """``rows`` >= B: output rows allocated (slices of equal size for the
+        final all-gather); the device writes the first B."""
         from .driver import _cfg_struct
         t = self.torch
         B = mu.shape[0]
+        R = max(rows, B)
         nD, nC, K = self.inst.n_primal, self.inst.n_mult, cfg.max_iter
         f64 = dict(dtype=t.float64, device=self.dev)
         i32 = dict(dtype=t.int32, device=self.dev)
@@ -81,11 +90,12 @@ class DeviceRoundEngine:
         self.x0 = None if x0 is None else t.as_tensor(np.asarray(x0, float).reshape(B, nD), **f64)
         self.lam0 = None if lam0 is None else t.as_tensor(np.asarray(lam0, float).reshape(B, nC), **f64)
         self.out = dict(
-            x=t.empty(B, nD, **f64), lam=t.empty(B, nC, **f64), n_iter=t.zeros(B, **i32),
-            n_evals=t.zeros(B, **i32), status=t.zeros(B, **i32), n_reg=t.zeros(B, **i32),
-            merit=t.empty(B, **f64), objective=t.empty(B, **f64),
-            merit_hist=t.empty(B, K + 1, **f64), obj_hist=t.empty(B, K + 1, **f64),
-            alpha_hist=t.empty(B, K, **f64), x0=t.empty(B, nD, **f64), lam0=t.empty(B, nC, **f64))
+            x=t.zeros(R, nD, **f64), lam=t.zeros(R, nC, **f64), n_iter=t.zeros(R, **i32),
+            n_evals=t.zeros(R, **i32), status=t.zeros(R, **i32), n_reg=t.zeros(R, **i32),
+            merit=t.zeros(R, **f64), objective=t.zeros(R, **f64),
+            merit_hist=t.zeros(R, K + 1, **f64), obj_hist=t.zeros(R, K + 1, **f64),
+            alpha_hist=t.zeros(R, K, **f64), x0=t.zeros(R, nD, **f64), lam0=t.zeros(R, nC, **f64))
+        self.B = B
         so = N.SolveOut()
         for k, v in self.out.items():
             ct = C.c_int32 if v.dtype == t.int32 else C.c_double
@@ -101,6 +111,26 @@ class DeviceRoundEngine:
             C.byref(n)))
         self.h = h
         return int(n.value)
+
+    def trial_len(self) -> int:
+        n = C.c_int64()
+        N.check(N.lib().ddnm_dd_trial_len(self.h, C.byref(n)))
+        return int(n.value)
+
+    def set_trials(self, trials, mu_lo: int, mu_hi: int) -> None:
+        """Trial records live in ``trials`` ([cap][trial_len], cap >= B);
+        ``step`` then advances only mu in [mu_lo, mu_hi)."""
+        cap = trials.numel() // self.trial_len()
+        N.check(N.lib().ddnm_dd_set_trials(self.h, C.c_void_p(trials.data_ptr()), cap, mu_lo,
+                                           mu_hi, self._stream()))
+
+    def gather_results(self, rank: int, chunk: int, world: int, group) -> None:
+        """Every rank's slice rows of every output to every rank."""
+        for v in self.out.values():
+            row = v.numel() // v.shape[0]
+            flat = v.view(-1)
+            _all_gather(flat, flat[rank * chunk * row:(rank + 1) * chunk * row].clone(), world,
+                        group)
 
     def eval(self, packets, stride: int) -> None:
         N.check(N.lib().ddnm_dd_eval(self.h, C.c_void_p(packets.data_ptr()), stride,
@@ -122,7 +152,7 @@ class DeviceRoundEngine:
     def finish(self, mu):
         from .driver import BatchResult
         self.torch.cuda.current_stream(self.dev).synchronize()
-        out = {k: v.cpu().numpy() for k, v in self.out.items()}
+        out = {k: v[:self.B].cpu().numpy() for k, v in self.out.items()}
         N.lib().ddnm_dd_end(self.h)
         self.h = None
         return BatchResult(mu=mu, tol=self.cfg.tol, counters=self.ctx.counters(), **out)
@@ -154,7 +184,16 @@ class ShardedSolve:
         self.stride = max(self.eng.packet_len(self.bounds[r], self.bounds[r + 1])
                           for r in range(world))
         self.lo, self.hi = self.bounds[rank], self.bounds[rank + 1]
-        self.active = self.eng.begin(mu, cfg, x0, lam0, self.lo, self.hi)
+        # mu slice of this rank's steps: equal slices (the all-gathers need
+        # equal chunks), the last ones may run past B (empty records)
+        self.chunk = -(-self.B // world)
+        self.mu_lo = min(self.B, rank * self.chunk)
+        self.mu_hi = min(self.B, (rank + 1) * self.chunk)
+        self.active = self.eng.begin(mu, cfg, x0, lam0, self.lo, self.hi,
+                                     rows=world * self.chunk)
+        self.rec = self.eng.trial_len()
+        self.trials = self.eng.buffer(world * self.chunk * self.rec)
+        self.eng.set_trials(self.trials, self.mu_lo, self.mu_hi)
         self.packets = self.eng.buffer(self.B * self.stride)
         self.rounds = 0
         # every round evaluates one trial point per running mu; a solve takes
@@ -171,19 +210,28 @@ class ShardedSolve:
         addresses valid on this GPU) over peer memory."""
         self.eng.eval_p2p(peers, self.rank, self.stride)
 
-    def step(self, gathered, count: bool = True) -> int:
-        """One SQP round.  ``count=False`` skips the host read of the running
-        count (no stream synchronisation); rounds after every mu finished do
-        nothing, so a caller may check only every few rounds."""
+    def step(self, gathered, count: bool = True):
+        """One SQP round of this rank's mu slice: returns the slice's running
+        count (``count=False``: None, no stream synchronisation; rounds after
+        every mu finished do nothing, so a caller may check only every few
+        rounds).  With several ranks the caller then all-gathers
+        :meth:`trial_chunk` into :attr:`trials` and sums the counts."""
         n = self.eng.step(gathered, self.world, self.bounds, self.stride, count)
-        if n is not None:
-            self.active = n
         self.rounds += 1
-        if self.active and self.rounds >= self.max_rounds:
+        if n is not None and n and self.rounds >= self.max_rounds:
             raise RuntimeError("sharded solve did not terminate within the SQP round bound")
-        return self.active
+        return n
 
-    def result(self):
+    def trial_chunk(self):
+        """This rank's slice of the trial records (its all-gather input)."""
+        r = self.rank
+        return self.trials[r * self.chunk * self.rec:(r + 1) * self.chunk * self.rec]
+
+    def result(self, group=None):
+        """The batch result; with several ranks every rank's slice rows are
+        all-gathered first (collective over ``group``)."""
+        if self.world > 1 and group is not False:
+            self.eng.gather_results(self.rank, self.chunk, self.world, group)
         return self.eng.finish(self.mu)
 
 
@@ -307,6 +355,7 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
         bufs = [g1, g1]
         ptrs = [[g1.data_ptr()]] * 2
     flag = sh.eng.buffer(1) if transport == "p2p" and world > 1 else None
+    cnt = sh.eng.buffer(1) if world > 1 else None
     done = False
     try:
         while active:
@@ -321,7 +370,17 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
                     _all_gather(gathered, packets, world, group)
             # the running count is read (one host sync) every CHECK rounds;
             # rounds after the last mu finished are empty launches
-            active = sh.step(gathered, count=sh.rounds % CHECK == CHECK - 1)
+            check = sh.rounds % CHECK == CHECK - 1
+            n = sh.step(gathered, count=check)
+            if world > 1:
+                # every rank's next trial points (its slice) to every rank
+                _all_gather(sh.trials, sh.trial_chunk().clone(), world, group)
+                if check:
+                    cnt.fill_(float(n))
+                    dist.all_reduce(cnt, group=group)
+                    n = int(cnt.item())
+            if check:
+                active = n
         done = True
     finally:
         if own:
@@ -335,7 +394,7 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
                 b.close()
         # on the error path the exported buffers are leaked rather than freed:
         # a peer may still have them mapped
-    res = sh.result()
+    res = sh.result(group)
     if hasattr(res, "seconds"):
         res.seconds = time.perf_counter() - t0
         res.rounds = sh.rounds

@@ -7,12 +7,20 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "c3s_nm", "dd16_nm", "c3_nm", "tiny42_nm"]
+NAMES = ["tiny_nm", "tiny_ls", "c0_nm", "c0_ls", "c3s_nm", "dd16_nm", "c3_nm", "c4_nm",
+         "tiny42_nm"]
 # BASELINE configs 3 (480^2) and 4 (960^2): the oracle takes seconds per
 # solve there, so whole-solve oracle comparisons use the first N_BIG mu
 # (the device is still checked against the reference goldens on all of them)
 BIG = {"c3_nm", "c4_nm"}
 N_BIG = 4
+# per-name oracle budgets (an oracle solve takes ~7 s at config 3, ~60 s at config 4)
+N_ORACLE = {"c3_nm": 4, "c4_nm": 2}
+
+
+def n_detail(g):
+    """mu with per-block detail goldens (d<k>_*): 3, or 1 for config 4."""
+    return sum(1 for k in range(3) if f"d{k}_rho" in g)
 # SRPC coupling and gappy HR variants (SURVEY.md §8(f3))
 VARIANTS = ["tiny_nmg", "tiny_srpc", "tiny_lsg", "tiny_lss", "c0_nmg", "c0_srpc", "c0_lsg",
             "c0_lss"]

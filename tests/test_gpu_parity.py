@@ -10,7 +10,7 @@ import pytest
 import paper_2305_15163_b200 as P
 from oracle import ddnm_oracle as O
 
-from .conftest import BIG, N_BIG, NAMES
+from .conftest import BIG, N_BIG, N_ORACLE, NAMES, n_detail
 from .test_oracle_golden import merit_noise, rel
 
 pytestmark = pytest.mark.gpu
@@ -55,8 +55,9 @@ def test_eval_blocks_match_oracle(name, gpu_instances, oracle_instances, goldens
 @pytest.mark.parametrize("name", NAMES)
 def test_eval_matches_reference_golden(name, gpu_instances, goldens):
     inst, g = gpu_instances[name], goldens[name]
-    ev = P.eval_gradients_batch(inst, g["mu"][:3], g["x0"][:3], g["lam0"][:3])
-    for k in range(3):
+    nd = n_detail(g)
+    ev = P.eval_gradients_batch(inst, g["mu"][:nd], g["x0"][:nd], g["lam0"][:nd])
+    for k in range(nd):
         assert rel(ev.rho[k], g[f"d{k}_rho"]) < 1e-11
         assert rel(ev.step[k, :ev.rho.shape[1]], g[f"d{k}_step"]) < 1e-8
         for b in range(inst.n_blocks):
@@ -79,7 +80,7 @@ def test_solve_batch_matches_oracle(name, gpu_instances, oracle_instances, golde
     for k in range(mu.shape[0]):
         assert rel(res.x[k], g["x"][k]) < 1e-9, k          # the reference itself, every mu
         assert rel(res.lam[k], g["lam"][k]) < 1e-9, k
-        if name in BIG and k >= N_BIG:
+        if k >= N_ORACLE.get(name, mu.shape[0]):
             continue
         r = O.solve(oi, *mu[k])
         assert rel(res.x0[k], g["x0"][k]) < 1e-13

@@ -8,7 +8,7 @@ import pytest
 
 from oracle import ddnm_oracle as O
 
-from .conftest import BIG, N_BIG, NAMES
+from .conftest import BIG, N_BIG, N_ORACLE, NAMES, n_detail
 
 
 def rel(a, b):
@@ -30,7 +30,7 @@ def test_init_guess_matches_reference(name, oracle_instances, goldens):
 @pytest.mark.parametrize("name", NAMES)
 def test_eval_pieces_match_reference(name, oracle_instances, goldens):
     inst, g = oracle_instances[name], goldens[name]
-    for k in range(3):
+    for k in range(n_detail(g)):
         a, lam = g["mu"][k]
         bbs = inst.boundary(a, lam)
         ev = O.eval_gradients(inst, bbs, g["x0"][k], g["lam0"][k])
@@ -60,7 +60,7 @@ def test_eval_pieces_match_reference(name, oracle_instances, goldens):
 @pytest.mark.parametrize("name", NAMES)
 def test_kkt_step_matches_reference(name, oracle_instances, goldens):
     inst, g = oracle_instances[name], goldens[name]
-    for k in range(3):
+    for k in range(n_detail(g)):
         a, lam = g["mu"][k]
         ev = O.eval_gradients(inst, inst.boundary(a, lam), g["x0"][k], g["lam0"][k])
         s, sl, reg = O.solve_kkt(inst, ev)
@@ -87,7 +87,7 @@ def test_solve_matches_reference(name, oracle_instances, goldens):
     identical whenever no tol/Armijo decision on the path was within the merit
     noise floor (SURVEY §7 hard part 1: the margin-aware gate)."""
     inst, g = oracle_instances[name], goldens[name]
-    B = N_BIG if name in BIG else g["mu"].shape[0]
+    B = N_ORACLE.get(name, g["mu"].shape[0])
     robust = same_iters = 0
     for k in range(B):
         a, lam = g["mu"][k]

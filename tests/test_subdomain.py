@@ -104,6 +104,10 @@ def _solve_gen(inst, a, lm, cfg):
 
 
 class OracleRoundEngine:
+    """CPU stand-in for DeviceRoundEngine with the same protocol: trial
+    records [running flag, x_trial] per mu, steps for a mu slice only,
+    slice results gathered at the end."""
+
     def __init__(self, inst):
         self.inst = inst
         self.n_blocks = len(inst.blocks)
@@ -120,25 +124,36 @@ class OracleRoundEngine:
         import torch
         return torch.zeros(n, dtype=torch.float64)
 
-    def begin(self, mu, cfg, x0, lam0, lo, hi):
+    def trial_len(self):
+        return 1 + self.inst.n_primal
+
+    def begin(self, mu, cfg, x0, lam0, lo, hi, rows=0):
+        import torch
         assert x0 is None and lam0 is None
         self.lo, self.hi = lo, hi
         self.B = mu.shape[0]
         self.bbs = [self.inst.boundary(a, lm) for a, lm in mu]
         self.gens = [_solve_gen(self.inst, a, lm, cfg) for a, lm in mu]
-        self.xt = [next(g) for g in self.gens]
+        rec = self.trial_len()
+        self.trials = torch.zeros(self.B * rec, dtype=torch.float64)
+        t = self.trials.numpy().reshape(self.B, rec)
+        for k, g in enumerate(self.gens):
+            t[k, 0], t[k, 1:] = 1.0, next(g)
         self.res = [None] * self.B
+        self.mlo, self.mhi = 0, self.B
         return self.B
 
-    def _split(self, x):
-        return self.inst.split(x)
+    def set_trials(self, trials, mu_lo, mu_hi):
+        trials[:self.trials.numel()] = self.trials
+        self.trials, self.mlo, self.mhi = trials, mu_lo, mu_hi
 
     def eval(self, packets, stride):
         pk = packets.numpy()
+        t = self.trials.numpy().reshape(-1, self.trial_len())
         for k in range(self.B):
-            if self.res[k] is not None:
+            if t[k, 0] == 0.0:
                 continue
-            parts = self._split(self.xt[k])
+            parts = self.inst.split(t[k, 1:])
             pos = k * stride
             for b in range(self.lo, self.hi):
                 blk = self.inst.blocks[b]
@@ -160,8 +175,9 @@ class OracleRoundEngine:
 
     def step(self, gathered, nranks, bounds, stride, count=True):
         g = gathered.numpy().reshape(nranks, self.B, stride)
+        t = self.trials.numpy().reshape(-1, self.trial_len())
         active = 0
-        for k in range(self.B):
+        for k in range(self.mlo, self.mhi):
             if self.res[k] is not None:
                 continue
             pieces = []
@@ -171,11 +187,18 @@ class OracleRoundEngine:
                     pieces.append(self._unpack(g[r, k, pos:], b))
                     pos += self.plen[b]
             try:
-                self.xt[k] = self.gens[k].send(pieces)
+                t[k, 1:] = self.gens[k].send(pieces)
                 active += 1
             except StopIteration as stop:
                 self.res[k] = stop.value
-        return active
+                t[k, 0] = 0.0
+        return active if count else None
+
+    def gather_results(self, rank, chunk, world, group):
+        import torch.distributed as dist
+        parts = [None] * world
+        dist.all_gather_object(parts, self.res[self.mlo:self.mhi], group=group)
+        self.res = [r for p in parts for r in p]
 
     def finish(self, mu):
         return self.res
@@ -260,6 +283,25 @@ def test_device_sharded_world1_equals_megakernel(name, gpu_instances):
                                   np.nan_to_num(ref.merit_hist, nan=-1))
 
 
+def _exchange_trials(ranks):
+    """What the all-gather of the trial records does, for rank states in one
+    process: every rank's slice into every rank's buffer."""
+    chunks = [sh.trial_chunk().clone() for sh in ranks]
+    for sh in ranks:
+        for r, c in enumerate(chunks):
+            n = c.numel()
+            sh.trials[r * n:(r + 1) * n] = c
+
+
+def _exchange_results(ranks):
+    """The final all-gather of the slices' result rows, in one process."""
+    for k in ranks[0].eng.out:
+        rows = [sh.eng.out[k][sh.rank * sh.chunk:(sh.rank + 1) * sh.chunk].clone() for sh in ranks]
+        for sh in ranks:
+            for r, c in enumerate(rows):
+                sh.eng.out[k][r * sh.chunk:(r + 1) * sh.chunk] = c
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3, 16])
 def test_device_sharded_ranks_in_one_process(world):
@@ -282,11 +324,11 @@ def test_device_sharded_ranks_in_one_process(world):
     while active:
         parts = [sh.eval().clone() for sh in ranks]
         torch.cat(parts, out=gathered)
-        counts = [sh.step(gathered) for sh in ranks]
-        assert len(set(counts)) == 1
-        active = counts[0]
+        active = sum(sh.step(gathered) for sh in ranks)    # each rank steps its mu slice
+        _exchange_trials(ranks)
+    _exchange_results(ranks)
     for sh in ranks:
-        r = sh.result()
+        r = sh.result(group=False)
         for k in ("x", "lam", "n_iter", "n_evals", "status", "merit"):
             np.testing.assert_array_equal(getattr(r, k), getattr(one, k), err_msg=k)
 
@@ -357,11 +399,11 @@ def test_device_fused_peer_gather(world):
     while active:
         for sh in ranks:
             sh.eval_p2p(ptrs)
-        counts = [sh.step(g) for sh, g in zip(ranks, gathered)]
-        assert len(set(counts)) == 1
-        active = counts[0]
+        active = sum(sh.step(g) for sh, g in zip(ranks, gathered))
+        _exchange_trials(ranks)
+    _exchange_results(ranks)
     for sh in ranks:
-        r = sh.result()
+        r = sh.result(group=False)
         for k in ("x", "lam", "n_iter", "n_evals", "status"):
             np.testing.assert_array_equal(getattr(r, k), getattr(one, k), err_msg=k)
 

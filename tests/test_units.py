@@ -92,3 +92,31 @@ def test_units_batch_composition_invariance(monkeypatch):
         one = P.solve_rom_batch(split, mu[k:k + 1])
         np.testing.assert_array_equal(one.x[0], full.x[k])
         np.testing.assert_array_equal(one.lam[0], full.lam[k])
+
+
+@pytest.mark.parametrize("name", ["c0_nm", "c3_nm", "tiny42_nm"])
+def test_tensor_core_hidden_layer_matches_oracle(name, goldens, oracle_instances, monkeypatch):
+    """The hidden pre-activation on the FP64 tensor cores (hidden_range,
+    DDNM_HIDDEN_DMMA=1; opt-in): decoder values and
+    Jacobians to 1e-13 against the oracle, solves to 1e-9 against the
+    reference goldens."""
+    from oracle import ddnm_oracle as O
+    monkeypatch.setenv("DDNM_HIDDEN_DMMA", "1")
+    inst = P.RomInstance.load(golden_path(name, "artifacts"))
+    inst.context()
+    monkeypatch.delenv("DDNM_HIDDEN_DMMA")
+    g, oi = goldens[name], oracle_instances[name]
+    ev = P.eval_gradients_batch(inst, g["mu"][:3], g["x0"][:3], g["lam0"][:3])
+    for k in range(3):
+        for b, blk in enumerate(oi.blocks):
+            d = ev.block(k, b)
+            xi, xg = oi.split(g["x0"][k])[b]
+            assert rel(d["int_g"], blk.int_map.decode(xi)) < 1e-13
+            assert rel(d["int_J"], blk.int_map.jacobian(xi)) < 1e-13
+            assert rel(d["gam_g"], blk.gam_map.decode(xg)) < 1e-13
+            assert rel(d["gam_J"], blk.gam_map.jacobian(xg)) < 1e-13
+        assert rel(ev.rho[k], O.eval_gradients(oi, oi.boundary(*g["mu"][k]), g["x0"][k],
+                                               g["lam0"][k]).rho) < 1e-11
+    res = P.solve_rom_batch(inst, g["mu"])
+    for k in range(g["mu"].shape[0]):
+        assert rel(res.x[k], g["x"][k]) < 1e-9 and rel(res.lam[k], g["lam"][k]) < 1e-9, k

@@ -53,7 +53,11 @@ active = ranks[0].active
 while active:
     for sh in ranks:
         sh.eval_p2p([b.data_ptr() for b in bufs])
-    active = [sh.step(b) for sh, b in zip(ranks, bufs)][0]
+    active = sum(sh.step(b) for sh, b in zip(ranks, bufs))   # each rank its mu slice
+    chunks = [sh.trial_chunk().clone() for sh in ranks]      # the trial all-gather
+    for sh in ranks:
+        for r, c in enumerate(chunks):
+            sh.trials[r * c.numel():(r + 1) * c.numel()] = c
 print("dd16 sharded ok", one.n_iter.tolist(), flush=True)
 
 with tempfile.TemporaryDirectory() as d:
