@@ -19,5 +19,11 @@ void register_8_5(std::vector<KernelEntry>& t) {
                           (const void*)&k_eval<1, 8, 5, true>,
                           (const void*)&k_dd_eval<1, 8, 5>,
                           (const void*)&k_dd_step<1, 8, 5, true>});
+  // config 4 (960^2, 16 blocks as ~600 evaluation units, n_C = 40): two
+  // slots per CTA with the KKT workspace in L2
+  t.push_back(KernelEntry{8, 5, 2, true, (const void*)&k_solve<2, 8, 5, true>,
+                          (const void*)&k_eval<2, 8, 5, true>,
+                          (const void*)&k_dd_eval<2, 8, 5>,
+                          (const void*)&k_dd_step<2, 8, 5, true>});
 }
 }  // namespace ddnm

@@ -76,7 +76,6 @@ def main():
     res = {"mu": mu}
     with get_context("fork").Pool(a.procs) as pool:
         parts = pool.map(_oracle, [(path, c) for c in chunks])
-    ox = np.zeros((a.n, 40)); ol = None
     rows = [None] * a.n
     for i, p in enumerate(parts):
         for j, r in enumerate(p):
@@ -85,7 +84,6 @@ def main():
     res["oracle_lam"] = np.array([r[1] for r in rows])
     res["oracle_n_iter"] = np.array([r[2] for r in rows], np.int64)
     res["robust"] = np.array([r[3] for r in rows], np.int64)
-    del ox, ol
     pkl = os.path.join(ROOT, "artifacts_cache", f"{a.name}.pkl")
     if os.path.exists(pkl) and os.path.isdir(REF):
         with get_context("fork").Pool(a.procs) as pool:
@@ -97,8 +95,9 @@ def main():
         res["reference_x"] = np.array([r[0] for r in rows])
         res["reference_lam"] = np.array([r[1] for r in rows])
         res["reference_n_iter"] = np.array([r[2] for r in rows], np.int64)
-        ex = max(float(np.max(np.abs(res["oracle_x"][k] - res["reference_x"][k])) /
-                       np.max(np.abs(res["reference_x"][k])) for k in range(a.n))
+        ex = max(float(np.max(np.abs(res["oracle_x"][k] - res["reference_x"][k]))
+                       / np.max(np.abs(res["reference_x"][k])))
+                 for k in range(a.n))
         print("oracle vs reference: max rel x", ex, "n_iter equal",
               int(np.sum(res["oracle_n_iter"] == res["reference_n_iter"])), "/", a.n)
     print("robust", int(res["robust"].sum()), "/", a.n)
