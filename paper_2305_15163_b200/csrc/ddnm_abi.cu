@@ -126,6 +126,8 @@ struct ddnm_ctx {
   double* gJg = nullptr;      // interface Jacobian rows per global slot
   double* kkt_g = nullptr;    // KKT workspace per global slot (KG kernels)
   size_t kkt_stride = 0;      // doubles per slot, 0: KKT in shared memory
+  bool ebg = false;           // evaluation buffers in global memory
+  double* eb_g = nullptr;     // [slots][2][eb_size] when ebg
   size_t gbv_slots = 0;
   int* work = nullptr;
   unsigned long long* counters = nullptr;
@@ -894,9 +896,12 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     int t = std::max(std::max(s0, kg ? P.n_C * (P.n_C + 1) : kkt_need), std::max(ls_need, rbf_need2));
     return (t + 1) & ~1;
   };
-  auto footprint = [&](int G, int level, bool kg = false) {
-    return ((size_t)state_d * G + (size_t)G * (8 * P.nK + 2 * P.eb_size + scr_total(level, kg))) * 8;
+  // ebg: the evaluation buffers live in global memory (Params::eb_glob)
+  auto footprint = [&](int G, int level, bool kg = false, bool ebg = false) {
+    return ((size_t)state_d * G +
+            (size_t)G * (8 * P.nK + (ebg ? 0 : 2 * P.eb_size) + scr_total(level, kg))) * 8;
   };
+  bool kern_ebg = false;
   const Kernels* kern = nullptr;
   int kern_level = 0;
   const char* jl = getenv("DDNM_JLEVEL");
@@ -920,17 +925,24 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
     if ((g % 2 == 0) != (best % 2 == 0)) return g % 2 == 0;
     return g > best;
   };
+  // pass 0: everything in shared memory; pass 1: the KKT workspace in L2
+  // (KG kernels), and -- when that alone leaves slots on the table -- the
+  // evaluation buffers too (config 4: 2 x 5.8k doubles per slot)
+  const bool ebg_ok = !getenv("DDNM_NO_EB_GLOBAL");
   for (int pass = 0; pass < 2 && !kern; ++pass) {
     for (const auto& k : kernel_table()) {
       if (k.ni != ni || k.ng != ng || k.kkt_global != (pass == 1)) continue;
       if (slots > 0 && k.g != slots) continue;
-      int lv = -1;
-      for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
-        if (footprint(k.g, level, k.kkt_global) <= soft_cap) lv = level;
-      for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
-        if (footprint(k.g, level, k.kkt_global) <= smem_cap) lv = level;
-      if (lv < 0) continue;
-      if (better(k.g, kern ? kern->g : -1)) { kern = &k; kern_level = lv; }
+      for (int eg = 0; eg < (pass == 1 && ebg_ok ? 2 : 1); ++eg) {
+        int lv = -1;
+        for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
+          if (footprint(k.g, level, k.kkt_global, eg) <= soft_cap) lv = level;
+        for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
+          if (footprint(k.g, level, k.kkt_global, eg) <= smem_cap) lv = level;
+        if (lv < 0) continue;
+        if (better(k.g, kern ? kern->g : -1)) { kern = &k; kern_level = lv; kern_ebg = eg; }
+        break;      // buffers in shared memory when they fit at this G
+      }
     }
   }
   if (!kern) {
@@ -1134,8 +1146,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.sm_state = 0;
   P.sm_vec = state_d * P.G;
   P.sm_eb = P.sm_vec + P.G * 8 * P.nK;
-  P.sm_scr = P.sm_eb + P.G * 2 * P.eb_size;
-  c->smem = footprint(P.G, kern_level, kern->kkt_global);
+  P.sm_scr = P.sm_eb + (kern_ebg ? 0 : P.G * 2 * P.eb_size);
+  c->ebg = kern_ebg;
+  c->smem = footprint(P.G, kern_level, kern->kkt_global, kern_ebg);
   if (raise_smem_limit(kern->solve, c->smem) != cudaSuccess ||
       raise_smem_limit(kern->eval, c->smem) != cudaSuccess ||
       raise_smem_limit(kern->dd_eval, c->smem) != cudaSuccess ||
@@ -1162,6 +1175,7 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   if (c->gJ) cudaFree(c->gJ);
   if (c->gJg) cudaFree(c->gJg);
   if (c->kkt_g) cudaFree(c->kkt_g);
+  if (c->eb_g) cudaFree(c->eb_g);
   if (c->work) cudaFree(c->work);
   if (c->counters) cudaFree(c->counters);
   if (c->prof) cudaFree(c->prof);
@@ -1211,6 +1225,9 @@ static int ensure_gbv(ddnm_ctx* c, size_t slots) {
   if (c->kkt_g) cudaFree(c->kkt_g);
   c->kkt_g = nullptr;
   if (c->kkt_stride) CUDA_TRY(cudaMalloc(&c->kkt_g, slots * c->kkt_stride * sizeof(double)));
+  if (c->eb_g) cudaFree(c->eb_g);
+  c->eb_g = nullptr;
+  if (c->ebg) CUDA_TRY(cudaMalloc(&c->eb_g, slots * 2 * (size_t)c->P.eb_size * sizeof(double)));
   c->gbv_slots = slots;
   return 0;
 }
@@ -1256,6 +1273,7 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
   P.gJ = c->gJ;
   P.gJg = c->gJg;
   P.kkt_g = c->kkt_g;
+  P.eb_glob = c->eb_g;
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
@@ -1396,6 +1414,7 @@ int ddnm_eval_batch(ddnm_ctx* c, int32_t B, const double* mu, const double* x, c
   P.gJ = c->gJ;
   P.gJg = c->gJg;
   P.kkt_g = c->kkt_g;
+  P.eb_glob = c->eb_g;
   P.work = c->work;
   P.counters = c->counters;
   void* args[] = {&P};
@@ -1538,6 +1557,7 @@ struct ddnm_dd {
   double* gJ = nullptr;
   double* gJg = nullptr;
   double* kkt_g = nullptr;
+  double* eb_g = nullptr;         // evaluation buffers (when the context keeps them in L2)
   double* trials = nullptr;       // own trial records [B][rec] (until ddnm_dd_set_trials)
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
 };
@@ -1599,11 +1619,14 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   d->B = B;
   d->ctas = (B + c->P.G - 1) / c->P.G;
   auto bail = [&](int r) { ddnm_dd_end(d); return r; };
-  const size_t slots = (size_t)d->ctas * c->P.G;
+  // per-mu scratch (slot = mu); one CTA of spare slots for a step slice that
+  // starts mid-CTA (k_dd_step maps mu_lo + blockIdx.x * G + s)
+  const size_t slots = (size_t)(d->ctas + 1) * c->P.G;
   if (cudaMalloc(&d->gbv, slots * std::max(c->tot_rows * 3, 1) * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&d->gJ, slots * std::max(c->P.gJ_stride, 1) * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&d->gJg, slots * std::max(c->P.gJg_stride, 1) * sizeof(double)) != cudaSuccess ||
-      (c->kkt_stride && cudaMalloc(&d->kkt_g, slots * c->kkt_stride * sizeof(double)) != cudaSuccess))
+      (c->kkt_stride && cudaMalloc(&d->kkt_g, slots * c->kkt_stride * sizeof(double)) != cudaSuccess) ||
+      (c->ebg && cudaMalloc(&d->eb_g, slots * 2 * (size_t)c->P.eb_size * sizeof(double)) != cudaSuccess))
     return bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve scratch"));
   if (cudaMalloc(&d->st, (size_t)B * sizeof(SlotState)) != cudaSuccess ||
       cudaMalloc(&d->vec, (size_t)B * 8 * c->P.nK * sizeof(double)) != cudaSuccess ||
@@ -1633,6 +1656,7 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   P.gJ = d->gJ;
   P.gJg = d->gJg;
   P.kkt_g = d->kkt_g;
+  P.eb_glob = d->eb_g;
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
@@ -1797,7 +1821,7 @@ int ddnm_dd_end(ddnm_dd* d) {
   if (d->vec) cudaFree(d->vec);
   if (d->ecur) cudaFree(d->ecur);
   if (d->active) cudaFree(d->active);
-  for (double* p : {d->gbv, d->gJ, d->gJg, d->kkt_g, d->trials})
+  for (double* p : {d->gbv, d->gJ, d->gJg, d->kkt_g, d->eb_g, d->trials})
     if (p) cudaFree(p);
   delete d;
   return 0;

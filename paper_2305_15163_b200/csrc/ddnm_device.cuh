@@ -240,6 +240,11 @@ struct Params {
   // KKT workspace in global memory (kernels instantiated with KG = true)
   double* kkt_g;          // per global slot [kkt_stride]
   long long kkt_stride;
+  // the two evaluation buffers of every slot in global memory (L2) instead of
+  // shared memory, [global slot][2][eb_size] (null: shared memory); chosen by
+  // the planner when they would cost slots (config 4: 16 blocks x 345
+  // doubles x 2 per slot)
+  double* eb_glob;
   // evaluation units: when non-null, eval_blocks walks units[u_bnd[b]] ..
   // units[u_bnd[b + 1] - 1] for real block b instead of blk[b] (blocks too
   // large for one CTA's shared memory are split into chunks of their sampled

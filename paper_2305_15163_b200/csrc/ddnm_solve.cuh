@@ -26,7 +26,10 @@ struct View {
   __device__ SlotState* st() const { return reinterpret_cast<SlotState*>(ddnm_smem + P.sm_state); }
   // vectors: 0 x, 1 lam, 2 s, 3 slam, 4 xt, 5 lt, 6 best x, 7 best lam
   __device__ double* vec(int s, int which) const { return ddnm_smem + P.sm_vec + (s * 8 + which) * P.nK; }
-  __device__ double* eb(int s, int which) const { return ddnm_smem + P.sm_eb + (s * 2 + which) * P.eb_size; }
+  __device__ double* eb(int s, int which) const {
+    return P.eb_glob ? P.eb_glob + ((size_t)(gslot0 + s) * 2 + which) * P.eb_size
+                     : ddnm_smem + P.sm_eb + (s * 2 + which) * P.eb_size;
+  }
   __device__ double* scr(int s) const { return ddnm_smem + P.sm_scr + s * P.scr_size; }
   // decoder Jacobian rows: shared memory when they fit, else per-slot L2 scratch
   __device__ double* jint(int s) const {
@@ -57,6 +60,8 @@ __device__ __forceinline__ void zero_slots(const View& V) {
   const Params& P = V.P;
   const int n = P.sm_scr + P.G * P.scr_size - P.sm_vec;
   for (int i = threadIdx.x; i < n; i += blockDim.x) ddnm_smem[P.sm_vec + i] = 0.0;
+  if (P.eb_glob)
+    for (int i = threadIdx.x; i < 2 * P.G * P.eb_size; i += blockDim.x) V.eb(0, 0)[i] = 0.0;
 }
 
 // block pieces inside an eval buffer

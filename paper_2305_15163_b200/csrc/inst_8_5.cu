@@ -5,6 +5,7 @@
 #include "ddnm_solve.cuh"
 
 namespace ddnm {
+void register_8_5_more(std::vector<KernelEntry>& t);   // inst_8_5b.cu
 void register_8_5(std::vector<KernelEntry>& t) {
   t.push_back(KernelEntry{8, 5, 1, false, (const void*)&k_solve<1, 8, 5, false>,
                           (const void*)&k_eval<1, 8, 5, false>,
@@ -19,11 +20,6 @@ void register_8_5(std::vector<KernelEntry>& t) {
                           (const void*)&k_eval<1, 8, 5, true>,
                           (const void*)&k_dd_eval<1, 8, 5>,
                           (const void*)&k_dd_step<1, 8, 5, true>});
-  // config 4 (960^2, 16 blocks as ~600 evaluation units, n_C = 40): two
-  // slots per CTA with the KKT workspace in L2
-  t.push_back(KernelEntry{8, 5, 2, true, (const void*)&k_solve<2, 8, 5, true>,
-                          (const void*)&k_eval<2, 8, 5, true>,
-                          (const void*)&k_dd_eval<2, 8, 5>,
-                          (const void*)&k_dd_step<2, 8, 5, true>});
+  register_8_5_more(t);
 }
 }  // namespace ddnm
