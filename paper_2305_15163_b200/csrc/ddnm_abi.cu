@@ -747,10 +747,15 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // block becomes units when any block needs splitting (DDNM_UNIT_ROWS forces
   // it, for tests on small instances)
   {
-    UnitLimits L{256, 1536, 512, 128, 256};
+    // <= 128 rows / 1536 hidden units per row unit (config 3: 128 units, 4
+    // slots, 120 ms per 1024 mu; 256 rows: 115 units but only 2 slots fit,
+    // 140-145 ms; 768-1024 hidden: more units, 129-142 ms; profiles/r2i.log)
+    UnitLimits L{128, 1536, 512, 128, 256};
     const char* ur = getenv("DDNM_UNIT_ROWS");
     if (ur) L.rows = std::max(1, atoi(ur));
     if (const char* ug = getenv("DDNM_UNIT_GAM")) L.gchunk = std::max(8, atoi(ug));
+    if (const char* uh = getenv("DDNM_UNIT_HIDDEN")) L.hidden = std::max(64, atoi(uh));
+    if (const char* uo = getenv("DDNM_UNIT_OUTS")) L.outs = std::max(16, atoi(uo));
     bool need = false;
     for (int b = 0; b < P.nb; ++b) {
       const ddnm_block& k = a->blocks[b];
@@ -918,13 +923,22 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // mu) 2 slots with the rows in shared memory (205 KB) take 33.3 ms and with
   // them in L2 (146 KB) 29.9 ms; c0_srpc keeps 2 slots at 219 KB (216 ms vs
   // 243 ms for 1 slot).  DDNM_SMEM_SOFT_CAP overrides (bytes).
-  size_t soft_cap = std::min<size_t>(smem_cap, 192 * 1024);
+  // (200 KB: config 3's evaluation units at 4 slots need 199 KB and take
+  // 120 ms per 1024 mu vs 140 ms at 2 slots; config 4 at 4 slots needs 214 KB
+  // and is slower than at 2, profiles/r2i.log)
+  size_t soft_cap = std::min<size_t>(smem_cap, 200 * 1024);
   if (const char* sc = getenv("DDNM_SMEM_SOFT_CAP")) soft_cap = std::min<size_t>(smem_cap, (size_t)atoll(sc));
-  auto better = [](int g, int best) {   // even before odd, then larger
+  // ranking: a footprint under the soft cap first (the L1 left for the
+  // weights matters more than one more slot: config 4 with the evaluation
+  // buffers in L2 takes 501 ms per 256 mu at 2 slots / 193 KB and 725 ms at
+  // 4 slots / 214 KB, profiles/r2h.log), then even before odd, then larger
+  auto better = [](int g, bool soft, int best, bool best_soft) {
     if (best < 0) return true;
+    if (soft != best_soft) return soft;
     if ((g % 2 == 0) != (best % 2 == 0)) return g % 2 == 0;
     return g > best;
   };
+  bool kern_soft = false;
   // pass 0: everything in shared memory; pass 1: the KKT workspace in L2
   // (KG kernels), and -- when that alone leaves slots on the table -- the
   // evaluation buffers too (config 4: 2 x 5.8k doubles per slot)
@@ -935,13 +949,16 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
       if (slots > 0 && k.g != slots) continue;
       for (int eg = 0; eg < (pass == 1 && ebg_ok ? 2 : 1); ++eg) {
         int lv = -1;
+        bool soft = false;
         for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
-          if (footprint(k.g, level, k.kkt_global, eg) <= soft_cap) lv = level;
+          if (footprint(k.g, level, k.kkt_global, eg) <= soft_cap) { lv = level; soft = true; }
         for (int level = lvl_lo; level <= lvl_hi && lv < 0; ++level)
           if (footprint(k.g, level, k.kkt_global, eg) <= smem_cap) lv = level;
         if (lv < 0) continue;
-        if (better(k.g, kern ? kern->g : -1)) { kern = &k; kern_level = lv; kern_ebg = eg; }
-        break;      // buffers in shared memory when they fit at this G
+        if (better(k.g, soft, kern ? kern->g : -1, kern_soft)) {
+          kern = &k; kern_level = lv; kern_ebg = eg; kern_soft = soft;
+        }
+        if (soft) break;   // buffers in shared memory when they fit this G under the cap
       }
     }
   }
