@@ -261,7 +261,10 @@ def run_gpu(args):
     # solve_rom on the same seed-1000 parameters, tools/make_bench_golden.py)
     parity = None
     if rank == 0:
-        parity = bench_parity(outs, lo)
+        try:
+            parity = bench_parity(outs, lo)
+        except Exception as exc:      # reported, never fatal for the headline line
+            parity = {"error": f"{type(exc).__name__}: {exc}"}
 
     # weak scaling beside it: 4096 mu per GPU (seed 1000 + rank)
     weak = None
@@ -408,7 +411,7 @@ def bench_parity(outs, lo):
     if not os.path.exists(PARITY_FILE) or lo != 0:
         return None
     z = dict(np.load(PARITY_FILE))
-    n = min(int(z["x"].shape[0]), outs["x"].shape[0])
+    n = min(int(z["oracle_x"].shape[0]), outs["x"].shape[0])
     x = outs["x"][:n].cpu().numpy()
     lam = outs["lam"][:n].cpu().numpy()
     it = outs["n_iter"][:n].cpu().numpy()

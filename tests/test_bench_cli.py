@@ -22,3 +22,20 @@ def test_reference_arm_prints_one_json_line():
               "e2e"):
         assert k in d, k
     assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_parity_block_against_committed_goldens():
+    """The bench line's parity block (device results of the timed batch vs
+    oracle + reference goldens), fed here with the oracle's own values."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, ROOT)
+    import bench
+    z = dict(np.load(bench.PARITY_FILE))
+    outs = {"x": torch.from_numpy(z["oracle_x"].copy()),
+            "lam": torch.from_numpy(z["oracle_lam"].copy()),
+            "n_iter": torch.from_numpy(z["oracle_n_iter"].astype(np.int32))}
+    p = bench.bench_parity(outs, 0)
+    assert p["sample"] == 256 and p["oracle"]["pass"] and p["reference"]["pass"]
+    assert p["oracle"]["n_iter_equal"] == 256 and p["reference"]["max_rel_x"] < 1e-12
+    assert bench.bench_parity(outs, 5) is None        # a shard not starting at mu 0
