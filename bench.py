@@ -350,14 +350,16 @@ def run_gpu(args):
     peak, peak_src = fp64_peak()
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1d_ncu_summary.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_summary.json")) as f:
             traffic = json.load(f)["traffic_bytes_per_launch"]   # ncu --set full capture
     except Exception:
         pass
     achieved = flops_per_step / (ms_per_step / 1e3) / 1e12
     roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "traffic_source": "dram__bytes_read+write per launch, profiles/r1d_ncu_summary.json",
+            "traffic_source": "dram__bytes_read+write per launch, profiles/r2_ncu_summary.json "
+                              "(this build; 1.25 MB weights + one write-back of the 16.6 MB "
+                              "per-slot L2 Jacobian-row scratch)",
             "kernel": "k_solve (persistent SQP megakernel)",
             "peak_source": peak_src,
             "algorithmic_flops_per_step": flops_per_step,

@@ -942,7 +942,12 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // pass 0: everything in shared memory; pass 1: the KKT workspace in L2
   // (KG kernels), and -- when that alone leaves slots on the table -- the
   // evaluation buffers too (config 4: 2 x 5.8k doubles per slot)
-  const bool ebg_ok = !getenv("DDNM_NO_EB_GLOBAL");
+  // only for instances split into evaluation units: their rounds are long
+  // enough to hide the buffers' L2 traffic (config 4: 501 ms at 2 slots vs
+  // 544-573 ms at 1 slot with the buffers in shared memory); dd16's small
+  // blocks are not (27.6 ms at 1 slot in shared memory, 58 ms at 4 slots
+  // with the buffers in L2, profiles/r2k_bench.json)
+  const bool ebg_ok = P.units && !getenv("DDNM_NO_EB_GLOBAL");
   for (int pass = 0; pass < 2 && !kern; ++pass) {
     for (const auto& k : kernel_table()) {
       if (k.ni != ni || k.ng != ng || k.kkt_global != (pass == 1)) continue;
