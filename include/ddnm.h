@@ -201,6 +201,16 @@ typedef struct {
 
 typedef struct ddnm_ctx ddnm_ctx;
 
+/* Host-only (no GPU): the evaluation units ddnm_ctx_create would split these
+ * artifacts into (0 when every block is evaluated whole).  row_unit
+ * [total_rows] (nullable): the unit of every sampled row, block by block;
+ * unit_info [n_units][8] (nullable; size it by a first call with both NULL):
+ * real block, UF_* flags (1 rows, 2 constraint, 4/8 accumulate), rows,
+ * interior outputs, interior hidden units, interface outputs, interface
+ * hidden units, constraint columns. */
+int ddnm_plan_units(const ddnm_artifacts* art, int32_t* n_units, int32_t* row_unit,
+                    int32_t* unit_info);
+
 const char* ddnm_last_error(void);
 int ddnm_abi_version(void);
 

@@ -477,6 +477,33 @@ struct HostUnit {
 
 struct UnitLimits { int rows, hidden, outs, grefs, gchunk; };
 
+// <= 128 rows / 1536 hidden units per row unit (config 3: 128 units, 4
+// slots, 120 ms per 1024 mu; 256 rows: 115 units but only 2 slots fit,
+// 140-145 ms; 768-1024 hidden: more units, 129-142 ms; profiles/r2i.log);
+// DDNM_UNIT_* override (tests, experiments)
+UnitLimits unit_limits() {
+  UnitLimits L{128, 1536, 512, 128, 256};
+  if (const char* ur = getenv("DDNM_UNIT_ROWS")) L.rows = std::max(1, atoi(ur));
+  if (const char* ug = getenv("DDNM_UNIT_GAM")) L.gchunk = std::max(8, atoi(ug));
+  if (const char* uh = getenv("DDNM_UNIT_HIDDEN")) L.hidden = std::max(64, atoi(uh));
+  if (const char* uo = getenv("DDNM_UNIT_OUTS")) L.outs = std::max(16, atoi(uo));
+  return L;
+}
+
+// blocks are split when any block is too large for one CTA's shared-memory
+// plan (or DDNM_UNIT_ROWS forces it); autoencoder WFPC collocation only
+bool wants_units(const ddnm_artifacts* a) {
+  bool need = false, nogappy = true;
+  for (int b = 0; b < a->n_blocks; ++b) {
+    const ddnm_block& k = a->blocks[b];
+    if (k.interior.n_hidden > 2048 || k.n_io > 512 || k.n_rows > 256 || k.interface.n_out > 512)
+      need = true;
+    if (k.n_basis > 0) nogappy = false;
+  }
+  const bool can = a->map_kind == DDNM_MAP_AUTOENCODER && a->constraint_mode == DDNM_CON_WFPC;
+  return (need || getenv("DDNM_UNIT_ROWS")) && can && nogappy && !getenv("DDNM_NO_UNITS");
+}
+
 // split block k into units (row chunks, then interface-output chunks)
 int split_block(const ddnm_artifacts* a, const ddnm_block& k, const HostRows& hr,
                 const UnitLimits& L, std::vector<HostUnit>& out) {
@@ -747,24 +774,8 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   // block becomes units when any block needs splitting (DDNM_UNIT_ROWS forces
   // it, for tests on small instances)
   {
-    // <= 128 rows / 1536 hidden units per row unit (config 3: 128 units, 4
-    // slots, 120 ms per 1024 mu; 256 rows: 115 units but only 2 slots fit,
-    // 140-145 ms; 768-1024 hidden: more units, 129-142 ms; profiles/r2i.log)
-    UnitLimits L{128, 1536, 512, 128, 256};
-    const char* ur = getenv("DDNM_UNIT_ROWS");
-    if (ur) L.rows = std::max(1, atoi(ur));
-    if (const char* ug = getenv("DDNM_UNIT_GAM")) L.gchunk = std::max(8, atoi(ug));
-    if (const char* uh = getenv("DDNM_UNIT_HIDDEN")) L.hidden = std::max(64, atoi(uh));
-    if (const char* uo = getenv("DDNM_UNIT_OUTS")) L.outs = std::max(16, atoi(uo));
-    bool need = false;
-    for (int b = 0; b < P.nb; ++b) {
-      const ddnm_block& k = a->blocks[b];
-      if (k.interior.n_hidden > 2048 || k.n_io > 512 || k.n_rows > 256 || k.interface.n_out > 512) need = true;
-    }
-    const bool can = a->map_kind == DDNM_MAP_AUTOENCODER && a->constraint_mode == DDNM_CON_WFPC;
-    bool nogappy = true;
-    for (int b = 0; b < P.nb; ++b) if (a->blocks[b].n_basis > 0) nogappy = false;
-    if ((need || ur) && can && nogappy && !getenv("DDNM_NO_UNITS")) {
+    const UnitLimits L = unit_limits();
+    if (wants_units(a)) {
       std::vector<BlockDev> units;
       max_nh = max_io = max_gam = max_rows = 0;
       for (int b = 0; b < P.nb; ++b) {
@@ -1184,6 +1195,38 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
       cudaMalloc(&c->counters, 2 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cudaMalloc failed"));
   *out = c;
+  return 0;
+}
+
+int ddnm_plan_units(const ddnm_artifacts* a, int32_t* n_units, int32_t* row_unit,
+                    int32_t* unit_info) {
+  if (!a || !n_units) return fail(DDNM_EINVAL, "null argument");
+  if (a->abi_version != DDNM_ABI_VERSION) return fail(DDNM_EINVAL, "ABI version mismatch");
+  if (a->n_blocks < 1 || a->n_blocks > MAXB) return fail(DDNM_EINVAL, "need 1..16 blocks");
+  *n_units = 0;
+  if (!wants_units(a)) return 0;
+  const UnitLimits L = unit_limits();
+  int rc, u = 0, row_off = 0;
+  for (int b = 0; b < a->n_blocks; ++b) {
+    const ddnm_block& k = a->blocks[b];
+    HostRows hr;
+    if ((rc = build_stencil(a, k, hr))) return rc;
+    std::vector<HostUnit> hu;
+    if ((rc = split_block(a, k, hr, L, hu))) return rc;
+    for (const HostUnit& x : hu) {
+      if (unit_info) {
+        int32_t* r = unit_info + (size_t)u * 8;
+        r[0] = b; r[1] = x.flags; r[2] = (int32_t)x.rows.size(); r[3] = x.in.d.n_out;
+        r[4] = x.in.d.n_hidden; r[5] = x.ga.d.n_out; r[6] = x.ga.d.n_hidden;
+        r[7] = x.CA.empty() ? 0 : (int32_t)(x.CA.size() / a->n_c);
+      }
+      if (row_unit)
+        for (int m : x.row_map) row_unit[row_off + m] = u;
+      ++u;
+    }
+    row_off += k.n_rows;
+  }
+  *n_units = u;
   return 0;
 }
 

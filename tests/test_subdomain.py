@@ -435,3 +435,76 @@ def test_ipc_handle_of_a_device_buffer():
     r = sh.result()
     buf.close()
     np.testing.assert_array_equal(r.x, one.x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_p2p_host_loop_protocol(world):
+    """The host loop of solve_rom_batch_subdomain_sharded(transport="p2p")
+    with several rank states in one process: two gathered-buffer sets
+    alternating by round parity, the running count read only every CHECK-th
+    round (count=False otherwise, no host synchronisation), each rank
+    stepping its mu slice, trial records exchanged every round: bitwise the
+    one-rank solve on every rank."""
+    import torch
+
+    import paper_2305_15163_b200 as P
+    from paper_2305_15163_b200.subdomain import CHECK, ShardedSolve
+    inst = P.RomInstance.load(golden_path(DD, "artifacts"))
+    mu = P.seeded_parameters(19, seed=6)
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    ranks = [ShardedSolve(inst, mu, P.SqpConfig(), r, world) for r in range(world)]
+    n = world * ranks[0].B * ranks[0].stride
+    bufs = [[torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in ranks]
+            for _ in range(2)]
+    ptrs = [[b.data_ptr() for b in bset] for bset in bufs]
+    active, rounds = ranks[0].active, 0
+    while active:
+        k = rounds % 2
+        for sh in ranks:
+            sh.eval_p2p(ptrs[k])
+        check = rounds % CHECK == CHECK - 1
+        counts = [sh.step(bufs[k][r], count=check) for r, sh in enumerate(ranks)]
+        _exchange_trials(ranks)
+        if check:
+            active = sum(counts)
+        else:
+            assert all(c is None for c in counts)
+        rounds += 1
+    _exchange_results(ranks)
+    for sh in ranks:
+        r = sh.result(group=False)
+        for key in ("x", "lam", "n_iter", "n_evals", "status"):
+            np.testing.assert_array_equal(getattr(r, key), getattr(one, key), err_msg=key)
+
+
+@pytest.mark.gpu
+def test_device_sharded_config4_units():
+    """Config 4 (960^2, 16 blocks as evaluation units): the mu-sharded rounds
+    at 1 and 2 rank states reproduce the persistent kernel bit for bit, and
+    the reference goldens to 1e-9."""
+    import torch
+
+    import paper_2305_15163_b200 as P
+    from paper_2305_15163_b200.subdomain import ShardedSolve
+    inst = P.RomInstance.load(golden_path("c4_nm", "artifacts"))
+    g = dict(np.load(golden_path("c4_nm", "golden")))
+    mu = g["mu"][:3]
+    ref = P.solve_rom_batch(inst, mu)
+    res = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    for k in ("x", "lam", "n_iter", "status"):
+        np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=k)
+    for k in range(3):
+        assert _rel(res.x[k], g["x"][k]) < 1e-9 and _rel(res.lam[k], g["lam"][k]) < 1e-9
+    ranks = [ShardedSolve(inst, mu, P.SqpConfig(), r, 2) for r in range(2)]
+    gathered = torch.empty(2 * ranks[0].B * ranks[0].stride, dtype=torch.float64, device="cuda")
+    active = ranks[0].active
+    while active:
+        torch.cat([sh.eval().clone() for sh in ranks], out=gathered)
+        active = sum(sh.step(gathered) for sh in ranks)
+        _exchange_trials(ranks)
+    _exchange_results(ranks)
+    for sh in ranks:
+        r = sh.result(group=False)
+        np.testing.assert_array_equal(r.x, ref.x)
+        np.testing.assert_array_equal(r.n_iter, ref.n_iter)
