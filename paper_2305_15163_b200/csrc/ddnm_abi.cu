@@ -108,6 +108,22 @@ const std::vector<Kernels>& kernel_table() {
 
 }  // namespace
 
+// device buffers of one subdomain-sharded solve (ddnm_dd_*), sized for up to
+// `cap` mu; pooled in the context between solves (allocated once, reused)
+struct DdBuffers {
+  int cap = 0;
+  SlotState* st = nullptr;
+  double *vec = nullptr, *ecur = nullptr, *gbv = nullptr, *gJ = nullptr, *gJg = nullptr,
+         *kkt_g = nullptr, *eb_g = nullptr, *trials = nullptr;
+  int* active = nullptr;
+  void release() {
+    for (void* p : {(void*)st, (void*)vec, (void*)ecur, (void*)gbv, (void*)gJ, (void*)gJg,
+                    (void*)kkt_g, (void*)eb_g, (void*)trials, (void*)active})
+      if (p) cudaFree(p);
+    *this = DdBuffers{};
+  }
+};
+
 struct ddnm_ctx {
   int device = 0;
   int sms = 0;
@@ -138,6 +154,7 @@ struct ddnm_ctx {
   // full decode (ddnm_ctx_set_full_decoders)
   int map_kind = 0;
   int n_units = 0;            // evaluation units (0: blocks evaluated whole)
+  std::vector<DdBuffers> dd_pool;   // buffers of finished sharded solves, for reuse
   DecodeJob* d_jobs = nullptr;
   int state_len = 0, dec_max_hidden = 0, dec_mu_tile = 0;
 };
@@ -1245,6 +1262,7 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   if (c->counters) cudaFree(c->counters);
   if (c->prof) cudaFree(c->prof);
   if (c->d_jobs) cudaFree(c->d_jobs);
+  for (DdBuffers& b : c->dd_pool) b.release();
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -1611,19 +1629,11 @@ struct ddnm_dd {
   ddnm_ctx* c = nullptr;
   Params P{};
   int B = 0, ctas = 0;
-  SlotState* st = nullptr;
-  double* vec = nullptr;
-  double* ecur = nullptr;
-  int* active = nullptr;
-  // per-solve copies of the context's per-slot scratch (boundary values,
-  // Jacobian rows, KKT workspace): a sharded solve never shares them with
-  // another solve on the same context
-  double* gbv = nullptr;
-  double* gJ = nullptr;
-  double* gJg = nullptr;
-  double* kkt_g = nullptr;
-  double* eb_g = nullptr;         // evaluation buffers (when the context keeps them in L2)
-  double* trials = nullptr;       // own trial records [B][rec] (until ddnm_dd_set_trials)
+  // per-solve state and copies of the context's per-slot scratch (boundary
+  // values, Jacobian rows, KKT workspace, evaluation buffers when in L2,
+  // own trial records): a sharded solve never shares them with another
+  // solve on the same context; taken from / returned to the context's pool
+  DdBuffers buf;
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
 };
 
@@ -1637,14 +1647,14 @@ int eb_span(const ddnm_ctx* c, int lo, int hi, int* off) {
 
 int dd_run(ddnm_dd* d, const void* kern, cudaStream_t s, int32_t* n_active, int ctas = 0) {
   ddnm_ctx* c = d->c;
-  CUDA_TRY(cudaMemsetAsync(d->active, 0, sizeof(int), s));
+  CUDA_TRY(cudaMemsetAsync(d->buf.active, 0, sizeof(int), s));
   void* args[] = {&d->P};
   if (ctas == 0) ctas = d->ctas;
   if (ctas > 0)
     CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(c->threads), args, c->smem, s));
   if (n_active) {
     int h = 0;
-    CUDA_TRY(cudaMemcpyAsync(&h, d->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&h, d->buf.active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     *n_active = h;
   }
@@ -1684,23 +1694,38 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   d->B = B;
   d->ctas = (B + c->P.G - 1) / c->P.G;
   auto bail = [&](int r) { ddnm_dd_end(d); return r; };
-  // per-mu scratch (slot = mu); one CTA of spare slots for a step slice that
-  // starts mid-CTA (k_dd_step maps mu_lo + blockIdx.x * G + s)
-  const size_t slots = (size_t)(d->ctas + 1) * c->P.G;
-  if (cudaMalloc(&d->gbv, slots * std::max(c->tot_rows * 3, 1) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&d->gJ, slots * std::max(c->P.gJ_stride, 1) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&d->gJg, slots * std::max(c->P.gJg_stride, 1) * sizeof(double)) != cudaSuccess ||
-      (c->kkt_stride && cudaMalloc(&d->kkt_g, slots * c->kkt_stride * sizeof(double)) != cudaSuccess) ||
-      (c->ebg && cudaMalloc(&d->eb_g, slots * 2 * (size_t)c->P.eb_size * sizeof(double)) != cudaSuccess))
-    return bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve scratch"));
-  if (cudaMalloc(&d->st, (size_t)B * sizeof(SlotState)) != cudaSuccess ||
-      cudaMalloc(&d->vec, (size_t)B * 8 * c->P.nK * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&d->ecur, (size_t)B * c->P.eb_size * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&d->active, sizeof(int)) != cudaSuccess)
-    return bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve state"));
   const int rec = (c->P.n_D + 1 + 1) & ~1;
-  if (cudaMalloc(&d->trials, (size_t)B * rec * sizeof(double)) != cudaSuccess)
-    return bail(fail(DDNM_ENOMEM, "cannot allocate the trial records"));
+  // buffers: the smallest pooled set that holds B mu, else new ones
+  {
+    int best = -1;
+    for (int i = 0; i < (int)c->dd_pool.size(); ++i)
+      if (c->dd_pool[i].cap >= B && (best < 0 || c->dd_pool[i].cap < c->dd_pool[best].cap)) best = i;
+    if (best >= 0) {
+      d->buf = c->dd_pool[best];
+      c->dd_pool.erase(c->dd_pool.begin() + best);
+    }
+  }
+  DdBuffers& bf = d->buf;
+  if (bf.cap < B) {
+    bf.release();
+    bf.cap = B;
+    // per-mu scratch (slot = mu); one CTA of spare slots for a step slice that
+    // starts mid-CTA (k_dd_step maps mu_lo + blockIdx.x * G + s)
+    const size_t slots = (size_t)(d->ctas + 1) * c->P.G;
+    if (cudaMalloc(&bf.gbv, slots * std::max(c->tot_rows * 3, 1) * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&bf.gJ, slots * std::max(c->P.gJ_stride, 1) * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&bf.gJg, slots * std::max(c->P.gJg_stride, 1) * sizeof(double)) != cudaSuccess ||
+        (c->kkt_stride && cudaMalloc(&bf.kkt_g, slots * c->kkt_stride * sizeof(double)) != cudaSuccess) ||
+        (c->ebg && cudaMalloc(&bf.eb_g, slots * 2 * (size_t)c->P.eb_size * sizeof(double)) != cudaSuccess))
+      return bf.release(), bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve scratch"));
+    if (cudaMalloc(&bf.st, (size_t)B * sizeof(SlotState)) != cudaSuccess ||
+        cudaMalloc(&bf.vec, (size_t)B * 8 * c->P.nK * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&bf.ecur, (size_t)B * c->P.eb_size * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&bf.active, sizeof(int)) != cudaSuccess)
+      return bf.release(), bail(fail(DDNM_ENOMEM, "cannot allocate the sharded solve state"));
+    if (cudaMalloc(&bf.trials, (size_t)B * rec * sizeof(double)) != cudaSuccess)
+      return bf.release(), bail(fail(DDNM_ENOMEM, "cannot allocate the trial records"));
+  }
   Params& P = d->P;
   P = c->P;
   P.B = B;
@@ -1717,21 +1742,21 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   P.so.merit_hist = o->merit_hist; P.so.obj_hist = o->obj_hist; P.so.alpha_hist = o->alpha_hist;
   P.so.x0 = o->x0; P.so.lam0 = o->lam0;
   P.so.n_iter = o->n_iter; P.so.n_evals = o->n_evals; P.so.status = o->status; P.so.n_reg = o->n_reg;
-  P.gbv = d->gbv;
-  P.gJ = d->gJ;
-  P.gJg = d->gJg;
-  P.kkt_g = d->kkt_g;
-  P.eb_glob = d->eb_g;
+  P.gbv = bf.gbv;
+  P.gJ = bf.gJ;
+  P.gJg = bf.gJg;
+  P.kkt_g = bf.kkt_g;
+  P.eb_glob = bf.eb_g;
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
   P.b_lo = blk_lo;
   P.b_hi = blk_hi;
-  P.dd_st = d->st;
-  P.dd_vec = d->vec;
-  P.dd_ecur = d->ecur;
-  P.dd_active = d->active;
-  P.dd_trial = d->trials;
+  P.dd_st = bf.st;
+  P.dd_vec = bf.vec;
+  P.dd_ecur = bf.ecur;
+  P.dd_active = bf.active;
+  P.dd_trial = bf.trials;
   P.dd_rec = rec;
   P.dd_mu_lo = 0;
   P.dd_mu_hi = B;
@@ -1844,7 +1869,7 @@ int ddnm_dd_step(ddnm_dd* d, const double* d_gathered, int32_t nranks, const int
   if (rc) return rc;
   if (n_active) {
     int h = 0;
-    CUDA_TRY(cudaMemcpyAsync(&h, d->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&h, d->buf.active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     *n_active = h;
   }
@@ -1882,12 +1907,11 @@ int ddnm_dd_end(ddnm_dd* d) {
   if (!d) return 0;
   cudaSetDevice(d->c->device);
   cudaStreamSynchronize(d->stream);
-  if (d->st) cudaFree(d->st);
-  if (d->vec) cudaFree(d->vec);
-  if (d->ecur) cudaFree(d->ecur);
-  if (d->active) cudaFree(d->active);
-  for (double* p : {d->gbv, d->gJ, d->gJg, d->kkt_g, d->eb_g, d->trials})
-    if (p) cudaFree(p);
+  // back to the context's pool (the next sharded solve skips the mallocs)
+  if (d->buf.cap > 0) {
+    if (d->c->dd_pool.size() < 4) d->c->dd_pool.push_back(d->buf);
+    else d->buf.release();
+  }
   delete d;
   return 0;
 }
