@@ -84,8 +84,11 @@ __device__ __forceinline__ double hval(const double* H, int w, int i, int j) { r
 
 // --------------------------------------------------------------------------
 // phase A: one hidden unit for all active slots.
-// z accumulates latent column by latent column with separately rounded
-// products, exactly as hyper.py:184-188 / autoencoder.py:134-140.
+// z accumulates latent column by latent column (the order of hyper.py:184-188
+// / autoencoder.py:134-140) with fused multiply-adds -- the reference rounds
+// each product and each sum separately (numpy), so z agrees with it to an ulp
+// rather than bitwise; k_decode (ddnm_decode.cu) keeps the reference's
+// separately rounded order for the final decode.
 template <int G, int L>
 __device__ __forceinline__ void hidden_unit(const View& V, const DecDev& D, int k, int xo,
                                             int sig_off, unsigned mask) {
@@ -167,11 +170,20 @@ __device__ __forceinline__ void hidden_range(const View& V, const DecDev& D, int
 }
 
 // phase B: one decoder output (value + latent Jacobian row) for all slots.
-// Row sweep in CSR storage order (hyper.py:190-197), read from the
-// ELL-transposed copy of W2 (entry e of output o at [e][o]: a warp's lanes
-// read consecutive addresses), four entries per batch so their index, weight
-// and W1-row loads are all in flight together:
-//   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e W2_e act'_e W1[k_e, d]) * scale
+// Row sweep over the CSR row (hyper.py:190-197), read from the ELL-transposed
+// copy of W2 (entry e of output o at [e][o]: a warp's lanes read consecutive
+// addresses), several entries per batch so their index, weight and W1-row
+// loads are all in flight together:
+//   g = (sum_e W2_e act_e) * scale + shift,  J_d = (sum_e (W2_e act'_e) W1[k_e, d]) * scale
+// Association and order differ from the reference's on purpose: it forms
+// W2 (act' (.) W1) with scipy's CSR matvec in storage order; here each product
+// is (W2_e act'_e) W1[k_e, d], NQ lanes take interleaved entries and their
+// partial sums are added at the end.  Same terms, different rounding (the
+// decoder values and Jacobians agree with the oracle to ~1e-15, gated at
+// 1e-13).  What is bitwise is the reference's subsetting invariant
+// (test_hyper.py:194-201) within this kernel: an output's value and
+// Jacobian row do not depend on which other outputs the (sub)net keeps
+// (tests/test_units.py compares restricted units with whole blocks bitwise).
 template <int G, int L, int NQ>
 __device__ __forceinline__ void sweep_output(const View& V, const DecDev& D, int o, int q,
                                              bool valid, int sig_off, int g_off, bool gam,

@@ -136,3 +136,24 @@ def test_decode_edge_cases(gpu_instances):
     # errors only (no states kept)
     d = P.decode_batch(inst, s["x"][:1], fom_states=s["fom0"][None], keep_states=False)
     assert d.states is None and abs(d.error[0] - float(s["err0"])) <= 1e-12 * float(s["err0"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c0_nm", "c3s_nm"])
+def test_solve_subnet_rows_match_decode_rows(name, gpu_instances, goldens):
+    """SURVEY §4's invariant between the two device decoders: the HR subnet
+    rows the solve kernel evaluates (ddnm_eval_batch: interior outputs `io`)
+    equal the full interior decoder's rows at those positions (k_decode,
+    RomInstance.decode) -- to rounding, since the solve kernel contracts
+    differently (fma, split-lane row sums; see ddnm_solve.cuh phase A/B)
+    while k_decode keeps the reference's order."""
+    import paper_2305_15163_b200 as P
+    inst, g = gpu_instances[name], goldens[name]
+    x = g["x"][:4]
+    ev = P.eval_gradients_batch(inst, g["mu"][:4], x, g["lam"][:4], step=False)
+    dec = P.decode_batch(inst, x)
+    for k in range(4):
+        for b, (xi, xg) in enumerate(dec.blocks(k)):
+            io = inst.arrays[f"b{b}_io"]
+            sub = ev.block(k, b)["int_g"]
+            assert np.max(np.abs(sub - xi[io])) <= 1e-14 * max(np.max(np.abs(xi[io])), 1e-300)
