@@ -350,6 +350,16 @@ int ddnm_dd_set_trials(ddnm_dd* dd, double* d_trials, int64_t cap, int32_t mu_lo
 
 int ddnm_dd_end(ddnm_dd* dd);
 
+/* Evaluate with the batch-wide kernels (one lane per mu; csrc/ddnm_wide.h)
+ * instead of one CTA slot per mu: for a handle that owns every block
+ * (blk_lo = 0, blk_hi = n_blocks) of an eligible instance (autoencoder maps,
+ * WFPC coupling, collocation HR, banded decoders).  ddnm_dd_eval then writes
+ * one packet per LANE (a running mu may come with several candidate step
+ * lengths per round), so d_packets must hold max(2 * roundup32(B), 1024) rows;
+ * ddnm_dd_step reads them from the same buffer with nranks = 1.  ddnm_solve_batch[_device] takes this path by
+ * itself for large batches (DDNM_WIDE=0/1 forces). */
+int ddnm_dd_set_wide(ddnm_dd* dd, int32_t on);
+
 /* CUDA IPC of a device buffer between the processes of one node (64-byte
  * handles, exchanged by the caller), for ddnm_dd_eval_p2p's peer buffers.
  * A handle maps the start of the cudaMalloc allocation holding dptr, so the

@@ -15,6 +15,7 @@
 #include "../../include/ddnm.h"
 #include "ddnm_device.cuh"
 #include "ddnm_registry.h"
+#include "ddnm_wide.h"
 
 using namespace ddnm;
 
@@ -116,7 +117,14 @@ struct DdBuffers {
   double *vec = nullptr, *ecur = nullptr, *gbv = nullptr, *gJ = nullptr, *gJg = nullptr,
          *kkt_g = nullptr, *eb_g = nullptr, *trials = nullptr;
   int* active = nullptr;
+  // batch-wide evaluation (ddnm_wide.h): its scratch and the packets of the
+  // in-library round loop
+  ddnm::WideBuffers wide;
+  double* pk = nullptr;
+  size_t pk_len = 0;
   void release() {
+    wide.release();
+    if (pk) cudaFree(pk);
     for (void* p : {(void*)st, (void*)vec, (void*)ecur, (void*)gbv, (void*)gJ, (void*)gJg,
                     (void*)kkt_g, (void*)eb_g, (void*)trials, (void*)active})
       if (p) cudaFree(p);
@@ -155,6 +163,8 @@ struct ddnm_ctx {
   int map_kind = 0;
   int n_units = 0;            // evaluation units (0: blocks evaluated whole)
   std::vector<DdBuffers> dd_pool;   // buffers of finished sharded solves, for reuse
+  ddnm::Wide* wide = nullptr;       // batch-wide evaluation program (null: not eligible)
+  std::string wide_why;             // why not
   DecodeJob* d_jobs = nullptr;
   int state_len = 0, dec_max_hidden = 0, dec_mu_tile = 0;
 };
@@ -1211,6 +1221,9 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   if (cudaMalloc(&c->work, 4 * sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->counters, 2 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cudaMalloc failed"));
+  // batch-wide evaluation program (lane = mu), when the instance is eligible
+  if (ddnm::wide_build(a, P, c->sms, &c->wide, c->wide_why) != 0)
+    return bail(fail(DDNM_ECUDA, "cannot upload the wide evaluation tables"));
   *out = c;
   return 0;
 }
@@ -1263,6 +1276,7 @@ int ddnm_ctx_destroy(ddnm_ctx* c) {
   if (c->prof) cudaFree(c->prof);
   if (c->d_jobs) cudaFree(c->d_jobs);
   for (DdBuffers& b : c->dd_pool) b.release();
+  if (c->wide) ddnm::wide_free(c->wide);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -1322,11 +1336,33 @@ static int fill_nan(cudaStream_t s, double* p, size_t n) {
   return 0;
 }
 
+static int solve_wide(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0,
+                      const double* d_lam0, const ddnm_sqp_cfg* cfg, ddnm_solve_out* o,
+                      cudaStream_t s);
+
+// which engine solves a batch: the persistent kernel (one slot per mu) or the
+// round-synchronous batch-wide kernels (one lane per mu, ddnm_wide.h).
+// DDNM_WIDE=0/1 forces; otherwise wide from DDNM_WIDE_MIN_B mu on (default:
+// see wide_min_batch) when the instance is eligible.
+static int wide_min_batch() {
+  if (const char* e = getenv("DDNM_WIDE_MIN_B")) return atoi(e);
+  return 1 << 30;
+}
+static bool use_wide(const ddnm_ctx* c, int B) {
+  if (!c->wide) return false;
+  if (const char* e = getenv("DDNM_WIDE")) return atoi(e) != 0;
+  return B >= wide_min_batch();
+}
+
 int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0,
                             const double* d_lam0, const ddnm_sqp_cfg* cfg, ddnm_solve_out* o,
                             void* stream) {
   if (!c || !cfg || !o || !d_mu || !o->x || !o->lam) return fail(DDNM_EINVAL, "null argument");
   if (B < 0) return fail(DDNM_EINVAL, "negative batch");
+  if (B > 0 && use_wide(c, B)) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    return solve_wide(c, B, d_mu, d_x0, d_lam0, cfg, o, stream ? (cudaStream_t)stream : c->stream);
+  }
   if (!(cfg->tol > 0) || cfg->max_iter < 1 || !(cfg->armijo_c1 > 0) || !(cfg->backtrack_factor > 0) ||
       !(cfg->backtrack_factor < 1) || cfg->max_halvings < 0)
     return fail(DDNM_EINVAL, "invalid solver configuration");
@@ -1635,6 +1671,8 @@ struct ddnm_dd {
   // solve on the same context; taken from / returned to the context's pool
   DdBuffers buf;
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
+  bool wide = false;              // evaluations by the batch-wide kernels (ddnm_wide.h)
+  size_t wide_pk_cap = 0;         // doubles in the caller's packet buffer when known
 };
 
 namespace {
@@ -1652,6 +1690,13 @@ int dd_run(ddnm_dd* d, const void* kern, cudaStream_t s, int32_t* n_active, int 
   if (ctas == 0) ctas = d->ctas;
   if (ctas > 0)
     CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(c->threads), args, c->smem, s));
+  if (getenv("DDNM_WIDE_SYNC")) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess)
+      fprintf(stderr, "ddnm: %s (init %d, %d CTAs, B %d) failed: %s\n",
+              kern == c->K.dd_step ? "k_dd_step" : "k_dd_eval", d->P.dd_init, ctas, d->P.B,
+              cudaGetErrorString(e));
+  }
   if (n_active) {
     int h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, d->buf.active, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1782,7 +1827,34 @@ int ddnm_dd_eval(ddnm_dd* d, double* d_packets, int64_t pk_stride, void* stream)
   d->stream = s;
   d->P.dd_pk = d_packets;
   d->P.pk_stride = (int)pk_stride;
+  if (d->wide) {
+    if ((size_t)pk_stride * ddnm::wide_packet_rows(d->buf.wide) > d->wide_pk_cap && d->wide_pk_cap)
+      return fail(DDNM_EINVAL, "packet buffer smaller than one row per lane");
+    if (ddnm::wide_eval(d->c->wide, d->P, d->buf.wide, d_packets, (int)pk_stride, s) != 0)
+      return fail(DDNM_ECUDA, "wide evaluation launch failed");
+    return 0;
+  }
   return dd_run(d, d->c->K.dd_eval, s, nullptr);
+}
+
+/* Switch a sharded solve that owns every block to the batch-wide evaluation
+ * kernels (ddnm_wide.h): same packets to rounding, one lane per mu. */
+int ddnm_dd_set_wide(ddnm_dd* d, int32_t on) {
+  if (!d) return fail(DDNM_EINVAL, "null argument");
+  if (!on) { d->wide = false; d->P.dd_vbase = nullptr; d->P.dd_kof = nullptr; return 0; }
+  ddnm_ctx* c = d->c;
+  if (!c->wide) return fail(DDNM_EUNSUPPORTED, "instance not eligible for the wide evaluation: " + c->wide_why);
+  if (d->P.b_lo != 0 || d->P.b_hi != d->P.nb)
+    return fail(DDNM_EUNSUPPORTED, "the wide evaluation needs every block on this rank");
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::string err;
+  if (ddnm::wide_alloc(c->wide, d->B, &d->buf.wide, err) != 0) return fail(DDNM_ENOMEM, err);
+  if (ddnm::wide_begin(c->wide, d->P, d->buf.wide, d->stream) != 0)
+    return fail(DDNM_ECUDA, "wide boundary-value launch failed");
+  d->P.dd_vbase = d->buf.wide.vbase;
+  d->P.dd_kof = d->buf.wide.kof;
+  d->wide = true;
+  return 0;
 }
 
 int ddnm_dd_eval_p2p(ddnm_dd* d, double* const* peers, int32_t nranks, int32_t rank,
@@ -1917,3 +1989,44 @@ int ddnm_dd_end(ddnm_dd* d) {
 }
 
 }  // extern "C"
+
+// The whole batched solve as rounds of the batch-wide evaluation and the SQP
+// step kernel (k_dd_step: Armijo decision, KKT solve, trial point), looped
+// here: rounds are launched back to back and the running count is read every
+// few rounds (rounds after the last mu finished are empty launches).
+static int solve_wide(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0,
+                      const double* d_lam0, const ddnm_sqp_cfg* cfg, ddnm_solve_out* o,
+                      cudaStream_t s) {
+  ddnm_dd* d = nullptr;
+  int rc = ddnm_dd_begin(c, B, d_mu, d_x0, d_lam0, cfg, 0, c->nb, o, s, &d, nullptr);
+  if (rc) return rc;
+  auto bail = [&](int r) { const std::string keep = g_err; ddnm_dd_end(d); g_err = keep; return r; };
+  if ((rc = ddnm_dd_set_wide(d, 1))) return bail(rc);
+  int off = 0;
+  const int stride = eb_span(c, 0, c->nb, &off);
+  DdBuffers& bf = d->buf;
+  const size_t pk_need = ddnm::wide_packet_rows(bf.wide) * stride;   // one packet per lane
+  if (bf.pk_len < pk_need) {
+    if (bf.pk) cudaFree(bf.pk);
+    bf.pk = nullptr;
+    bf.pk_len = 0;
+    if (cudaMalloc(&bf.pk, pk_need * sizeof(double)) != cudaSuccess)
+      return bail(fail(DDNM_ENOMEM, "cannot allocate the evaluation packets"));
+    bf.pk_len = pk_need;
+  }
+  d->wide_pk_cap = bf.pk_len;
+  const int32_t bounds[2] = {0, c->nb};
+  int check = 4;
+  if (const char* e = getenv("DDNM_DD_CHECK")) check = std::max(1, atoi(e));
+  int32_t active = B;
+  for (long long round = 0;; ++round) {
+    if ((rc = ddnm_dd_eval(d, bf.pk, stride, s))) return bail(rc);
+    const bool count = round % check == check - 1;
+    if ((rc = ddnm_dd_step(d, bf.pk, 1, bounds, stride, s, count ? &active : nullptr))) return bail(rc);
+    if (count && active == 0) break;
+    if (count) bf.wide.lane_bound = std::min<long long>(bf.wide.vpad, (long long)active * 8);
+  }
+  bf.wide.lane_bound = 0;
+  return ddnm_dd_end(d);
+}
+

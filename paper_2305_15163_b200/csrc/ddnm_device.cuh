@@ -228,6 +228,11 @@ struct Params {
   // the mu it advances, [dd_mu_lo, dd_mu_hi) (its slice), k_dd_eval reads all
   double* dd_trial;
   int dd_rec, dd_mu_lo, dd_mu_hi;
+  // batch-wide evaluation (ddnm_wide.cu): dd_gath holds one packet per lane;
+  // mu's candidates are rows dd_vbase[mu] .. + dd_kof[mu] - 1 (null: one
+  // packet per mu per rank, the subdomain-sharded layout above)
+  const int* dd_vbase;
+  const int* dd_kof;
   // peer-memory all-gather fused into k_dd_eval: when dd_npeers > 0 the
   // packets go straight to every rank's gathered buffer (NVLink stores)
   double* dd_peers[MAXB];
@@ -350,6 +355,23 @@ __device__ inline void exact_uv(double a, double lam, double x, double y, double
   const double psi = a * (1.0 + x) + (ep + em) * cy;
   u = -2.0 * nu * (a + lam * (ep - em) * cy) / psi;
   v = 2.0 * nu * lam * (ep + em) * sy / psi;
+}
+
+// boundary values (bx, by, c) of assemble() at every sampled row
+// (burgers.py:188-210): ghost points just outside the edges the node touches.
+__device__ inline void row_bvals(const Params& P, const StRows& RW, int row, double a, double lm, double* out) {
+  const double hx = P.hx, hy = P.hy, nu = P.nu;
+  const int bflags = RW.bflags[row];
+  const double xc = RW.xc[row], yc = RW.yc[row];
+  const bool isv = (bflags >> 4) & 1;
+  double exl = 0.0, exr = 0.0, eyb = 0.0, eyt = 0.0, u, v;
+  if (bflags & 1) { exact_uv(a, lm, -1.0, yc, nu, u, v); exl = isv ? v : u; }
+  if (bflags & 2) { exact_uv(a, lm, 1.0, yc, nu, u, v); exr = isv ? v : u; }
+  if (bflags & 4) { exact_uv(a, lm, xc, 0.0, nu, u, v); eyb = isv ? v : u; }
+  if (bflags & 8) { exact_uv(a, lm, xc, 0.05, nu, u, v); eyt = isv ? v : u; }
+  out[0] = (-1.0 / (2.0 * hx)) * (exl - exr);
+  out[1] = (-1.0 / (2.0 * hy)) * (eyb - eyt);
+  out[2] = (nu / (hx * hx)) * (exl + exr) + (nu / (hy * hy)) * (eyb + eyt);
 }
 
 }  // namespace ddnm

@@ -1980,23 +1980,6 @@ static __device__ void warp_rbf(const Params& P, double a, double lm, double* x0
   __syncwarp();
 }
 
-// boundary values (bx, by, c) of assemble() at every sampled row
-// (burgers.py:188-210): ghost points just outside the edges the node touches.
-static __device__ void row_bvals(const Params& P, const StRows& RW, int row, double a, double lm, double* out) {
-  const double hx = P.hx, hy = P.hy, nu = P.nu;
-  const int bflags = RW.bflags[row];
-  const double xc = RW.xc[row], yc = RW.yc[row];
-  const bool isv = (bflags >> 4) & 1;
-  double exl = 0.0, exr = 0.0, eyb = 0.0, eyt = 0.0, u, v;
-  if (bflags & 1) { exact_uv(a, lm, -1.0, yc, nu, u, v); exl = isv ? v : u; }
-  if (bflags & 2) { exact_uv(a, lm, 1.0, yc, nu, u, v); exr = isv ? v : u; }
-  if (bflags & 4) { exact_uv(a, lm, xc, 0.0, nu, u, v); eyb = isv ? v : u; }
-  if (bflags & 8) { exact_uv(a, lm, xc, 0.05, nu, u, v); eyt = isv ? v : u; }
-  out[0] = (-1.0 / (2.0 * hx)) * (exl - exr);
-  out[1] = (-1.0 / (2.0 * hy)) * (eyb - eyt);
-  out[2] = (nu / (hx * hx)) * (exl + exr) + (nu / (hy * hy)) * (eyb + eyt);
-}
-
 // --------------------------------------------------------------------------
 // per-slot pieces of one SQP round, shared by the persistent kernel (k_solve)
 // and the round-synchronous subdomain-sharded kernels (k_dd_eval / k_dd_step)
@@ -2295,7 +2278,7 @@ __device__ __forceinline__ unsigned dd_load_state(const View& V, int* mu_of, int
   if (threadIdx.x < G) {
     const int s = threadIdx.x, mu = mu0 + blockIdx.x * G + s;
     if (mu < mu_hi) st[s] = P.dd_st[mu];
-    else { st[s].mu = -1; st[s].phase = PH_IDLE; }
+    else { st[s] = SlotState{}; st[s].mu = -1; st[s].phase = PH_IDLE; }   // (need_kkt = 0: shared memory is not zeroed)
     mu_of[s] = mu;
   }
   __syncthreads();
@@ -2422,7 +2405,12 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
   if (tid == 0) s_kkts = 0;
   zero_slots(V);
   // state, current eval buffer (slot 0) and the gathered trial evaluation
-  // (slot 1; slot 0 for the first evaluation of a new mu)
+  // (slot 1; slot 0 for the first evaluation of a new mu).  With the
+  // batch-wide evaluation (dd_vbase) a mu may come with several evaluations,
+  // its next step lengths alpha, alpha f, ... (ddnm_wide.cu): they are
+  // consumed in order until one is accepted -- exactly the decisions the
+  // reference takes one evaluation at a time (sqp.py:262-293).
+  __shared__ int s_k[G], s_go[G];
   for (int s = 0; s < G; ++s) {
     if (!((mask >> s) & 1u)) continue;
     const int mu = s_mu[s];
@@ -2433,19 +2421,48 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
       const double* ec = P.dd_ecur + (size_t)mu * P.eb_size;
       for (int i = tid; i < P.eb_size; i += T) V.eb(s, 0)[i] = ec[i];
     }
-    double* e = V.eb(s, ebi);
-    for (int r = 0; r < P.dd_nranks; ++r) {
-      const int b0 = P.dd_bnd[r], b1 = P.dd_bnd[r + 1];
-      const int off = P.blk[b0].eb_off;
-      const int len = (b1 < P.nb ? P.blk[b1].eb_off : P.eb_rho) - off;
-      const double* g = P.dd_gath + ((size_t)r * P.B + mu) * P.pk_stride;
-      for (int i = tid; i < len; i += T) e[off + i] = g[i];
-    }
     if (tid == 0) { s_cur[s] = 0; s_ebi[s] = ebi; }
   }
+  if (tid < G) {
+    const bool on = (mask >> tid) & 1u;
+    s_go[tid] = on ? 1 : 0;
+    s_k[tid] = on && P.dd_kof ? P.dd_kof[s_mu[tid]] : 1;
+  }
   __syncthreads();
-  if (warp < G && ((mask >> warp) & 1u)) slot_decide<NI, NG>(V, warp, s_ebi[warp], s_cur);
-  __syncthreads();
+  for (int j = 0;; ++j) {
+    bool any = false;
+    for (int s = 0; s < G; ++s) any = any || (s_go[s] && j < s_k[s]);
+    if (!any) break;
+    for (int s = 0; s < G; ++s) {
+      if (!(s_go[s] && j < s_k[s])) continue;
+      const int mu = s_mu[s];
+      double* e = V.eb(s, s_ebi[s]);
+      if (P.dd_vbase) {
+        const int off = P.blk[0].eb_off, len = P.eb_rho - off;
+        const double* g = P.dd_gath + (size_t)(P.dd_vbase[mu] + j) * P.pk_stride;
+        for (int i = tid; i < len; i += T) e[off + i] = g[i];
+      } else {
+        for (int r = 0; r < P.dd_nranks; ++r) {
+          const int b0 = P.dd_bnd[r], b1 = P.dd_bnd[r + 1];
+          const int off = P.blk[b0].eb_off;
+          const int len = (b1 < P.nb ? P.blk[b1].eb_off : P.eb_rho) - off;
+          const double* g = P.dd_gath + ((size_t)r * P.B + mu) * P.pk_stride;
+          for (int i = tid; i < len; i += T) e[off + i] = g[i];
+        }
+      }
+    }
+    __syncthreads();
+    if (warp < G && s_go[warp] && j < s_k[warp]) {
+      slot_decide<NI, NG>(V, warp, s_ebi[warp], s_cur);
+      if ((tid & 31) == 0) {
+        // rejected with halvings left: the next candidate is this mu's next trial
+        const SlotState& S = st[warp];
+        s_go[warp] = S.phase == PH_TRIAL && S.need_kkt == 0 ? 1 : 0;
+        if (P.dd_vbase) atomicAdd(P.counters, (unsigned long long)P.nb);
+      }
+    }
+    __syncthreads();
+  }
   kkt_advance<G, NI, NG, KG>(V, s_cur, s_kres, s_kflag, &s_kkts);
   if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) slot_write(V, warp);
   __syncthreads();

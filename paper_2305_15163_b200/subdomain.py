@@ -132,6 +132,11 @@ class DeviceRoundEngine:
             _all_gather(flat, flat[rank * chunk * row:(rank + 1) * chunk * row].clone(), world,
                         group)
 
+    def set_wide(self, on: bool = True) -> None:
+        """Evaluate with the batch-wide kernels (one lane per mu) instead of
+        k_dd_eval; needs every block on this rank."""
+        N.check(N.lib().ddnm_dd_set_wide(self.h, 1 if on else 0))
+
     def eval(self, packets, stride: int) -> None:
         N.check(N.lib().ddnm_dd_eval(self.h, C.c_void_p(packets.data_ptr()), stride,
                                      self._stream()))

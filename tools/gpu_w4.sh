@@ -1,0 +1,6 @@
+set -x
+timeout 300 python tools/wide_check.py c0_nm 4096 2>&1 | tail -3
+timeout 300 python tools/wide_spec_check.py c0_nm 1024 2>&1 | tail -8
+timeout 300 python tools/wide_check.py tiny_nm 64 2>&1 | tail -3
+ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/w4_launches.csv python tools/prof_wide.py c0_nm 4096 1 > gpurun_out/w4_ncu.log 2>&1
+tail -2 gpurun_out/w4_ncu.log
