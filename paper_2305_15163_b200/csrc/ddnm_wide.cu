@@ -182,25 +182,70 @@ __device__ __forceinline__ long long wide_next(int* counter) {
   return __shfl_sync(0xffffffffu, v, 0);
 }
 
+// --- per-warp weight staging (cp.async, double buffered) ---------------------
+// A tile's weights -- its W2 stream, the W1 rows and biases of its hidden
+// window, the scale/shift of its outputs: at most one ring of rows -- are
+// copied global -> shared asynchronously one tile ahead, so the sweep and the
+// hidden layer read them as broadcast shared loads and never wait on L2.
+// Layout of one buffer (doubles): W2 [32][4] | W1 [32][LPM] | b1 [32] | scale[4] shift[4]
+__host__ __device__ constexpr int wide_lp(int L) { return (L + 1) & ~1; }
+__host__ __device__ constexpr int wide_stage_doubles(int lpm) { return 128 + 32 * lpm + 32 + 8; }
+// doubles of shared memory per decoder warp: ring (32 x 32 double2) + 2 buffers
+__host__ __device__ constexpr int wide_warp_doubles(int lpm) { return 2 * WRING * 32 + 2 * wide_stage_doubles(lpm); }
+
+__device__ __forceinline__ void wide_cp16(double* smem, const double* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void wide_cp8(double* smem, const double* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void wide_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wide_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct WTileR { int o0, cnt, klo, khi, soff; };
+__device__ __forceinline__ WTileR wide_tile_load(const WTile* tp) {
+  WTileR t;
+  t.o0 = __ldg(&tp->o0); t.cnt = __ldg(&tp->cnt); t.klo = __ldg(&tp->klo);
+  t.khi = __ldg(&tp->khi); t.soff = __ldg(&tp->soff);
+  return t;
+}
+
+template <int L, int LPM>
+__device__ __forceinline__ void wide_stage(const WDecDev& D, const WTileR& t, double* buf) {
+  constexpr int T = wide_tile_outputs(L), LP = wide_lp(L);
+  const int lane = threadIdx.x & 31;
+  const int nk = t.khi - t.klo;
+  const double* g2 = D.w2 + (size_t)t.soff;
+  for (int i = lane; i < nk * (T / 2); i += 32) wide_cp16(buf + 2 * i, g2 + 2 * i);
+  const double* g1 = D.W1p + (size_t)t.klo * LP;
+  for (int i = lane; i < nk * (LP / 2); i += 32) wide_cp16(buf + 128 + 2 * i, g1 + 2 * i);
+  if (lane < nk) wide_cp8(buf + 128 + 32 * LPM + lane, D.b1 + t.klo + lane);
+  if (lane < t.cnt) wide_cp8(buf + 128 + 32 * LPM + 32 + lane, D.scale + t.o0 + lane);
+  else if (lane >= 4 && lane - 4 < t.cnt) wide_cp8(buf + 128 + 32 * LPM + 32 + lane, D.shift + t.o0 + lane - 4);
+  // (scale at [0, 4), shift at [4, 8) of the last 8 doubles)
+}
+
 template <int L, int CNT>
-__device__ __forceinline__ void wide_sweep(const double2* ring, const double* __restrict__ W1p,
-                                           const double* __restrict__ w2, int klo, int khi,
+__device__ __forceinline__ void wide_sweep(const double2* ring, const double* stg, int klo, int khi,
                                            double (&acc)[wide_tile_outputs(L)][L + 1]) {
-  constexpr int T = wide_tile_outputs(L), LP = (L + 1) & ~1;
-  const double2* w1 = reinterpret_cast<const double2*>(W1p) + (size_t)klo * (LP / 2);
-  const double2* wv = reinterpret_cast<const double2*>(w2);
+  constexpr int T = wide_tile_outputs(L), LP = wide_lp(L);
+  const double2* wv = reinterpret_cast<const double2*>(stg);
+  const double2* w1 = reinterpret_cast<const double2*>(stg + 128);
 #pragma unroll 2
   for (int k = klo; k < khi; ++k) {
     const double2 sd = ring[(k & (WRING - 1)) * 32];
     double w[LP], v[T];
 #pragma unroll
     for (int i = 0; i < LP / 2; ++i) {
-      const double2 t = __ldg(w1 + i);
+      const double2 t = w1[i];
       w[2 * i] = t.x; w[2 * i + 1] = t.y;
     }
 #pragma unroll
     for (int i = 0; i < T / 2; ++i) {
-      const double2 t = __ldg(wv + i);
+      const double2 t = wv[i];
       v[2 * i] = t.x; v[2 * i + 1] = t.y;
     }
     w1 += LP / 2;
@@ -237,32 +282,44 @@ __device__ __forceinline__ void wide_trial_point(const WArgs& A, int e, int xoff
   }
 }
 
-template <int L>
+template <int L, int LPM>
 __device__ __forceinline__ void wide_dec_part(const WArgs& A, const WDecDev& D, int t0, int t1,
-                                              int tile, int nact, double2* ring) {
-  constexpr int T = wide_tile_outputs(L), LP = (L + 1) & ~1;
+                                              int tile, int nact, double* wsm) {
+  constexpr int T = wide_tile_outputs(L), LP = wide_lp(L), STG = wide_stage_doubles(LPM);
   const int lane = threadIdx.x & 31;
+  double2* ring = reinterpret_cast<double2*>(wsm) + lane;
+  double* stg0 = wsm + 2 * WRING * 32;
   double x[L];
   wide_trial_point<L>(A, A.act[min(tile * 32 + lane, nact - 1)], D.xoff, x);
   double* out = A.gj + ((size_t)tile * A.S + D.gj_off) * 32 + lane;
-  int next_k = __ldg(&D.tiles[t0].klo);
   const int act = D.act;
+  // tile ti staged in buffer cur, tile ti + 1's record loaded (staged below)
+  WTileR m0 = wide_tile_load(D.tiles + t0);
+  WTileR m1 = t0 + 1 < t1 ? wide_tile_load(D.tiles + t0 + 1) : m0;
+  int next_k = m0.klo, cur = 0;
+  __syncwarp();                      // the previous item's reads of the buffers are done
+  wide_stage<L, LPM>(D, m0, stg0);
+  wide_cp_commit();
   for (int ti = t0; ti < t1; ++ti) {
-    const WTile* tp = D.tiles + ti;
-    const int o0 = __ldg(&tp->o0), cnt = __ldg(&tp->cnt), klo = __ldg(&tp->klo),
-              khi = __ldg(&tp->khi), soff = __ldg(&tp->soff);
+    const WTileR m2 = ti + 2 < t1 ? wide_tile_load(D.tiles + ti + 2) : m1;
+    if (ti + 1 < t1) wide_stage<L, LPM>(D, m1, stg0 + (cur ^ 1) * STG);
+    wide_cp_commit();
+    wide_cp_wait<1>();
+    __syncwarp();
+    const double* stg = stg0 + cur * STG;
+    const int klo = m0.klo, khi = m0.khi, cnt = m0.cnt;
     // hidden units of the window not in the ring yet: z = b1 + W1 x in latent
     // order (hyper.py:184-188), activation and derivative (autoencoder.py:31-45)
 #pragma unroll 2
     for (int k = max(next_k, klo); k < khi; ++k) {
-      const double2* wr = reinterpret_cast<const double2*>(D.W1p) + (size_t)k * (LP / 2);
+      const double2* wr = reinterpret_cast<const double2*>(stg + 128) + (k - klo) * (LP / 2);
       double w[LP];
 #pragma unroll
       for (int i = 0; i < LP / 2; ++i) {
-        const double2 t = __ldg(wr + i);
+        const double2 t = wr[i];
         w[2 * i] = t.x; w[2 * i + 1] = t.y;
       }
-      double z = __ldg(D.b1 + k);
+      double z = stg[128 + 32 * LPM + (k - klo)];
 #pragma unroll
       for (int d = 0; d < L; ++d) z = fma(w[d], x[d], z);
       double a, da;
@@ -275,44 +332,47 @@ __device__ __forceinline__ void wide_dec_part(const WArgs& A, const WDecDev& D, 
     for (int j = 0; j < T; ++j)
 #pragma unroll
       for (int d = 0; d <= L; ++d) acc[j][d] = 0.0;
-    const double* w2 = D.w2 + (size_t)soff;
     if constexpr (T == 4) {
-      if (cnt == 4) wide_sweep<L, 4>(ring, D.W1p, w2, klo, khi, acc);
-      else if (cnt == 3) wide_sweep<L, 3>(ring, D.W1p, w2, klo, khi, acc);
-      else if (cnt == 2) wide_sweep<L, 2>(ring, D.W1p, w2, klo, khi, acc);
-      else wide_sweep<L, 1>(ring, D.W1p, w2, klo, khi, acc);
+      if (cnt == 4) wide_sweep<L, 4>(ring, stg, klo, khi, acc);
+      else if (cnt == 3) wide_sweep<L, 3>(ring, stg, klo, khi, acc);
+      else if (cnt == 2) wide_sweep<L, 2>(ring, stg, klo, khi, acc);
+      else wide_sweep<L, 1>(ring, stg, klo, khi, acc);
     } else {
-      if (cnt == 2) wide_sweep<L, 2>(ring, D.W1p, w2, klo, khi, acc);
-      else wide_sweep<L, 1>(ring, D.W1p, w2, klo, khi, acc);
+      if (cnt == 2) wide_sweep<L, 2>(ring, stg, klo, khi, acc);
+      else wide_sweep<L, 1>(ring, stg, klo, khi, acc);
     }
 #pragma unroll
     for (int j = 0; j < T; ++j) {
       if (j >= cnt) break;
-      const int o = o0 + j;
-      const double scl = __ldg(D.scale + o), sh = __ldg(D.shift + o);
+      const int o = m0.o0 + j;
+      const double scl = stg[128 + 32 * LPM + 32 + j], sh = stg[128 + 32 * LPM + 36 + j];
       double* p = out + (size_t)o * (L + 1) * 32;
       p[0] = __dadd_rn(__dmul_rn(acc[j][0], scl), sh);
 #pragma unroll
       for (int d = 0; d < L; ++d) p[(1 + d) * 32] = acc[j][1 + d] * scl;
     }
+    __syncwarp();                    // buffer cur is free for the tile after next
+    m0 = m1; m1 = m2; cur ^= 1;
   }
+  wide_cp_wait<0>();
 }
 
 template <int NI, int NG>
 __global__ void __launch_bounds__(WDEC_WARPS * 32, 1) k_wide_dec(const __grid_constant__ WArgs A) {
+  constexpr int LPM = wide_lp(NI) > wide_lp(NG) ? wide_lp(NI) : wide_lp(NG);
   const int nact = A.ctl[0];
   if (nact <= 0) return;
   const int ntile = (nact + 31) >> 5, mode = wide_mode(nact);
   const WPart* parts = A.parts[mode];
   const long long total = (long long)A.nparts[mode] * ntile;
-  double2* ring = wide_ring + (threadIdx.x >> 5) * (WRING * 32) + (threadIdx.x & 31);
+  double* wsm = reinterpret_cast<double*>(wide_ring) + (size_t)(threadIdx.x >> 5) * wide_warp_doubles(LPM);
   for (long long item = wide_next(A.ctl + 1); item < total; item = wide_next(A.ctl + 1)) {
     const int pi = (int)(item / ntile), tile = (int)(item - (long long)pi * ntile);
     const WPart* pp = parts + pi;
     const int b = __ldg(&pp->blk), which = __ldg(&pp->which), t0 = __ldg(&pp->t0), t1 = __ldg(&pp->t1);
     const WBlockDev& B = A.blk[b];
-    if (which == 0) wide_dec_part<NI>(A, B.dec[0], t0, t1, tile, nact, ring);
-    else wide_dec_part<NG>(A, B.dec[1], t0, t1, tile, nact, ring);
+    if (which == 0) wide_dec_part<NI, LPM>(A, B.dec[0], t0, t1, tile, nact, wsm);
+    else wide_dec_part<NG, LPM>(A, B.dec[1], t0, t1, tile, nact, wsm);
   }
 }
 
@@ -354,9 +414,13 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
   const double* gG = A.gj + ((size_t)tile * A.S + B.dec[1].gj_off) * 32 + lane;
   const StRows& RW = B.rows;
   const int nr = B.nrows;
-  auto val = [&](int c) -> double {
-    return c >= 0 ? gI[(size_t)c * (NI + 1) * 32] : gG[(size_t)(-1 - c) * (NG + 1) * 32];
+  // offset of an entry's g value from gI (its Jacobian row follows it):
+  // interior output c, or interface output -1 - c of the block's second decoder
+  const long long goff = (long long)(B.dec[1].gj_off - B.dec[0].gj_off) * 32;
+  auto slot = [&](int c) -> long long {
+    return c >= 0 ? (long long)c * (NI + 1) * 32 : goff + (long long)(-1 - c) * (NG + 1) * 32;
   };
+  constexpr int LM = NI > NG ? NI : NG;
   double acc[NA];
 #pragma unroll
   for (int q = 0; q < NA; ++q) acc[q] = 0.0;
@@ -364,26 +428,65 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
 #pragma unroll
   for (int i = 0; i < W; ++i) proj[i] = 0.0;
   double rr = 0.0;
+  // Every value a row needs from memory -- the g of its <= 6 columns and of
+  // the node's (u, v), its boundary values, the Jacobian rows of its columns:
+  // WROW_SLOTS coalesced 256-byte lines per warp -- has an address that
+  // depends on the row only, so row r + 1 is fetched into shared memory with
+  // cp.async (each lane its own 8 bytes of every line) while row r is computed:
+  // ~90 lines in flight per warp instead of what fits in registers.  A lane
+  // reads back only what it copied itself (no warp synchronisation).  Rows
+  // are padded to MAXE entries with zero coefficients on a valid column;
+  // adding their exact zeros changes no sum.
+  constexpr int NSL = 11 + MAXE * LM;
+  double* pbuf = red + (size_t)warp * 2 * NSL * 32 + lane;
+  auto fetch = [&](int row, double* buf) {
+    const int cu = __ldg(RW.src_gu + row), cv = __ldg(RW.src_gv + row);
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) {
+      const int ce = __ldg(RW.src + e * nr + row);
+      const double* src = gI + slot(ce);
+      wide_cp8(buf + e * 32, src);
+      const int le = ce >= 0 ? NI : NG;
+#pragma unroll
+      for (int d = 0; d < LM; ++d)
+        if (d < le) wide_cp8(buf + (11 + e * LM + d) * 32, src + (1 + d) * 32);
+    }
+    wide_cp8(buf + 6 * 32, gI + slot(cu));
+    wide_cp8(buf + 7 * 32, gI + slot(cv));
+    const double* bvp = A.bvT + (size_t)(B.row_off + row) * 3 * A.bpad + mu;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) wide_cp8(buf + (8 + i) * 32, bvp + (size_t)i * A.bpad);
+  };
+  if (r0 < r1) fetch(r0, pbuf);
+  wide_cp_commit();
   for (int row = r0; row < r1; ++row) {
+    const int par = (row - r0) & 1;
+    if (row + 1 < r1) fetch(row + 1, pbuf + (par ^ 1) * NSL * 32);
+    wide_cp_commit();
+    wide_cp_wait<1>();
+    const double* buf = pbuf + par * NSL * 32;
     const int ne = __ldg(RW.nent + row);
-    const int gu = __ldg(RW.src_gu + row), gv = __ldg(RW.src_gv + row);
+    const int cu = __ldg(RW.src_gu + row), cv = __ldg(RW.src_gv + row);
+    int c[MAXE];
+    double bxc[MAXE], byc[MAXE], cdc[MAXE], xe[MAXE];
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) {
+      c[e] = __ldg(RW.src + e * nr + row);
+      bxc[e] = __ldg(RW.bxc + e * nr + row);
+      byc[e] = __ldg(RW.byc + e * nr + row);
+      cdc[e] = __ldg(RW.cdc + e * nr + row);
+      xe[e] = buf[e * 32];
+    }
+    const double xu = buf[6 * 32], xv = buf[7 * 32];
+    const double bx = buf[8 * 32], by = buf[9 * 32], bc = buf[10 * 32];
     // xu (Bx x - bx) + xv (By x - by) + Cd x + c   (partition.py:434-441)
     double sx = 0.0, sy = 0.0, scd = 0.0;
 #pragma unroll
     for (int e = 0; e < MAXE; ++e) {
-      if (e < ne) {
-        const int c = __ldg(RW.src + e * nr + row);
-        const double bxc = __ldg(RW.bxc + e * nr + row), byc = __ldg(RW.byc + e * nr + row),
-                     cdc = __ldg(RW.cdc + e * nr + row);
-        const double xe = val(c);
-        if (bxc != 0.0) sx = __dadd_rn(sx, __dmul_rn(bxc, xe));
-        if (byc != 0.0) sy = __dadd_rn(sy, __dmul_rn(byc, xe));
-        if (cdc != 0.0) scd = __dadd_rn(scd, __dmul_rn(cdc, xe));
-      }
+      sx = __dadd_rn(sx, __dmul_rn(bxc[e], xe[e]));
+      sy = __dadd_rn(sy, __dmul_rn(byc[e], xe[e]));
+      scd = __dadd_rn(scd, __dmul_rn(cdc[e], xe[e]));
     }
-    const double xu = val(gu), xv = val(gv);
-    const double* bvp = A.bvT + (size_t)(B.row_off + row) * 3 * A.bpad + mu;
-    const double bx = bvp[0], by = bvp[A.bpad], bc = bvp[2 * (size_t)A.bpad];
     const double tx = sx - bx, ty = sy - by;
     const double r = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(xu, tx), __dmul_rn(xv, ty)), scd), bc);
     double R[W];
@@ -391,26 +494,21 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
     for (int d = 0; d < W; ++d) R[d] = 0.0;
 #pragma unroll
     for (int e = 0; e < MAXE; ++e) {
-      if (e < ne) {
-        const int c = __ldg(RW.src + e * nr + row);
-        const double bxc = __ldg(RW.bxc + e * nr + row), byc = __ldg(RW.byc + e * nr + row),
-                     cdc = __ldg(RW.cdc + e * nr + row);
-        // diag(Bx x - b) E_u + diag(x_u) Bx + diag(x_v) By + diag(By x - b) E_v + Cd
-        double j = 0.0;
-        if (c == gu) j = tx;
-        if (c == gv) j = __dadd_rn(j, ty);
-        if (bxc != 0.0) j = __dadd_rn(j, __dmul_rn(xu, bxc));
-        if (byc != 0.0) j = __dadd_rn(j, __dmul_rn(xv, byc));
-        if (cdc != 0.0) j = __dadd_rn(j, cdc);
-        if (c >= 0) {
-          const double* jr = gI + ((size_t)c * (NI + 1) + 1) * 32;
+      // diag(Bx x - b) E_u + diag(x_u) Bx + diag(x_v) By + diag(By x - b) E_v + Cd
+      double j = 0.0;
+      if (c[e] == cu) j = tx;
+      if (c[e] == cv) j = __dadd_rn(j, ty);
+      j = __dadd_rn(j, __dmul_rn(xu, bxc[e]));
+      j = __dadd_rn(j, __dmul_rn(xv, byc[e]));
+      j = __dadd_rn(j, cdc[e]);
+      if (e >= ne) j = 0.0;
+      const double* jr = buf + (11 + e * LM) * 32;
+      if (c[e] >= 0) {
 #pragma unroll
-          for (int d = 0; d < NI; ++d) R[d] = fma(j, jr[d * 32], R[d]);
-        } else {
-          const double* jr = gG + ((size_t)(-1 - c) * (NG + 1) + 1) * 32;
+        for (int d = 0; d < NI; ++d) R[d] = fma(j, jr[d * 32], R[d]);
+      } else {
 #pragma unroll
-          for (int d = 0; d < NG; ++d) R[NI + d] = fma(j, jr[d * 32], R[NI + d]);
-        }
+        for (int d = 0; d < NG; ++d) R[NI + d] = fma(j, jr[d * 32], R[NI + d]);
       }
     }
     // H += R^T R (rows I0 .. I1 of the upper triangle), R^T r, r^T r
@@ -428,6 +526,8 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
     }
   }
   constexpr int NR = NA + (H == 0 ? W + 1 : 0);     // values per lane
+  wide_cp_wait<0>();
+  __syncthreads();                                   // the reduction scratch aliases the row buffers
   if (warp > 0) {
     double* mine = red + (size_t)(warp - 1) * NR * 32 + lane;
 #pragma unroll
@@ -527,7 +627,7 @@ extern __shared__ __align__(16) double wide_red[];
 
 // CTA items: row chunks (x NH triangle parts) first, then the constraint chunks
 template <int NI, int NG, int NH>
-__global__ void __launch_bounds__(WROW_THREADS, 3) k_wide_rows(const __grid_constant__ WArgs A) {
+__global__ void __launch_bounds__(WROW_THREADS, 2) k_wide_rows(const __grid_constant__ WArgs A) {
   const int nact = A.ctl[0];
   if (nact <= 0) return;
   __shared__ int s_item;
@@ -618,6 +718,7 @@ struct Wide {
   int sms = 0;
   int total_rows = 0;
   size_t ring_smem = 0, red_smem = 0;
+  int dec_warps = WDEC_WARPS;
   ~Wide() {
     for (void* p : allocs) cudaFree(p);
   }
@@ -790,9 +891,15 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
   A.nC = nC; A.nCp = nCp; A.NI = ni; A.NG = ng;
   A.spec = getenv("DDNM_WIDE_NOSPEC") ? 0 : 1;
   w->total_rows = P.total_rows;
-  w->ring_smem = (size_t)WDEC_WARPS * WRING * 32 * sizeof(double2);
+  {
+    const int lpm = std::max(wide_lp(ni), wide_lp(ng));
+    const size_t per_warp = (size_t)wide_warp_doubles(lpm) * sizeof(double);
+    w->dec_warps = (int)std::min<size_t>(WDEC_WARPS, (size_t)(227 * 1024 - 1024) / per_warp);
+    w->ring_smem = per_warp * w->dec_warps;
+  }
   // reduction scratch of a row / constraint CTA: 3 warps x values per lane x 32 lanes
-  w->red_smem = (size_t)3 * std::max(A.NQ, 8 * (ng + 1)) * 32 * sizeof(double);
+  w->red_smem = std::max((size_t)3 * std::max(A.NQ, 8 * (ng + 1)) * 32,
+                         (size_t)4 * 2 * (11 + MAXE * std::max(ni, ng)) * 32) * sizeof(double);
   if (cudaFuncSetAttribute(K->dec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->ring_smem) != cudaSuccess ||
       cudaFuncSetAttribute(K->rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->red_smem) != cudaSuccess)
     return delete w, -1;
@@ -874,10 +981,10 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   if (!chk("k_wide_compact")) return -1;
   void* args[] = {&A};
   const int ctas = w->sms;
-  if (cudaLaunchKernel(w->K->dec, dim3(ctas), dim3(WDEC_WARPS * 32), args, w->ring_smem, s) != cudaSuccess)
+  if (cudaLaunchKernel(w->K->dec, dim3(ctas), dim3(w->dec_warps * 32), args, w->ring_smem, s) != cudaSuccess)
     return -1;
   if (!chk("k_wide_dec")) return -1;
-  if (cudaLaunchKernel(w->K->rows, dim3(ctas * 3), dim3(WROW_THREADS), args, w->red_smem, s) != cudaSuccess)
+  if (cudaLaunchKernel(w->K->rows, dim3(ctas * 2), dim3(WROW_THREADS), args, w->red_smem, s) != cudaSuccess)
     return -1;
   if (!chk("k_wide_rows")) return -1;
   // lanes of the round are only known on the device: the grid covers the
