@@ -122,9 +122,11 @@ struct DdBuffers {
   ddnm::WideBuffers wide;
   double* pk = nullptr;
   size_t pk_len = 0;
+  double* kkt_fb = nullptr;         // dense-fallback KKT workspace per mu (wide solve)
   void release() {
     wide.release();
     if (pk) cudaFree(pk);
+    if (kkt_fb) cudaFree(kkt_fb);
     for (void* p : {(void*)st, (void*)vec, (void*)ecur, (void*)gbv, (void*)gJ, (void*)gJg,
                     (void*)kkt_g, (void*)eb_g, (void*)trials, (void*)active})
       if (p) cudaFree(p);
@@ -164,6 +166,12 @@ struct ddnm_ctx {
   int n_units = 0;            // evaluation units (0: blocks evaluated whole)
   std::vector<DdBuffers> dd_pool;   // buffers of finished sharded solves, for reuse
   ddnm::Wide* wide = nullptr;       // batch-wide evaluation program (null: not eligible)
+  // step kernel of the batch-wide solve: shared scratch sized for the
+  // block-structured KKT only (the dense fallback gets a global workspace),
+  // two CTAs per SM when the specialisation has k_dd_step2
+  int step_scr = 0;                 // doubles per slot (0: use the planner's plan)
+  size_t step_smem = 0;
+  size_t kkt_fb_stride = 0;
   std::string wide_why;             // why not
   DecodeJob* d_jobs = nullptr;
   int state_len = 0, dec_max_hidden = 0, dec_mu_tile = 0;
@@ -1209,6 +1217,15 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
   P.sm_scr = P.sm_eb + (kern_ebg ? 0 : P.G * 2 * P.eb_size);
   c->ebg = kern_ebg;
   c->smem = footprint(P.G, kern_level, kern->kkt_global, kern_ebg);
+  if (!kern->kkt_global && !kern_ebg) {
+    const int block_need = P.nb * (W + P.n_C) * (W + P.n_C + 1) + P.nb * W + P.n_C * (P.n_C + 1) +
+                           P.n_C + P.nb * P.n_C + 4 * P.nK;
+    c->step_scr = (std::max(std::max(block_need, ls_need), rbf_need) + 1) & ~1;
+    c->step_smem = ((size_t)state_d * P.G + (size_t)P.G * (8 * P.nK + 2 * P.eb_size + c->step_scr)) * 8;
+    c->kkt_fb_stride = (size_t)((P.nK * (P.nK + 1) + 6 * P.nK + 31) & ~31);
+    if (kern->dd_step2 && raise_smem_limit(kern->dd_step2, c->step_smem) != cudaSuccess)
+      return bail(fail(DDNM_ECUDA, "cannot reserve dynamic shared memory"));
+  }
   if (raise_smem_limit(kern->solve, c->smem) != cudaSuccess ||
       raise_smem_limit(kern->eval, c->smem) != cudaSuccess ||
       raise_smem_limit(kern->dd_eval, c->smem) != cudaSuccess ||
@@ -1673,6 +1690,8 @@ struct ddnm_dd {
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
   bool wide = false;              // evaluations by the batch-wide kernels (ddnm_wide.h)
   size_t wide_pk_cap = 0;         // doubles in the caller's packet buffer when known
+  const void* step_kern = nullptr; // step kernel / shared memory of the wide solve (null: the context's)
+  size_t step_smem = 0;
 };
 
 namespace {
@@ -1688,8 +1707,10 @@ int dd_run(ddnm_dd* d, const void* kern, cudaStream_t s, int32_t* n_active, int 
   CUDA_TRY(cudaMemsetAsync(d->buf.active, 0, sizeof(int), s));
   void* args[] = {&d->P};
   if (ctas == 0) ctas = d->ctas;
+  size_t smem = c->smem;
+  if (kern == c->K.dd_step && d->step_kern && !d->P.dd_init) { kern = d->step_kern; smem = d->step_smem; }
   if (ctas > 0)
-    CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(c->threads), args, c->smem, s));
+    CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(c->threads), args, smem, s));
   if (getenv("DDNM_WIDE_SYNC")) {
     const cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess)
@@ -1841,7 +1862,11 @@ int ddnm_dd_eval(ddnm_dd* d, double* d_packets, int64_t pk_stride, void* stream)
  * kernels (ddnm_wide.h): same packets to rounding, one lane per mu. */
 int ddnm_dd_set_wide(ddnm_dd* d, int32_t on) {
   if (!d) return fail(DDNM_EINVAL, "null argument");
-  if (!on) { d->wide = false; d->P.dd_vbase = nullptr; d->P.dd_kof = nullptr; return 0; }
+  if (!on) {
+    d->wide = false; d->P.dd_vbase = nullptr; d->P.dd_kof = nullptr;
+    d->P.scr_size = d->c->P.scr_size; d->P.kkt_fb = nullptr; d->step_kern = nullptr;
+    return 0;
+  }
   ddnm_ctx* c = d->c;
   if (!c->wide) return fail(DDNM_EUNSUPPORTED, "instance not eligible for the wide evaluation: " + c->wide_why);
   if (d->P.b_lo != 0 || d->P.b_hi != d->P.nb)
@@ -1853,6 +1878,21 @@ int ddnm_dd_set_wide(ddnm_dd* d, int32_t on) {
     return fail(DDNM_ECUDA, "wide boundary-value launch failed");
   d->P.dd_vbase = d->buf.wide.vbase;
   d->P.dd_kof = d->buf.wide.kof;
+  // the step kernel runs alone: KKT-sized shared scratch, dense fallback in a
+  // global workspace, two CTAs per SM when compiled (DDNM_STEP2=0: the plain one)
+  if (c->step_scr > 0 && !getenv("DDNM_STEP_FULL")) {
+    DdBuffers& bf = d->buf;
+    if (!bf.kkt_fb &&
+        cudaMalloc(&bf.kkt_fb, (size_t)(bf.cap + 2 * c->P.G) * c->kkt_fb_stride * sizeof(double)) != cudaSuccess)
+      return fail(DDNM_ENOMEM, "cannot allocate the KKT fallback workspace");
+    d->P.scr_size = c->step_scr;
+    d->P.kkt_fb = bf.kkt_fb;
+    d->P.kkt_fb_stride = (long long)c->kkt_fb_stride;
+    const char* e2 = getenv("DDNM_STEP2");
+    const bool two = c->K.dd_step2 && !(e2 && atoi(e2) == 0);
+    d->step_kern = two ? c->K.dd_step2 : c->K.dd_step;
+    d->step_smem = c->step_smem;
+  }
   d->wide = true;
   return 0;
 }

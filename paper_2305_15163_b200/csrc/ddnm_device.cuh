@@ -233,6 +233,9 @@ struct Params {
   // packet per mu per rank, the subdomain-sharded layout above)
   const int* dd_vbase;
   const int* dd_kof;
+  // dense-fallback KKT workspace per global slot (null: the slot's own scratch)
+  double* kkt_fb;
+  long long kkt_fb_stride;
   // peer-memory all-gather fused into k_dd_eval: when dd_npeers > 0 the
   // packets go straight to every rank's gathered buffer (NVLink stores)
   double* dd_peers[MAXB];

@@ -10,5 +10,6 @@ struct KernelEntry {
   const void* eval;
   const void* dd_eval;   // subdomain-sharded round kernels
   const void* dd_step;
+  const void* dd_step2 = nullptr;   // two CTAs per SM (batch-wide solve), or null
 };
 }  // namespace ddnm

@@ -1861,7 +1861,9 @@ __device__ void kkt_stage(const View& V, unsigned kmask, const int* ebi, int* kr
   // slot at a time with the whole CTA
   for (int ss = 0; ss < G; ++ss) {
     if (!((kmask >> ss) & 1u) || kflag[ss]) continue;   // uniform (shared flags)
-    double* work = kws<KG>(V, ss);
+    // (kkt_fb: a per-slot global workspace, when the shared scratch is sized
+    // for the block-structured path only)
+    double* work = P.kkt_fb ? P.kkt_fb + (size_t)(V.gslot0 + ss) * P.kkt_fb_stride : kws<KG>(V, ss);
     double* sol = work + (size_t)P.nK * (P.nK + 1) + 4 * P.nK;
     const int r = cta_kkt<NI, NG>(P, V.eb(ss, ebi[ss]), work, sol);
     if (warp == 0) {
@@ -2360,7 +2362,7 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_eval(const __grid_co
 }
 
 template <int G, int NI, int NG, bool KG>
-__global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_constant__ Params P) {
+__device__ __forceinline__ void dd_step_body(const Params& P) {
   View V(P, ddnm_smem);
   SlotState* st = V.st();
   const int tid = threadIdx.x, T = blockDim.x, warp = tid >> 5;
@@ -2485,6 +2487,20 @@ __global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_co
     if (st[tid].phase != PH_DONE) atomicAdd(P.dd_active, 1);
   }
   if (tid == 0) atomicAdd(P.counters + 1, s_kkts);
+}
+
+template <int G, int NI, int NG, bool KG>
+__global__ void __launch_bounds__(DDNM_MAX_THREADS, 1) k_dd_step(const __grid_constant__ Params P) {
+  dd_step_body<G, NI, NG, KG>(P);
+}
+
+// The same step with two CTAs per SM (64 registers per thread): for the
+// batch-wide solve, where the step kernel runs alone with a KKT-sized
+// shared-memory plan (ddnm_dd_set_wide) and is bound by the latency of the
+// per-slot factorisations, not by registers or shared memory.
+template <int G, int NI, int NG, bool KG>
+__global__ void __launch_bounds__(DDNM_MAX_THREADS, 2) k_dd_step2(const __grid_constant__ Params P) {
+  dd_step_body<G, NI, NG, KG>(P);
 }
 
 }  // namespace ddnm

@@ -21,6 +21,7 @@ void register_6_4(std::vector<KernelEntry>& t) {
   t.push_back(KernelEntry{6, 4, 4, false, (const void*)&k_solve<4, 6, 4, false>,
                           (const void*)&k_eval<4, 6, 4, false>,
                           (const void*)&k_dd_eval<4, 6, 4>,
-                          (const void*)&k_dd_step<4, 6, 4, false>});
+                          (const void*)&k_dd_step<4, 6, 4, false>,
+                          (const void*)&k_dd_step2<4, 6, 4, false>});
 }
 }  // namespace ddnm
