@@ -226,13 +226,17 @@ def run_gpu(args):
     torch.cuda.set_stream(stream)
     mu_d = mu_d.clone()                        # allocated on the bench stream
     torch.cuda.synchronize()
+    # engine: "auto" = the library's default (the batch-wide kernels when the
+    # instance is eligible: one lane per mu, rounds of evaluation + SQP-step
+    # kernels; else the persistent slot kernel)
+    ctx.set_engine(args.engine)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    times, evals, kkts = [], 0, 0
+    times, evals, kkts, launches, rounds = [], 0, 0, 0, 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(float(len(times)))           # L2 flush between timed steps
@@ -246,6 +250,9 @@ def run_gpu(args):
             ev, kk = ctx.counters()
             evals += ev
             kkts += kk
+            rd, ln = ctx.rounds()
+            rounds += rd
+            launches += ln
     torch.cuda.synchronize()
     total_ms = float(np.sum(times))
     if dist:
@@ -255,6 +262,37 @@ def run_gpu(args):
         dist.barrier()
     ms_per_step = total_ms / args.steps
     value = BATCH * args.steps / (total_ms / 1e3)
+
+    # the persistent slot kernel on the same batch, beside the headline
+    # (reported, not the headline, when the default engine is the wide one)
+    slot_engine = None
+    if rounds > 0:
+        ctx.set_engine("slots")
+        outs_keep = {k: v.clone() for k, v in outs.items()}
+        step()
+        st = []
+        for _ in range(min(args.steps, 5)):
+            flush.fill_(2.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            st.append(e0.elapsed_time(e1))
+        sms = float(np.median(st))
+        if dist:
+            t = torch.tensor([sms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sms = float(t.item())
+        same = int((outs["n_iter"] == outs_keep["n_iter"]).sum().item())
+        slot_engine = {"kernel": "k_solve (persistent: one CTA slot per mu, one launch)",
+                       "ms_per_step": sms, "value": BATCH / (sms / 1e3), "unit": UNIT,
+                       "n_iter_equal_to_headline_engine": same, "of": B}
+        for k, v in outs_keep.items():
+            outs[k].copy_(v)
+        ctx.set_engine(args.engine)
+        torch.cuda.synchronize()
 
     # parity of the timed batch (last timed step) against CPU goldens of its
     # first mu (tests/golden/bench_c0_parity.npz: oracle and reference
@@ -312,7 +350,7 @@ def run_gpu(args):
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        res = P.solve_rom_batch(inst, mu_h, cfg, slots=args.slots)
+        res = P.solve_rom_batch(inst, mu_h, cfg, slots=args.slots, engine=args.engine)
         e2e_vals.append(time.perf_counter() - t0)
     e2e_t = float(np.mean(e2e_vals[1:])) if len(e2e_vals) > 1 else e2e_vals[0]
     if dist:
@@ -348,19 +386,35 @@ def run_gpu(args):
     kkts_per_step = kkts / args.steps
     flops_per_step = evals_per_step * fl["per_eval"] + kkts_per_step * fl["kkt"]
     peak, peak_src = fp64_peak()
-    traffic = None
+    achieved = flops_per_step / (ms_per_step / 1e3) / 1e12
+    wide = rounds > 0
+    prof_file = "r2w_ncu_summary.json" if wide else "r2_ncu_summary.json"
+    traffic, kern_prof = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "r2_ncu_summary.json")) as f:
-            traffic = json.load(f)["traffic_bytes_per_launch"]   # ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", prof_file)) as f:
+            pj = json.load(f)
+        traffic = pj["traffic_bytes_per_launch"]   # ncu --set full capture of the dominant kernel
+        kern_prof = pj.get("kernels")
     except Exception:
         pass
-    achieved = flops_per_step / (ms_per_step / 1e3) / 1e12
+    if wide:
+        kernel = ("round loop of the batch-wide engine: k_wide_dec (hidden ring + banded decoder "
+                  "sweep, the dominant kernel), k_wide_rows (stencil, chain rule, Gram, constraint), "
+                  "k_dd_step2 (Armijo / KKT), k_wide_compact, k_wide_pack")
+        tsrc = (f"dram__bytes_read+write of one full-batch k_wide_dec launch, profiles/{prof_file} "
+                "(the g / Jacobian rows of 4096 lanes written once)")
+    else:
+        kernel = "k_solve (persistent SQP megakernel)"
+        tsrc = (f"dram__bytes_read+write per launch, profiles/{prof_file} (1.25 MB weights + one "
+                "write-back of the 16.6 MB per-slot L2 Jacobian-row scratch)")
+    # achieved / frac: ALL algorithmic flops of the step (every kernel's) over
+    # the whole step's device time; `kernels` = each kernel's share of the
+    # step's device time and its own FP64-pipe utilisation (ncu, profiles/)
     roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "traffic_source": "dram__bytes_read+write per launch, profiles/r2_ncu_summary.json "
-                              "(this build; 1.25 MB weights + one write-back of the 16.6 MB "
-                              "per-slot L2 Jacobian-row scratch)",
-            "kernel": "k_solve (persistent SQP megakernel)",
+            "traffic_source": tsrc,
+            "kernel": kernel,
+            "kernels": kern_prof,
             "peak_source": peak_src,
             "algorithmic_flops_per_step": flops_per_step,
             "exp_per_step": evals_per_step * fl["exp_per_eval"],
@@ -379,12 +433,15 @@ def run_gpu(args):
         "run": {"batch_per_gpu": B,
                    "parallelism": f"mu-shard x{world} (contiguous shards of the fixed batch)",
                    "l2": "flushed (256 MB write) between timed steps",
+                   "engine": "wide (one lane per mu)" if wide else "slots (persistent kernel)",
+                   "sqp_rounds_per_step": rounds / args.steps,
                    "slots_per_cta": info.slots_per_cta, "ctas": info.ctas,
                    "mean_n_iter": float(n_iter.mean()), "status_counts": np.bincount(status, minlength=4).tolist()},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": launches,
+        "slot_engine": slot_engine,
         "clocks": clk.summary(),
         "parity": parity,
         "weak_scaling": weak,
@@ -520,22 +577,29 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
             N.check(N.lib().ddnm_solve_batch_device(ctx.h, B, C.c_void_p(mu.data_ptr()), None,
                                                     None, C.byref(cs), C.byref(so),
                                                     C.c_void_p(stream.cuda_stream)))
-        launch()
-        times = []
-        for _ in range(reps):
-            flush.fill_(3.0)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+        def timed(engine):
+            ctx.set_engine(engine)
             launch()
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
-        ms = float(np.median(times))
-        if dist:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            times = []
+            for _ in range(reps):
+                flush.fill_(3.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                launch()
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+            ms = float(np.median(times))
+            if dist:
+                t = torch.tensor([ms], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            return ms
+        # the slot kernel beside the default engine when that is the wide one
+        slots_ms = timed("slots") if ctx.info.wide else None
+        ms = timed("auto")
+        rounds, _ = ctx.rounds()
         from paper_2305_15163_b200.workmodel import eval_flops
         evals, _ = ctx.counters()            # block evaluations of the last launch
         fl = eval_flops(inst.arrays, inst.meta)
@@ -550,6 +614,8 @@ def other_configs_bench(P, N, C, cfg_struct, torch, dist, dev, stream, flush, re
                     "solves_per_s": Bt / (ms / 1e3),
                     "ms_per_batch": ms, "mean_n_iter": float(it.float().mean().item()),
                     "status_counts": torch.bincount(st.long(), minlength=4).tolist(),
+                    "engine": "wide" if rounds > 0 else "slots", "sqp_rounds": rounds,
+                    "slot_engine_ms_per_batch": slots_ms,
                     "slots_per_cta": ctx.info.slots_per_cta, "eval_units": ctx.info.eval_units,
                     "eval_tflops": round(eval_tf, 3), "eval_frac_of_fp64_peak": round(eval_tf / peak, 4)}
     return out
@@ -625,6 +691,8 @@ def main():
                     help="skip the extra measurements (subdomain-sharded dd16, other configs)")
     ap.add_argument("--slots", type=int, default=0, help="mu slots per CTA (0 = largest that fits)")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling extra")
+    ap.add_argument("--engine", default="auto", choices=["auto", "slots", "wide"],
+                    help="solve engine of the headline (auto: the library's default)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: launch the ranks ourselves (the driver may also

@@ -158,6 +158,8 @@ typedef struct {
                                 are evaluated as chunks of their sampled rows plus
                                 chunks of interface outputs; DDNM_UNIT_ROWS=<rows>
                                 forces the split (tests) */
+  int32_t wide;              /* 1: the batch-wide engine (one lane per mu, csrc/ddnm_wide.h)
+                                is available for this instance */
 } ddnm_info;
 
 /* Per-mu solve results; every pointer may be NULL except x and lam. */
@@ -244,6 +246,25 @@ int ddnm_eval_batch(ddnm_ctx* ctx, int32_t B, const double* mu,
 /* Device work counters of the last solve (for the roofline): total block
  * evaluations and KKT solves executed. */
 int ddnm_last_counters(const ddnm_ctx* ctx, int64_t* evals, int64_t* kkts);
+
+/* Which engine ddnm_solve_batch[_device] runs: the persistent kernel (one CTA
+ * slot per mu, the whole SQP loop in one launch) or the batch-wide engine (one
+ * lane per mu, rounds of evaluation + SQP-step kernels looped inside the
+ * library; available when ddnm_info.wide: autoencoder maps, WFPC coupling,
+ * collocation HR, banded decoders).  AUTO (default): wide when available
+ * (environment: DDNM_WIDE=0/1 forces, DDNM_WIDE_MIN_B=<batch> sets the
+ * smallest batch that goes wide).  Both engines take the same decisions on the
+ * same evaluations (sqp.py:230-299); their evaluations differ by rounding. */
+#define DDNM_ENGINE_AUTO 0
+#define DDNM_ENGINE_SLOTS 1
+#define DDNM_ENGINE_WIDE 2
+int ddnm_ctx_set_engine(ddnm_ctx* ctx, int32_t engine);
+/* SQP rounds and kernel launches of the last batched solve (slots: 0 and 1). */
+int ddnm_last_rounds(const ddnm_ctx* ctx, int64_t* rounds, int64_t* launches);
+/* Evaluations (lanes) the wide engine launched in the last solve, including
+ * speculative candidates that were not consumed (ddnm_last_counters counts
+ * the consumed ones). */
+int ddnm_last_lanes(const ddnm_ctx* ctx, int64_t* lanes);
 
 /* Device-side phase profile of the last solve when the environment variable
  * DDNM_PROF is set (SM clock cycles summed over CTAs, thread 0 of each CTA):

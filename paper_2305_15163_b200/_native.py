@@ -74,7 +74,7 @@ class Info(C.Structure):
         "n_primal", "n_mult", "n_blocks", "total_rows", "total_out_rows", "total_out_R",
         "total_int_out", "total_gam_out",
         "total_R", "total_cjac", "total_int_J", "total_gam_J", "slots_per_cta", "ctas",
-        "smem_bytes", "device", "eval_units")]
+        "smem_bytes", "device", "eval_units", "wide")]
 
 
 class SolveOut(C.Structure):
@@ -136,6 +136,9 @@ def lib():
                                _ip]
     L.ddnm_dd_end.argtypes = [C.c_void_p]
     L.ddnm_dd_set_wide.argtypes = [C.c_void_p, C.c_int32]
+    L.ddnm_ctx_set_engine.argtypes = [C.c_void_p, C.c_int32]
+    L.ddnm_last_rounds.argtypes = [C.c_void_p, _lp, _lp]
+    L.ddnm_last_lanes.argtypes = [C.c_void_p, _lp]
     L.ddnm_plan_units.argtypes = [C.POINTER(Artifacts), _ip, _ip, _ip]
     L.ddnm_dd_trial_len.argtypes = [C.c_void_p, _lp]
     L.ddnm_dd_set_trials.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
@@ -173,7 +176,7 @@ EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_
             "ddnm_binio_write", "ddnm_ctx_create_binio", "ddnm_dd_eval_p2p",
             "ddnm_ipc_get_handle", "ddnm_ipc_open_handle", "ddnm_ipc_close_handle",
             "ddnm_dev_alloc", "ddnm_dev_free", "ddnm_dd_trial_len", "ddnm_dd_set_trials",
-            "ddnm_dd_set_wide",
+            "ddnm_dd_set_wide", "ddnm_ctx_set_engine", "ddnm_last_rounds", "ddnm_last_lanes",
             "ddnm_plan_units")
 
 

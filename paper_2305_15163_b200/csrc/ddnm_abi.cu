@@ -169,6 +169,9 @@ struct ddnm_ctx {
   // step kernel of the batch-wide solve: shared scratch sized for the
   // block-structured KKT only (the dense fallback gets a global workspace),
   // two CTAs per SM when the specialisation has k_dd_step2
+  int engine = 0;                   // DDNM_ENGINE_*: 0 auto, 1 slots (persistent kernel), 2 wide
+  long long last_rounds = 0, last_launches = 0;   // of the last batched solve
+  long long last_lanes = 0;         // evaluations launched by the wide engine (incl. unused candidates)
   int step_scr = 0;                 // doubles per slot (0: use the planner's plan)
   size_t step_smem = 0;
   size_t kkt_fb_stride = 0;
@@ -1318,6 +1321,7 @@ int ddnm_ctx_info(const ddnm_ctx* c, ddnm_info* i) {
   i->smem_bytes = (int32_t)c->smem;
   i->device = c->device;
   i->eval_units = c->n_units;
+  i->wide = c->wide ? 1 : 0;
   return 0;
 }
 
@@ -1363,10 +1367,11 @@ static int solve_wide(ddnm_ctx* c, int32_t B, const double* d_mu, const double* 
 // see wide_min_batch) when the instance is eligible.
 static int wide_min_batch() {
   if (const char* e = getenv("DDNM_WIDE_MIN_B")) return atoi(e);
-  return 1 << 30;
+  return 1;
 }
 static bool use_wide(const ddnm_ctx* c, int B) {
-  if (!c->wide) return false;
+  if (!c->wide || c->engine == DDNM_ENGINE_SLOTS) return false;
+  if (c->engine == DDNM_ENGINE_WIDE) return true;
   if (const char* e = getenv("DDNM_WIDE")) return atoi(e) != 0;
   return B >= wide_min_batch();
 }
@@ -1376,6 +1381,8 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
                             void* stream) {
   if (!c || !cfg || !o || !d_mu || !o->x || !o->lam) return fail(DDNM_EINVAL, "null argument");
   if (B < 0) return fail(DDNM_EINVAL, "negative batch");
+  if (c->engine == DDNM_ENGINE_WIDE && !c->wide)
+    return fail(DDNM_EUNSUPPORTED, "instance not eligible for the wide engine: " + c->wide_why);
   if (B > 0 && use_wide(c, B)) {
     CUDA_TRY(cudaSetDevice(c->device));
     return solve_wide(c, B, d_mu, d_x0, d_lam0, cfg, o, stream ? (cudaStream_t)stream : c->stream);
@@ -1425,6 +1432,31 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(unsigned long long), s));
   void* args[] = {&P};
   CUDA_TRY(cudaLaunchKernel(c->K.solve, dim3(ctas), dim3(c->threads), args, c->smem, s));
+  c->last_rounds = 0;
+  c->last_launches = 1;
+  c->last_lanes = 0;
+  return 0;
+}
+
+int ddnm_ctx_set_engine(ddnm_ctx* c, int32_t engine) {
+  if (!c) return fail(DDNM_EINVAL, "null argument");
+  if (engine < DDNM_ENGINE_AUTO || engine > DDNM_ENGINE_WIDE) return fail(DDNM_EINVAL, "unknown engine");
+  if (engine == DDNM_ENGINE_WIDE && !c->wide)
+    return fail(DDNM_EUNSUPPORTED, "instance not eligible for the wide engine: " + c->wide_why);
+  c->engine = engine;
+  return 0;
+}
+
+int ddnm_last_rounds(const ddnm_ctx* c, int64_t* rounds, int64_t* launches) {
+  if (!c) return fail(DDNM_EINVAL, "null argument");
+  if (rounds) *rounds = c->last_rounds;
+  if (launches) *launches = c->last_launches;
+  return 0;
+}
+
+int ddnm_last_lanes(const ddnm_ctx* c, int64_t* lanes) {
+  if (!c || !lanes) return fail(DDNM_EINVAL, "null argument");
+  *lanes = c->last_lanes;
   return 0;
 }
 
@@ -2059,14 +2091,23 @@ static int solve_wide(ddnm_ctx* c, int32_t B, const double* d_mu, const double* 
   int check = 4;
   if (const char* e = getenv("DDNM_DD_CHECK")) check = std::max(1, atoi(e));
   int32_t active = B;
+  c->last_rounds = 0;
+  c->last_launches = 2;               // init step, boundary values
   for (long long round = 0;; ++round) {
     if ((rc = ddnm_dd_eval(d, bf.pk, stride, s))) return bail(rc);
     const bool count = round % check == check - 1;
     if ((rc = ddnm_dd_step(d, bf.pk, 1, bounds, stride, s, count ? &active : nullptr))) return bail(rc);
+    c->last_rounds += 1;
+    c->last_launches += 5;            // compact, decoder, rows, pack, step
     if (count && active == 0) break;
-    if (count) bf.wide.lane_bound = std::min<long long>(bf.wide.vpad, (long long)active * 8);
+    if (count) bf.wide.lane_bound = std::min<long long>(bf.wide.vpad, (long long)active * 16);
   }
   bf.wide.lane_bound = 0;
+  unsigned long long lanes = 0;
+  if (cudaMemcpyAsync(&lanes, bf.wide.lanes_total, sizeof lanes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return bail(fail(DDNM_ECUDA, "cannot read the lane count"));
+  c->last_lanes = (long long)lanes;
   return ddnm_dd_end(d);
 }
 

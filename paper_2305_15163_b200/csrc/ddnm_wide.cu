@@ -12,6 +12,13 @@ namespace ddnm {
 // --------------------------------------------------------------------------
 // device tables
 
+#ifndef DDNM_WIDE_HU
+#define DDNM_WIDE_HU 2             // hidden units computed together (unroll of the activation chain)
+#endif
+#ifndef DDNM_WIDE_SU
+#define DDNM_WIDE_SU 2             // sweep steps unrolled
+#endif
+constexpr int WIDE_HU = DDNM_WIDE_HU, WIDE_SU = DDNM_WIDE_SU;
 constexpr int WRING = 32;          // hidden units a warp keeps in its ring
 constexpr int WDEC_WARPS = 12;     // warps per decoder CTA (16 KB ring each)
 constexpr int WROW_THREADS = 128;
@@ -56,7 +63,8 @@ struct WRowChunk { int blk, r0, r1, pslot; };
 struct WConChunk { int blk, j0, j1, cslot; };
 
 constexpr int WFINE_TILES = 32;   // fine items when at most this many lane tiles run
-constexpr int WSPEC_MAX = 8;      // most step lengths of one mu evaluated in one round
+constexpr int WSPEC_MAX = 16;     // most step lengths of one mu evaluated in one round
+constexpr int WSPEC_BOOST_LANES = 384;   // boost the candidates while the round stays below this
 
 struct WArgs {
   const WBlockDev* blk;
@@ -72,6 +80,7 @@ struct WArgs {
   int* vbase;            // [B] first lane of each running mu
   int* kof;              // [B] its candidates this round
   int* ctl;              // [0] lanes, [1] decoder items, [2] row / constraint items
+  unsigned long long* lanes_total;   // evaluations launched since wide_begin (incl. unused candidates)
   const double* trial;
   int rec;
   const SlotState* st;   // [B] SQP state (phase, rejected trials, step length)
@@ -104,26 +113,26 @@ __device__ __forceinline__ int wide_mode(int nlane) { return nlane <= WFINE_TILE
 // (1, 2, 4, 4, 8, ...), so at most about as many evaluations are wasted as were
 // needed; K = 1 for everybody when the lanes would not fit.
 
-__device__ __forceinline__ int wide_kspec(const WArgs& A, const SlotState& S) {
+__device__ __forceinline__ int wide_kspec(const WArgs& A, const SlotState& S, bool boost) {
   if (!A.spec || S.phase != PH_TRIAL || S.n_trials == 0) return 1;
   const int left = A.max_halvings + 1 - S.n_trials;      // trials the reference may still run
-  const int k = S.n_trials == 1 ? 2 : (S.n_trials < 4 ? 4 : WSPEC_MAX);
+  int k = S.n_trials == 1 ? 2 : (S.n_trials < 4 ? 4 : 8);
+  // few lanes: a round costs its latency, not its lanes, so candidates are free
+  if (boost) k = WSPEC_MAX;
   return max(1, min(k, left));
 }
 
 __global__ void __launch_bounds__(1024) k_wide_compact(const WArgs A) {
   __shared__ int s_cnt[1024];
-  __shared__ int s_k1;
   const int tid = threadIdx.x, T = blockDim.x;
   const int per = (A.B + T - 1) / T;
   const int lo = min(A.B, tid * per), hi = min(A.B, lo + per);
-  if (tid == 0) s_k1 = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    __syncthreads();
-    const bool k1 = s_k1 != 0;
+  // policy 2: boosted candidates (few lanes), 1: by rejections seen, 0: one each
+  for (int policy = 2; policy >= 0; --policy) {
     int n = 0;
     for (int mu = lo; mu < hi; ++mu)
-      if (A.trial[(size_t)mu * A.rec] != 0.0) n += k1 ? 1 : wide_kspec(A, A.st[mu]);
+      if (A.trial[(size_t)mu * A.rec] != 0.0) n += policy ? wide_kspec(A, A.st[mu], policy == 2) : 1;
+    __syncthreads();                  // the previous policy's totals have been read
     s_cnt[tid] = n;
     __syncthreads();
     // inclusive scan (Hillis-Steele on 1024 counts)
@@ -134,15 +143,11 @@ __global__ void __launch_bounds__(1024) k_wide_compact(const WArgs A) {
       __syncthreads();
     }
     const int total = s_cnt[T - 1];
-    if (total > A.vpad && !k1) {        // does not fit: one candidate each
-      __syncthreads();
-      if (tid == 0) s_k1 = 1;
-      continue;
-    }
+    if (policy > 0 && total > (policy == 2 ? min(WSPEC_BOOST_LANES, A.vpad) : A.vpad)) continue;
     int at = s_cnt[tid] - n;
     for (int mu = lo; mu < hi; ++mu)
       if (A.trial[(size_t)mu * A.rec] != 0.0) {
-        const int k = k1 ? 1 : wide_kspec(A, A.st[mu]);
+        const int k = policy ? wide_kspec(A, A.st[mu], policy == 2) : 1;
         A.vbase[mu] = at;
         A.kof[mu] = k;
         for (int j = 0; j < k; ++j) A.act[at++] = mu | (j << 24);
@@ -150,6 +155,7 @@ __global__ void __launch_bounds__(1024) k_wide_compact(const WArgs A) {
     if (tid == T - 1) {
       A.ctl[0] = total;
       A.ctl[1] = 0; A.ctl[2] = 0; A.ctl[3] = 0;
+      *A.lanes_total += (unsigned long long)total;
     }
     break;
   }
@@ -234,7 +240,7 @@ __device__ __forceinline__ void wide_sweep(const double2* ring, const double* st
   constexpr int T = wide_tile_outputs(L), LP = wide_lp(L);
   const double2* wv = reinterpret_cast<const double2*>(stg);
   const double2* w1 = reinterpret_cast<const double2*>(stg + 128);
-#pragma unroll 2
+#pragma unroll WIDE_SU
   for (int k = klo; k < khi; ++k) {
     const double2 sd = ring[(k & (WRING - 1)) * 32];
     double w[LP], v[T];
@@ -310,7 +316,7 @@ __device__ __forceinline__ void wide_dec_part(const WArgs& A, const WDecDev& D, 
     const int klo = m0.klo, khi = m0.khi, cnt = m0.cnt;
     // hidden units of the window not in the ring yet: z = b1 + W1 x in latent
     // order (hyper.py:184-188), activation and derivative (autoencoder.py:31-45)
-#pragma unroll 2
+#pragma unroll WIDE_HU
     for (int k = max(next_k, klo); k < khi; ++k) {
       const double2* wr = reinterpret_cast<const double2*>(stg + 128) + (k - klo) * (LP / 2);
       double w[LP];
@@ -726,7 +732,7 @@ struct Wide {
 
 void WideBuffers::release() {
   for (void* p : {(void*)gj, (void*)part, (void*)conpart, (void*)bvT, (void*)act, (void*)ctl,
-                  (void*)vbase, (void*)kof})
+                  (void*)vbase, (void*)kof, (void*)lanes_total})
     if (p) cudaFree(p);
   *this = WideBuffers{};
 }
@@ -924,6 +930,7 @@ int wide_alloc(const Wide* w, int B, WideBuffers* b, std::string& err) {
       cudaMalloc(&b->act, (size_t)vpad * sizeof(int)) != cudaSuccess ||
       cudaMalloc(&b->vbase, (size_t)bpad * sizeof(int)) != cudaSuccess ||
       cudaMalloc(&b->kof, (size_t)bpad * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&b->lanes_total, sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&b->ctl, 4 * sizeof(int)) != cudaSuccess) {
     b->release();
     cudaGetLastError();
@@ -938,6 +945,7 @@ int wide_alloc(const Wide* w, int B, WideBuffers* b, std::string& err) {
 
 int wide_begin(const Wide* w, const Params& P, WideBuffers& b, cudaStream_t s) {
   (void)w;
+  if (cudaMemsetAsync(b.lanes_total, 0, sizeof(unsigned long long), s) != cudaSuccess) return -1;
   if (P.total_rows == 0) return 0;
   dim3 grid((P.B + 127) / 128, P.total_rows);
   k_wide_bv<<<grid, 128, 0, s>>>(P, b.bvT, b.bpad);
@@ -954,6 +962,7 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   A.vbase = b.vbase;
   A.kof = b.kof;
   A.ctl = b.ctl;
+  A.lanes_total = b.lanes_total;
   A.trial = P.dd_trial;
   A.rec = P.dd_rec;
   A.st = P.dd_st;

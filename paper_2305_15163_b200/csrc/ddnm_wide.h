@@ -42,6 +42,7 @@ struct WideBuffers {
   int* vbase = nullptr;       // [bpad] first lane of a running mu
   int* kof = nullptr;         // [bpad] its candidates this round
   int* ctl = nullptr;         // [0] lanes, [1..3] work counters
+  unsigned long long* lanes_total = nullptr;   // evaluations launched this solve
   void release();
 };
 

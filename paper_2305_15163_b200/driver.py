@@ -280,6 +280,28 @@ class _Context:
         N.check(N.lib().ddnm_last_counters(self.h, C.byref(e), C.byref(k)))
         return e.value, k.value
 
+    def set_engine(self, engine: str = "auto") -> None:
+        """Engine of the batched solve: ``"slots"`` (persistent kernel, one CTA
+        slot per mu), ``"wide"`` (one lane per mu, rounds of evaluation and
+        SQP-step kernels) or ``"auto"`` (wide when the instance is eligible)."""
+        N.check(N.lib().ddnm_ctx_set_engine(self.h, ENGINES[engine]))
+
+    def lanes(self) -> int:
+        """Evaluations the wide engine launched in the last solve (with the
+        speculative candidates that were not consumed)."""
+        n = C.c_int64()
+        N.check(N.lib().ddnm_last_lanes(self.h, C.byref(n)))
+        return n.value
+
+    def rounds(self):
+        """(SQP rounds, kernel launches) of the last batched solve."""
+        r, n = C.c_int64(), C.c_int64()
+        N.check(N.lib().ddnm_last_rounds(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+
+ENGINES = {"auto": 0, "slots": 1, "wide": 2}
+
 
 def _cfg_struct(cfg: SqpConfig):
     c = N.SqpCfg()
@@ -323,6 +345,8 @@ class BatchResult:
     seconds: float = 0.0
     tol: float = 1e-4
     counters: tuple = field(default=(0, 0))
+    rounds: int = 0        # SQP rounds of the batch-wide engine (0: persistent kernel)
+    launches: int = 0      # kernel launches of the solve
 
     @property
     def converged(self) -> np.ndarray:
@@ -350,8 +374,11 @@ class BatchResult:
 
 
 def _solve_arrays(inst: RomInstance, mu: np.ndarray, cfg: SqpConfig, x0=None, lam0=None,
-                  device: int = -1, slots: int = 0) -> BatchResult:
+                  device: int = -1, slots: int = 0, engine: str = "auto") -> BatchResult:
+    if engine not in ENGINES:
+        raise ValueError(f"engine must be one of {sorted(ENGINES)}")
     ctx = inst.context(device, slots)
+    ctx.set_engine(engine)
     B = mu.shape[0]
     nD, nC, K = inst.n_primal, inst.n_mult, cfg.max_iter
     out = dict(
@@ -371,17 +398,23 @@ def _solve_arrays(inst: RomInstance, mu: np.ndarray, cfg: SqpConfig, x0=None, la
     N.check(N.lib().ddnm_solve_batch(ctx.h, B, N.ptr(mu), N.ptr(x0), N.ptr(lam0),
                                      C.byref(_cfg_struct(cfg)), C.byref(so)))
     dt = time.perf_counter() - t0
-    return BatchResult(mu=mu, seconds=dt, tol=cfg.tol, counters=ctx.counters(), **out)
+    rounds, launches = ctx.rounds()
+    ctx.set_engine("auto")
+    return BatchResult(mu=mu, seconds=dt, tol=cfg.tol, counters=ctx.counters(), rounds=rounds,
+                       launches=launches, **out)
 
 
 def solve_rom_batch(instance: RomInstance, mus, cfg: SqpConfig = SqpConfig(), *,
-                    x0=None, lam0=None, device: int = -1, slots: int = 0) -> BatchResult:
+                    x0=None, lam0=None, device: int = -1, slots: int = 0,
+                    engine: str = "auto") -> BatchResult:
     """``solve_rom`` (driver.py:554-597, compute_error=False) for every mu.
 
     ``mus``: (B, 2) array of (a, lambda) or a list of ParameterPoint.
     ``x0``/``lam0``: optional (B, n_D) / (B, n_C) starting points; when absent
     the device evaluates the RBF initializer (driver.py:82-90) and the
-    least-squares multipliers (driver.py:461-471), as ``init_guess`` does."""
+    least-squares multipliers (driver.py:461-471), as ``init_guess`` does.
+    ``engine``: ``"auto"`` (the batch-wide kernels when the instance is
+    eligible, else the persistent kernel), ``"slots"`` or ``"wide"``."""
     mu = _mu_array(mus)
     span_lo = instance.arrays.get("rbf_lo")
     if x0 is None and span_lo is not None:
@@ -391,7 +424,7 @@ def solve_rom_batch(instance: RomInstance, mus, cfg: SqpConfig = SqpConfig(), *,
         if np.any(qn < -0.1) or np.any(qn > 1.1):
             warnings.warn("initializing far outside the training box", RuntimeWarning,
                           stacklevel=2)
-    return _solve_arrays(instance, mu, cfg, x0, lam0, device, slots)
+    return _solve_arrays(instance, mu, cfg, x0, lam0, device, slots, engine)
 
 
 @dataclass(eq=False)

@@ -68,21 +68,35 @@ def test_eval_matches_reference_golden(name, gpu_instances, goldens):
             assert rel(d["con_jac"], g[q + "con_jac"]) < 1e-12
 
 
+_ORACLE_SOLVES = {}
+
+
+def oracle_solve(name, oi, mu, k):
+    """Oracle solve of golden mu k of an instance, computed once per session."""
+    if (name, k) not in _ORACLE_SOLVES:
+        _ORACLE_SOLVES[(name, k)] = O.solve(oi, *mu[k])
+    return _ORACLE_SOLVES[(name, k)]
+
+
+@pytest.mark.parametrize("engine", ["auto", "slots"])
 @pytest.mark.parametrize("name", NAMES)
-def test_solve_batch_matches_oracle(name, gpu_instances, oracle_instances, goldens):
+def test_solve_batch_matches_oracle(name, engine, gpu_instances, oracle_instances, goldens):
     """Full batched solve (device RBF init, LS multipliers, SQP loop) vs the
     oracle: x, lam to 1e-9; trajectory identical whenever no decision was
-    within the merit noise floor."""
+    within the merit noise floor.  Both engines: "auto" is the batch-wide one
+    on the NM instances (and the same slot kernel as "slots" on the LS ones)."""
     inst, oi, g = gpu_instances[name], oracle_instances[name], goldens[name]
     mu = g["mu"]
-    res = P.solve_rom_batch(inst, mu)
+    if engine == "slots" and not inst.context().info.wide:
+        pytest.skip("auto already is the slot engine here")
+    res = P.solve_rom_batch(inst, mu, engine=engine)
     robust = both = same = 0
     for k in range(mu.shape[0]):
         assert rel(res.x[k], g["x"][k]) < 1e-9, k          # the reference itself, every mu
         assert rel(res.lam[k], g["lam"][k]) < 1e-9, k
         if k >= N_ORACLE.get(name, mu.shape[0]):
             continue
-        r = O.solve(oi, *mu[k])
+        r = oracle_solve(name, oi, mu, k)
         assert rel(res.x0[k], g["x0"][k]) < 1e-13
         assert rel(res.lam0[k], g["lam0"][k]) < 1e-10
         assert rel(res.x[k], r.x) < 1e-9, k
@@ -106,7 +120,7 @@ def test_solve_batch_matches_oracle(name, gpu_instances, oracle_instances, golde
     # floor (1e-13 merit0, e.g. c0_nm mu 4: merit ~1.2e-3 against a floor of
     # 2e-2 for its last three steps) the count is decided by round-off and
     # only the states are gated.  Agreement is reported and may not regress.
-    print(f"{name}: device n_iter equal to oracle+reference on {same} of {both} mu "
+    print(f"{name} [{engine}]: device n_iter equal to oracle+reference on {same} of {both} mu "
           f"({robust} robust)")
     if name != "c0_ls":               # config 1 claims no iteration-count parity
         assert both - same <= max(1, both // 8), (name, same, both)
@@ -140,16 +154,17 @@ def test_batch_composition_invariance(gpu_instances):
     bitwise-identical results (slots are independent state machines)."""
     inst = gpu_instances["c0_nm"]
     mu = P.seeded_parameters(64, seed=5)
-    full = P.solve_rom_batch(inst, mu)
+    full = P.solve_rom_batch(inst, mu, engine="slots")
     for k in (0, 17, 63):
-        one = P.solve_rom_batch(inst, mu[k:k + 1])
+        one = P.solve_rom_batch(inst, mu[k:k + 1], engine="slots")
         np.testing.assert_array_equal(one.x[0], full.x[k])
         np.testing.assert_array_equal(one.lam[0], full.lam[k])
         assert one.n_iter[0] == full.n_iter[k]
     # a different slot count changes the tensor-core tile shapes (association
     # order of the decoder sums), so only round-off-level agreement
-    g1 = P.solve_rom_batch(inst, mu, slots=1)
+    g1 = P.solve_rom_batch(inst, mu, slots=1, engine="slots")
     assert rel(g1.x, full.x) < 1e-9 and rel(g1.lam, full.lam) < 1e-9
+    # (the wide engine's invariance: tests/test_wide.py)
 
 
 def test_given_initial_point_and_multipliers(gpu_instances, oracle_instances, goldens):
@@ -253,7 +268,7 @@ def test_results_independent_of_launch_history():
     for name in ("c0_nm", "dd16_nm", "tiny_srpc"):
         P.solve_rom_batch(P.RomInstance.load(golden_path(name, "artifacts")), mu)
     inst = P.RomInstance.load(golden_path("c0_nmg", "artifacts"))
-    runs = [P.solve_rom_batch(inst, mu) for _ in range(3)]
+    runs = [P.solve_rom_batch(inst, mu, engine="slots") for _ in range(3)]
     shard = P.solve_rom_batch_subdomain_sharded(inst, mu)
     for r in runs[1:] + [shard]:
         np.testing.assert_array_equal(r.x, runs[0].x)

@@ -274,7 +274,7 @@ def test_device_sharded_world1_equals_megakernel(name, gpu_instances):
     inst = gpu_instances[name] if name in gpu_instances else P.RomInstance.load(
         golden_path(name, "artifacts"))
     mu = P.seeded_parameters(64, seed=3)
-    ref = P.solve_rom_batch(inst, mu)
+    ref = P.solve_rom_batch(inst, mu, engine="slots")   # the persistent kernel
     res = P.solve_rom_batch_subdomain_sharded(inst, mu)
     for k in ("x", "lam", "n_iter", "n_evals", "status", "n_reg", "merit", "objective",
               "x0", "lam0"):
@@ -360,10 +360,10 @@ def test_device_sharded_edge_cases(B):
     inst = P.RomInstance.load(golden_path("c0_nm", "artifacts"))
     mu = P.seeded_parameters(B, seed=21)
     cfg = P.SqpConfig(max_iter=3)
-    base = P.solve_rom_batch(inst, mu, cfg)
+    base = P.solve_rom_batch(inst, mu, cfg, engine="slots")
     x0 = base.x0 * (1.0 + 1e-3)
     for kw in ({}, {"x0": x0}, {"x0": x0, "lam0": base.lam0}):
-        ref = P.solve_rom_batch(inst, mu, cfg, **kw)
+        ref = P.solve_rom_batch(inst, mu, cfg, engine="slots", **kw)
         res = P.solve_rom_batch_subdomain_sharded(inst, mu, cfg, **kw)
         for k in ("x", "lam", "n_iter", "n_evals", "status", "x0", "lam0"):
             np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=f"{k} {kw.keys()}")
@@ -490,7 +490,7 @@ def test_device_sharded_config4_units():
     inst = P.RomInstance.load(golden_path("c4_nm", "artifacts"))
     g = dict(np.load(golden_path("c4_nm", "golden")))
     mu = g["mu"][:3]
-    ref = P.solve_rom_batch(inst, mu)
+    ref = P.solve_rom_batch(inst, mu, engine="slots")
     res = P.solve_rom_batch_subdomain_sharded(inst, mu)
     for k in ("x", "lam", "n_iter", "status"):
         np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=k)

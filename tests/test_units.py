@@ -70,8 +70,8 @@ def test_units_eval_match_whole_blocks(name, gpu_instances, goldens, monkeypatch
 def test_units_solve_match_reference(name, gpu_instances, goldens, monkeypatch):
     whole, g = _whole_instance(name, monkeypatch), goldens[name]
     split = _split_instance(name, monkeypatch)
-    rw = P.solve_rom_batch(whole, g["mu"])
-    rs = P.solve_rom_batch(split, g["mu"])
+    rw = P.solve_rom_batch(whole, g["mu"], engine="slots")
+    rs = P.solve_rom_batch(split, g["mu"], engine="slots")
     for k in range(g["mu"].shape[0]):
         if g["failure"][k] == 2:
             continue
@@ -87,9 +87,9 @@ def test_units_batch_composition_invariance(monkeypatch):
     """Split evaluation stays deterministic: a mu alone or in a batch is bitwise equal."""
     split = _split_instance("c0_nm", monkeypatch)
     mu = P.seeded_parameters(40, seed=9)
-    full = P.solve_rom_batch(split, mu)
+    full = P.solve_rom_batch(split, mu, engine="slots")
     for k in (0, 13, 39):
-        one = P.solve_rom_batch(split, mu[k:k + 1])
+        one = P.solve_rom_batch(split, mu[k:k + 1], engine="slots")
         np.testing.assert_array_equal(one.x[0], full.x[k])
         np.testing.assert_array_equal(one.lam[0], full.lam[k])
 
@@ -117,6 +117,6 @@ def test_tensor_core_hidden_layer_matches_oracle(name, goldens, oracle_instances
             assert rel(d["gam_J"], blk.gam_map.jacobian(xg)) < 1e-13
         assert rel(ev.rho[k], O.eval_gradients(oi, oi.boundary(*g["mu"][k]), g["x0"][k],
                                                g["lam0"][k]).rho) < 1e-11
-    res = P.solve_rom_batch(inst, g["mu"])
+    res = P.solve_rom_batch(inst, g["mu"], engine="slots")     # the slot kernels' hidden layer
     for k in range(g["mu"].shape[0]):
         assert rel(res.x[k], g["x"][k]) < 1e-9 and rel(res.lam[k], g["lam"][k]) < 1e-9, k
