@@ -62,7 +62,6 @@ struct WPart { int blk, which, t0, t1; };     // a run of tiles of one decoder
 struct WRowChunk { int blk, r0, r1, pslot; };
 struct WConChunk { int blk, j0, j1, cslot; };
 
-constexpr int WFINE_TILES = 32;   // fine items when at most this many lane tiles run
 constexpr int WSPEC_MAX = 16;     // most step lengths of one mu evaluated in one round
 constexpr int WSPEC_BOOST_LANES = 384;   // boost the candidates while the round stays below this
 
@@ -98,8 +97,13 @@ struct WArgs {
   int pk_stride, eb_base;
 };
 
-// lanes of the round -> item granularity (0 coarse, 1 fine) and partial stride
-__device__ __forceinline__ int wide_mode(int nlane) { return nlane <= WFINE_TILES * 32 ? 1 : 0; }
+// lanes of the round -> decoder part granularity (0 coarse, 1 fine): fine parts
+// (more items, hidden units at part boundaries computed twice) only while the
+// coarse ones would leave warps of the machine without an item
+constexpr int WIDE_FILL_ITEMS = 4096;
+__device__ __forceinline__ int wide_mode(const WArgs& A, int nlane) {
+  return (long long)A.nparts[0] * ((nlane + 31) >> 5) < WIDE_FILL_ITEMS ? 1 : 0;
+}
 
 // --------------------------------------------------------------------------
 // compaction + speculation.  Running mu (trial record flag != 0) in ascending
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(WDEC_WARPS * 32, 1) k_wide_dec(const __grid_co
   constexpr int LPM = wide_lp(NI) > wide_lp(NG) ? wide_lp(NI) : wide_lp(NG);
   const int nact = A.ctl[0];
   if (nact <= 0) return;
-  const int ntile = (nact + 31) >> 5, mode = wide_mode(nact);
+  const int ntile = (nact + 31) >> 5, mode = wide_mode(A, nact);
   const WPart* parts = A.parts[mode];
   const long long total = (long long)A.nparts[mode] * ntile;
   double* wsm = reinterpret_cast<double*>(wide_ring) + (size_t)(threadIdx.x >> 5) * wide_warp_doubles(LPM);
@@ -411,14 +415,21 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
   constexpr int I0 = wide_tri_row(W, NH, H), I1 = wide_tri_row(W, NH, H + 1);
   constexpr int NA = wide_tri_count(W, I0, I1);
   constexpr int TRI = W * (W + 1) / 2;
+  // the CTA's 4 warps: NSPLIT row splits x NH triangle parts.  With NH = 2
+  // the two warps of a split walk the same rows: they share the fetched row
+  // (each copies every other line) and synchronise on a named barrier.
+  constexpr int NSPLIT = 4 / NH;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = c0 + (c1 - c0) * warp / 4, r1 = c0 + (c1 - c0) * (warp + 1) / 4;
+  const int sp = NH == 2 ? warp >> 1 : warp;
+  const int r0 = c0 + (c1 - c0) * sp / NSPLIT, r1 = c0 + (c1 - c0) * (sp + 1) / NSPLIT;
   const int pstride = A.vpad;
   const int pos = tile * 32 + lane;
   const int mu = A.act[min(pos, nact - 1)] & 0xffffff;
   const double* gI = A.gj + ((size_t)tile * A.S + B.dec[0].gj_off) * 32 + lane;
-  const double* gG = A.gj + ((size_t)tile * A.S + B.dec[1].gj_off) * 32 + lane;
   const StRows& RW = B.rows;
+  auto pair_sync = [&]() {
+    if constexpr (NH == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + sp) : "memory");
+  };
   const int nr = B.nrows;
   // offset of an entry's g value from gI (its Jacobian row follows it):
   // interior output c, or interface output -1 - c of the block's second decoder
@@ -444,32 +455,37 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
   // are padded to MAXE entries with zero coefficients on a valid column;
   // adding their exact zeros changes no sum.
   constexpr int NSL = 11 + MAXE * LM;
-  double* pbuf = red + (size_t)warp * 2 * NSL * 32 + lane;
+  double* pbuf = red + (size_t)sp * 2 * NSL * 32 + lane;
+  // this warp's share of a row's lines: all of them, or every other one
+  auto mine = [&](int line) { return NH == 1 || (line & 1) == H; };
   auto fetch = [&](int row, double* buf) {
     const int cu = __ldg(RW.src_gu + row), cv = __ldg(RW.src_gv + row);
 #pragma unroll
     for (int e = 0; e < MAXE; ++e) {
       const int ce = __ldg(RW.src + e * nr + row);
       const double* src = gI + slot(ce);
-      wide_cp8(buf + e * 32, src);
+      if (mine(e)) wide_cp8(buf + e * 32, src);
       const int le = ce >= 0 ? NI : NG;
 #pragma unroll
       for (int d = 0; d < LM; ++d)
-        if (d < le) wide_cp8(buf + (11 + e * LM + d) * 32, src + (1 + d) * 32);
+        if (d < le && mine(11 + e * LM + d)) wide_cp8(buf + (11 + e * LM + d) * 32, src + (1 + d) * 32);
     }
-    wide_cp8(buf + 6 * 32, gI + slot(cu));
-    wide_cp8(buf + 7 * 32, gI + slot(cv));
+    if (mine(6)) wide_cp8(buf + 6 * 32, gI + slot(cu));
+    if (mine(7)) wide_cp8(buf + 7 * 32, gI + slot(cv));
     const double* bvp = A.bvT + (size_t)(B.row_off + row) * 3 * A.bpad + mu;
 #pragma unroll
-    for (int i = 0; i < 3; ++i) wide_cp8(buf + (8 + i) * 32, bvp + (size_t)i * A.bpad);
+    for (int i = 0; i < 3; ++i)
+      if (mine(8 + i)) wide_cp8(buf + (8 + i) * 32, bvp + (size_t)i * A.bpad);
   };
   if (r0 < r1) fetch(r0, pbuf);
   wide_cp_commit();
   for (int row = r0; row < r1; ++row) {
     const int par = (row - r0) & 1;
+    pair_sync();                       // the pair is done with the row before (its buffer is refilled now)
     if (row + 1 < r1) fetch(row + 1, pbuf + (par ^ 1) * NSL * 32);
     wide_cp_commit();
     wide_cp_wait<1>();
+    pair_sync();                       // both halves of this row have landed
     const double* buf = pbuf + par * NSL * 32;
     const int ne = __ldg(RW.nent + row);
     const int cu = __ldg(RW.src_gu + row), cv = __ldg(RW.src_gv + row);
@@ -532,10 +548,11 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
     }
   }
   constexpr int NR = NA + (H == 0 ? W + 1 : 0);     // values per lane
+  constexpr int NRM = TRI + W + 1;                   // room of one (split, part) region
   wide_cp_wait<0>();
   __syncthreads();                                   // the reduction scratch aliases the row buffers
-  if (warp > 0) {
-    double* mine = red + (size_t)(warp - 1) * NR * 32 + lane;
+  if (sp > 0) {
+    double* mine = red + (size_t)((sp - 1) * NH + H) * NRM * 32 + lane;
 #pragma unroll
     for (int q = 0; q < NA; ++q) mine[q * 32] = acc[q];
     if (H == 0) {
@@ -545,9 +562,9 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
     }
   }
   __syncthreads();
-  if (warp == 0) {
-    for (int w = 0; w < 3; ++w) {
-      const double* o = red + (size_t)w * NR * 32 + lane;
+  if (sp == 0) {
+    for (int w = 0; w < NSPLIT - 1; ++w) {
+      const double* o = red + (size_t)(w * NH + H) * NRM * 32 + lane;
 #pragma unroll
       for (int q = 0; q < NA; ++q) acc[q] = acc[q] + o[q * 32];
       if (H == 0) {
@@ -633,12 +650,12 @@ extern __shared__ __align__(16) double wide_red[];
 
 // CTA items: row chunks (x NH triangle parts) first, then the constraint chunks
 template <int NI, int NG, int NH>
-__global__ void __launch_bounds__(WROW_THREADS, 2) k_wide_rows(const __grid_constant__ WArgs A) {
+__global__ void __launch_bounds__(WROW_THREADS, NH == 2 ? 3 : 2) k_wide_rows(const __grid_constant__ WArgs A) {
   const int nact = A.ctl[0];
   if (nact <= 0) return;
   __shared__ int s_item;
   const int ntile = (nact + 31) >> 5;
-  const int nrow_items = A.nrc * NH;
+  const int nrow_items = A.nrc;
   const long long total = (long long)(nrow_items + A.ncc) * ntile;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(A.ctl + 2, 1);
@@ -648,11 +665,11 @@ __global__ void __launch_bounds__(WROW_THREADS, 2) k_wide_rows(const __grid_cons
     if (item >= total) break;
     const int ci = (int)(item / ntile), tile = (int)(item - (long long)ci * ntile);
     if (ci < nrow_items) {
-      const int rci = ci / NH, h = ci - rci * NH;
-      const WRowChunk* rc = A.rcs + rci;
+      const WRowChunk* rc = A.rcs + ci;
       const int b = __ldg(&rc->blk), r0 = __ldg(&rc->r0), r1 = __ldg(&rc->r1), ps = __ldg(&rc->pslot);
       const WBlockDev& B = A.blk[b];
-      if (NH == 1 || h == 0) wide_rows_body<NI, NG, NH, 0>(A, B, r0, r1, ps, tile, nact, wide_red);
+      // (NH = 2: warps 0, 2 take the first triangle part, warps 1, 3 the second)
+      if (NH == 1 || ((threadIdx.x >> 5) & 1) == 0) wide_rows_body<NI, NG, NH, 0>(A, B, r0, r1, ps, tile, nact, wide_red);
       else wide_rows_body<NI, NG, NH, NH - 1>(A, B, r0, r1, ps, tile, nact, wide_red);
     } else {
       const WConChunk* cc = A.ccs + (ci - nrow_items);
@@ -904,8 +921,11 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
     w->ring_smem = per_warp * w->dec_warps;
   }
   // reduction scratch of a row / constraint CTA: 3 warps x values per lane x 32 lanes
-  w->red_smem = std::max((size_t)3 * std::max(A.NQ, 8 * (ng + 1)) * 32,
-                         (size_t)4 * 2 * (11 + MAXE * std::max(ni, ng)) * 32) * sizeof(double);
+  {
+    const int nh = K->nh, nsplit = 4 / nh;
+    w->red_smem = std::max((size_t)3 * std::max(A.NQ, 8 * (ng + 1)) * 32,
+                           (size_t)nsplit * 2 * (11 + MAXE * std::max(ni, ng)) * 32) * sizeof(double);
+  }
   if (cudaFuncSetAttribute(K->dec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->ring_smem) != cudaSuccess ||
       cudaFuncSetAttribute(K->rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->red_smem) != cudaSuccess)
     return delete w, -1;
@@ -918,7 +938,7 @@ int wide_alloc(const Wide* w, int B, WideBuffers* b, std::string& err) {
   b->release();
   const int bpad = (B + 31) & ~31;
   // lanes: every mu once plus room for the speculative candidates
-  const int vpad = std::max(2 * bpad, WFINE_TILES * 32);
+  const int vpad = std::max(2 * bpad, 1024);
   const WArgs& A = w->A;
   const size_t tiles = (size_t)vpad / 32;
   const size_t part_n = (size_t)A.nrc * vpad * A.NQ;
@@ -993,7 +1013,7 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   if (cudaLaunchKernel(w->K->dec, dim3(ctas), dim3(w->dec_warps * 32), args, w->ring_smem, s) != cudaSuccess)
     return -1;
   if (!chk("k_wide_dec")) return -1;
-  if (cudaLaunchKernel(w->K->rows, dim3(ctas * 2), dim3(WROW_THREADS), args, w->red_smem, s) != cudaSuccess)
+  if (cudaLaunchKernel(w->K->rows, dim3(ctas * (w->K->nh == 2 ? 3 : 2)), dim3(WROW_THREADS), args, w->red_smem, s) != cudaSuccess)
     return -1;
   if (!chk("k_wide_rows")) return -1;
   // lanes of the round are only known on the device: the grid covers the

@@ -14,5 +14,7 @@ inst = P.RomInstance.load(os.path.join(ROOT, "tests", "golden", f"{name}_artifac
 mu = P.seeded_parameters(B, seed=1000)
 for _ in range(reps):
     r = P.solve_rom_batch(inst, mu)
+ctx = inst.context()
 print(f"{name} B={B} wide={os.environ['DDNM_WIDE']} solve {r.seconds*1e3:.2f} ms, evals {r.counters}, "
-      f"mean n_iter {r.n_iter.mean():.2f}")
+      f"mean n_iter {r.n_iter.mean():.2f}, rounds {r.rounds}, lanes launched {ctx.lanes()} vs consumed "
+      f"{int(r.n_evals.sum())}")
