@@ -213,6 +213,16 @@ typedef struct ddnm_ctx ddnm_ctx;
 int ddnm_plan_units(const ddnm_artifacts* art, int32_t* n_units, int32_t* row_unit,
                     int32_t* unit_info);
 
+/* Host-only (no GPU): how the batch-wide engine (csrc/ddnm_wide.h) would lay
+ * these artifacts out.  info10: [0] eligible (else ddnm_last_error says why
+ * not), [1] sweep tiles, [2] coarse and [3] fine decoder parts, [4] row
+ * chunks, [5] constraint chunks, [6] W2 stream slots (tile steps x outputs per
+ * tile), [7] stored decoder entries (their ratio is the sweep's useful
+ * fraction), [8] g / J doubles per lane, [9] longest window union of a tile
+ * (<= 32, the hidden ring).  tile_of_output (nullable): the tile of every
+ * decoder output, concatenated block by block (interior, then interface). */
+int ddnm_wide_plan(const ddnm_artifacts* art, int32_t* info10, int32_t* tile_of_output);
+
 const char* ddnm_last_error(void);
 int ddnm_abi_version(void);
 

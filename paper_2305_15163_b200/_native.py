@@ -139,6 +139,7 @@ def lib():
     L.ddnm_ctx_set_engine.argtypes = [C.c_void_p, C.c_int32]
     L.ddnm_last_rounds.argtypes = [C.c_void_p, _lp, _lp]
     L.ddnm_last_lanes.argtypes = [C.c_void_p, _lp]
+    L.ddnm_wide_plan.argtypes = [C.POINTER(Artifacts), _ip, _ip]
     L.ddnm_plan_units.argtypes = [C.POINTER(Artifacts), _ip, _ip, _ip]
     L.ddnm_dd_trial_len.argtypes = [C.c_void_p, _lp]
     L.ddnm_dd_set_trials.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
@@ -176,7 +177,7 @@ EXPORTED = ("ddnm_last_error", "ddnm_abi_version", "ddnm_ctx_create", "ddnm_ctx_
             "ddnm_binio_write", "ddnm_ctx_create_binio", "ddnm_dd_eval_p2p",
             "ddnm_ipc_get_handle", "ddnm_ipc_open_handle", "ddnm_ipc_close_handle",
             "ddnm_dev_alloc", "ddnm_dev_free", "ddnm_dd_trial_len", "ddnm_dd_set_trials",
-            "ddnm_dd_set_wide", "ddnm_ctx_set_engine", "ddnm_last_rounds", "ddnm_last_lanes",
+            "ddnm_dd_set_wide", "ddnm_ctx_set_engine", "ddnm_last_rounds", "ddnm_last_lanes", "ddnm_wide_plan",
             "ddnm_plan_units")
 
 

@@ -770,16 +770,109 @@ bool wup(Wide* w, const std::vector<T>& h, const T** d) {
 
 void wide_free(Wide* w) { delete w; }
 
+// ---- host-only planning (no GPU): tiles, W2 streams, parts, chunks ----------
+
+struct WidePlanDec {
+  std::vector<WTile> tiles;
+  std::vector<double> w2;       // per tile [khi - klo][T]
+  std::vector<int> tile_of;     // tile of every output
+  long long steps = 0;          // sum of khi - klo
+  long long useful = 0;         // stored W2 entries
+};
+
+// why the instance cannot run on the wide engine, or null
+static const char* wide_ineligible(const ddnm_artifacts* a) {
+  if (getenv("DDNM_NO_WIDE")) return "disabled (DDNM_NO_WIDE)";
+  if (a->map_kind != DDNM_MAP_AUTOENCODER) return "linear maps";
+  if (a->constraint_mode != DDNM_CON_WFPC) return "SRPC coupling";
+  if (!wide_kernels(a->blocks[0].n_int, a->blocks[0].n_gam)) return "latent pair has no wide kernels";
+  for (int b = 0; b < a->n_blocks; ++b) {
+    if (a->blocks[b].n_basis > 0) return "gappy hyper-reduction";
+    if (a->blocks[b].n_int != a->blocks[0].n_int || a->blocks[b].n_gam != a->blocks[0].n_gam)
+      return "blocks with different latent dims";
+  }
+  return nullptr;
+}
+
+// sweep tiles of one decoder: up to T consecutive outputs whose windows start
+// within 8 hidden units of the first one's and whose union fits the ring
+static const char* wide_plan_decoder(const ddnm_decoder& h, int L, WidePlanDec& out) {
+  const int T = wide_tile_outputs(L);
+  std::vector<int> k0(h.n_out), wd(h.n_out);
+  for (int o = 0; o < h.n_out; ++o) {
+    wd[o] = (int)(h.indptr[o + 1] - h.indptr[o]);
+    k0[o] = wd[o] > 0 ? (int)h.indices[h.indptr[o]] : (o > 0 ? k0[o - 1] : 0);
+    for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e)
+      if (h.indices[e] != k0[o] + (e - h.indptr[o])) return "decoder rows are not contiguous windows";
+    if (wd[o] > WRING) return "decoder row wider than the hidden ring";
+    if (o > 0 && k0[o] < k0[o - 1]) return "decoder windows not ascending";
+  }
+  out.tile_of.assign(h.n_out, -1);
+  for (int o = 0; o < h.n_out;) {
+    int lo = k0[o], hi = k0[o] + wd[o], cnt = 1;
+    while (cnt < T && o + cnt < h.n_out) {
+      const int nhi = std::max(hi, k0[o + cnt] + wd[o + cnt]);
+      // a joined output must overlap enough to pay for the longer walk
+      if (nhi - lo > WRING || k0[o + cnt] - lo > 8) break;
+      hi = nhi;
+      ++cnt;
+    }
+    WTile t{o, cnt, lo, hi, (int)out.w2.size()};
+    for (int kk = lo; kk < hi; ++kk)
+      for (int j = 0; j < T; ++j) {
+        double v = 0.0;
+        if (j < cnt) {
+          const int e = kk - k0[o + j];
+          if (e >= 0 && e < wd[o + j]) v = h.data[h.indptr[o + j] + e];
+        }
+        out.w2.push_back(v);
+      }
+    for (int j = 0; j < cnt; ++j) {
+      out.tile_of[o + j] = (int)out.tiles.size();
+      out.useful += wd[o + j];
+    }
+    out.steps += hi - lo;
+    out.tiles.push_back(t);
+    o += cnt;
+  }
+  return nullptr;
+}
+
+// parts: runs of ~pt tiles, cut where the windows do not overlap when such a
+// cut is near (no hidden unit computed twice)
+static void wide_plan_parts(const std::vector<WTile>& tiles, int pt, int b, int which,
+                            std::vector<WPart>& parts) {
+  const int nt = (int)tiles.size();
+  for (int t0 = 0; t0 < nt;) {
+    int t1 = std::min(nt, t0 + pt);
+    if (t1 < nt && pt >= 4) {
+      int best = -1;
+      for (int c = std::max(t0 + pt / 2, t0 + 1); c <= std::min(nt - 1, t0 + pt + pt / 2); ++c) {
+        int hi_prev = 0;
+        for (int q = std::max(t0, c - 4); q < c; ++q) hi_prev = std::max(hi_prev, tiles[q].khi);
+        if (tiles[c].klo >= hi_prev && (best < 0 || std::abs(c - (t0 + pt)) < std::abs(best - (t0 + pt))))
+          best = c;
+      }
+      if (best > 0) t1 = best;
+    }
+    parts.push_back(WPart{b, which, t0, t1});
+    t0 = t1;
+  }
+}
+
+static void wide_part_sizes(int (&part_tiles)[2], int& row_chunk, int& con_chunk) {
+  part_tiles[0] = 16; part_tiles[1] = 2;
+  row_chunk = WROW_CHUNK;
+  con_chunk = WCON_CHUNK;
+  if (const char* e = getenv("DDNM_WIDE_PART")) part_tiles[0] = std::max(1, atoi(e));
+  if (const char* e = getenv("DDNM_WIDE_ROWS")) row_chunk = std::max(4, atoi(e));
+}
+
 int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, std::string& why) {
   *out = nullptr;
-  if (getenv("DDNM_NO_WIDE")) { why = "disabled (DDNM_NO_WIDE)"; return 0; }
-  if (a->map_kind != DDNM_MAP_AUTOENCODER) { why = "linear maps"; return 0; }
-  if (a->constraint_mode != DDNM_CON_WFPC) { why = "SRPC coupling"; return 0; }
+  if (const char* r = wide_ineligible(a)) { why = r; return 0; }
   const int ni = a->blocks[0].n_int, ng = a->blocks[0].n_gam;
   const WideKernels* K = wide_kernels(ni, ng);
-  if (!K) { why = "latent pair has no wide kernels"; return 0; }
-  for (int b = 0; b < a->n_blocks; ++b)
-    if (a->blocks[b].n_basis > 0) { why = "gappy hyper-reduction"; return 0; }
   auto* w = new Wide();
   w->K = K;
   w->sms = sms;
@@ -789,11 +882,10 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
   std::vector<WConChunk> ccs;
   const int nC = a->n_c, nCp = (nC + 7) & ~7;
   int S = 0;
-  // tiles per decoder part, sampled rows per Gram partial, interface outputs
-  // per constraint partial: coarse / fine
-  int part_tiles[2] = {16, 2}, row_chunk = WROW_CHUNK, con_chunk = WCON_CHUNK;
-  if (const char* e = getenv("DDNM_WIDE_PART")) part_tiles[0] = std::max(1, atoi(e));
-  if (const char* e = getenv("DDNM_WIDE_ROWS")) row_chunk = std::max(4, atoi(e));
+  // tiles per decoder part (coarse / fine), sampled rows per Gram partial,
+  // interface outputs per constraint partial
+  int part_tiles[2], row_chunk, con_chunk;
+  wide_part_sizes(part_tiles, row_chunk, con_chunk);
   auto fail_build = [&](const char* msg) { why = msg; delete w; return 0; };
   for (int b = 0; b < a->n_blocks; ++b) {
     const ddnm_block& k = a->blocks[b];
@@ -801,7 +893,7 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
     std::memset(&WB, 0, sizeof WB);
     for (int which = 0; which < 2; ++which) {
       const ddnm_decoder& h = which == 0 ? k.interior : k.interface;
-      const int L = which == 0 ? ni : ng, LP = (L + 1) & ~1, T = wide_tile_outputs(L);
+      const int L = which == 0 ? ni : ng, LP = (L + 1) & ~1;
       WDecDev& D = WB.dec[which];
       D.L = L; D.n_out = h.n_out; D.n_hidden = h.n_hidden;
       D.xoff = P.blk[b].xoff + (which == 0 ? 0 : ni);
@@ -811,66 +903,14 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
       D.b1 = which == 0 ? P.blk[b].in.b1 : P.blk[b].ga.b1;
       D.scale = which == 0 ? P.blk[b].in.scale : P.blk[b].ga.scale;
       D.shift = which == 0 ? P.blk[b].in.shift : P.blk[b].ga.shift;
-      // windows: contiguous, first indices ascending, at most one ring wide
-      std::vector<int> k0(h.n_out), wd(h.n_out);
-      for (int o = 0; o < h.n_out; ++o) {
-        wd[o] = (int)(h.indptr[o + 1] - h.indptr[o]);
-        k0[o] = wd[o] > 0 ? (int)h.indices[h.indptr[o]] : (o > 0 ? k0[o - 1] : 0);
-        for (int64_t e = h.indptr[o]; e < h.indptr[o + 1]; ++e)
-          if (h.indices[e] != k0[o] + (e - h.indptr[o])) return fail_build("decoder rows are not contiguous windows");
-        if (wd[o] > WRING) return fail_build("decoder row wider than the hidden ring");
-        if (o > 0 && k0[o] < k0[o - 1]) return fail_build("decoder windows not ascending");
-      }
+      WidePlanDec pd;
+      if (const char* r = wide_plan_decoder(h, L, pd)) return fail_build(r);
       std::vector<double> w1p((size_t)h.n_hidden * LP, 0.0);
       for (int kk = 0; kk < h.n_hidden; ++kk)
         for (int d = 0; d < L; ++d) w1p[(size_t)kk * LP + d] = h.W1[(size_t)kk * L + d];
-      std::vector<WTile> tiles;
-      std::vector<double> w2;
-      for (int o = 0; o < h.n_out;) {
-        int lo = k0[o], hi = k0[o] + wd[o], cnt = 1;
-        while (cnt < T && o + cnt < h.n_out) {
-          const int nhi = std::max(hi, k0[o + cnt] + wd[o + cnt]);
-          // a joined output must overlap enough to pay for the longer walk
-          if (nhi - lo > WRING || k0[o + cnt] - lo > 8) break;
-          hi = nhi;
-          ++cnt;
-        }
-        WTile t{o, cnt, lo, hi, (int)w2.size()};
-        for (int kk = lo; kk < hi; ++kk)
-          for (int j = 0; j < T; ++j) {
-            double v = 0.0;
-            if (j < cnt) {
-              const int e = kk - k0[o + j];
-              if (e >= 0 && e < wd[o + j]) v = h.data[h.indptr[o + j] + e];
-            }
-            w2.push_back(v);
-          }
-        tiles.push_back(t);
-        o += cnt;
-      }
-      if (!wup(w, w1p, &D.W1p) || !wup(w, tiles, &D.tiles) || !wup(w, w2, &D.w2))
+      if (!wup(w, w1p, &D.W1p) || !wup(w, pd.tiles, &D.tiles) || !wup(w, pd.w2, &D.w2))
         return delete w, -1;
-      // parts: runs of ~pt tiles, cut where the windows do not overlap when
-      // such a cut is near (no hidden unit computed twice)
-      const int nt = (int)tiles.size();
-      for (int m = 0; m < 2; ++m) {
-        const int pt = part_tiles[m];
-        for (int t0 = 0; t0 < nt;) {
-          int t1 = std::min(nt, t0 + pt);
-          if (t1 < nt && pt >= 4) {
-            int best = -1;
-            for (int c = std::max(t0 + pt / 2, t0 + 1); c <= std::min(nt - 1, t0 + pt + pt / 2); ++c) {
-              int hi_prev = 0;
-              for (int q = std::max(t0, c - 4); q < c; ++q) hi_prev = std::max(hi_prev, tiles[q].khi);
-              if (tiles[c].klo >= hi_prev && (best < 0 || std::abs(c - (t0 + pt)) < std::abs(best - (t0 + pt))))
-                best = c;
-            }
-            if (best > 0) t1 = best;
-          }
-          parts[m].push_back(WPart{b, which, t0, t1});
-          t0 = t1;
-        }
-      }
+      for (int m = 0; m < 2; ++m) wide_plan_parts(pd.tiles, part_tiles[m], b, which, parts[m]);
     }
     WB.rows = P.blk[b].rows;
     WB.nrows = k.n_rows;
@@ -920,7 +960,7 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
     w->dec_warps = (int)std::min<size_t>(WDEC_WARPS, (size_t)(227 * 1024 - 1024) / per_warp);
     w->ring_smem = per_warp * w->dec_warps;
   }
-  // reduction scratch of a row / constraint CTA: 3 warps x values per lane x 32 lanes
+  // reduction scratch of a row / constraint CTA, aliased with its row buffers
   {
     const int nh = K->nh, nsplit = 4 / nh;
     w->red_smem = std::max((size_t)3 * std::max(A.NQ, 8 * (ng + 1)) * 32,
@@ -930,6 +970,50 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
       cudaFuncSetAttribute(K->rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->red_smem) != cudaSuccess)
     return delete w, -1;
   *out = w;
+  return 0;
+}
+
+// host-only plan summary and the tile of every output (ddnm_wide_plan)
+int wide_plan(const ddnm_artifacts* a, int32_t* info, int32_t* tile_of, std::string& why) {
+  for (int i = 0; i < 10; ++i) info[i] = 0;
+  if (const char* r = wide_ineligible(a)) { why = r; return 0; }
+  const int ni = a->blocks[0].n_int, ng = a->blocks[0].n_gam;
+  int part_tiles[2], row_chunk, con_chunk;
+  wide_part_sizes(part_tiles, row_chunk, con_chunk);
+  long long tiles = 0, steps = 0, useful = 0, S = 0, outs = 0;
+  int maxu = 0;
+  std::vector<WPart> parts[2];
+  int nrc = 0, ncc = 0;
+  for (int b = 0; b < a->n_blocks; ++b) {
+    const ddnm_block& k = a->blocks[b];
+    for (int which = 0; which < 2; ++which) {
+      const ddnm_decoder& h = which == 0 ? k.interior : k.interface;
+      const int L = which == 0 ? ni : ng;
+      WidePlanDec pd;
+      if (const char* r = wide_plan_decoder(h, L, pd)) { why = r; return 0; }
+      for (const WTile& t : pd.tiles) maxu = std::max(maxu, t.khi - t.klo);
+      for (int m = 0; m < 2; ++m) wide_plan_parts(pd.tiles, part_tiles[m], b, which, parts[m]);
+      if (tile_of)
+        for (int o = 0; o < h.n_out; ++o) tile_of[outs + o] = (int32_t)(tiles + pd.tile_of[o]);
+      outs += h.n_out;
+      tiles += (long long)pd.tiles.size();
+      steps += pd.steps * wide_tile_outputs(L);
+      useful += pd.useful;
+      S += (long long)h.n_out * (L + 1);
+    }
+    nrc += (k.n_rows + row_chunk - 1) / row_chunk;
+    ncc += std::max(1, (k.interface.n_out + con_chunk - 1) / con_chunk);
+  }
+  info[0] = 1;
+  info[1] = (int32_t)tiles;
+  info[2] = (int32_t)parts[0].size();
+  info[3] = (int32_t)parts[1].size();
+  info[4] = nrc;
+  info[5] = ncc;
+  info[6] = (int32_t)std::min<long long>(steps, INT32_MAX);     // W2 stream slots (tile steps x T)
+  info[7] = (int32_t)std::min<long long>(useful, INT32_MAX);    // stored decoder entries
+  info[8] = (int32_t)std::min<long long>(S, INT32_MAX);         // g / J doubles per lane
+  info[9] = maxu;                                               // longest window union (<= ring)
   return 0;
 }
 
@@ -1026,3 +1110,14 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
 }
 
 }  // namespace ddnm
+
+extern "C" int ddnm_wide_plan(const ddnm_artifacts* a, int32_t* info10, int32_t* tile_of_output) {
+  if (!a || !info10) { ddnm::set_error("null argument"); return DDNM_EINVAL; }
+  if (a->abi_version != DDNM_ABI_VERSION) { ddnm::set_error("ABI version mismatch"); return DDNM_EINVAL; }
+  if (a->n_blocks < 1 || a->n_blocks > ddnm::MAXB) { ddnm::set_error("need 1..16 blocks"); return DDNM_EINVAL; }
+  std::string why;
+  const int rc = ddnm::wide_plan(a, info10, tile_of_output, why);
+  ddnm::set_error(why);
+  return rc;
+}
+

@@ -26,6 +26,8 @@
 
 namespace ddnm {
 
+void set_error(const std::string& msg);   // ddnm_abi.cu: the thread's ddnm_last_error
+
 struct Wide;   // the wide program of one instance (device tables)
 
 // scratch of one solve of up to `cap` mu
