@@ -1242,7 +1242,12 @@ int ddnm_ctx_create(int32_t device, const ddnm_artifacts* a, int32_t slots, ddnm
       cudaMalloc(&c->counters, 2 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(DDNM_ECUDA, "cudaMalloc failed"));
   // batch-wide evaluation program (lane = mu), when the instance is eligible
-  if (ddnm::wide_build(a, P, c->sms, &c->wide, c->wide_why) != 0)
+  std::vector<ddnm::WideHostRows> whr(a->n_blocks);
+  for (int b = 0; b < a->n_blocks; ++b)
+    whr[b] = ddnm::WideHostRows{hrows[b].src.data(), hrows[b].sgu.data(), hrows[b].sgv.data(),
+                                hrows[b].nent.data(), hrows[b].bxc.data(), hrows[b].byc.data(),
+                                hrows[b].cdc.data()};
+  if (ddnm::wide_build(a, P, whr.data(), c->sms, &c->wide, c->wide_why) != 0)
     return bail(fail(DDNM_ECUDA, "cannot upload the wide evaluation tables"));
   *out = c;
   return 0;

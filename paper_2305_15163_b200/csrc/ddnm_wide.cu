@@ -43,6 +43,18 @@ struct WDecDev {
   const double* w2;
 };
 
+// one sampled row's tables (RestrictedResidual, partition.py:372-425), 256 bytes:
+// source codes of its <= 6 columns (>= 0 interior output, < 0: -1 - interface
+// output; padded with the node's own column and zero coefficients), of the
+// node's (u, v), its entry count, and the Bx / By / Cdiff coefficients
+struct WRowMeta {
+  int c[MAXE];
+  int cu, cv, ne, pad;
+  double bxc[MAXE], byc[MAXE], cdc[MAXE];
+  double pad2[9];
+};
+static_assert(sizeof(WRowMeta) == 256, "one record per 32 lanes x 8 bytes");
+
 // Decoder work comes in two granularities: coarse parts when the running mu
 // fill the machine by themselves, fine parts (a couple of tiles each) for the
 // rounds where few mu are left and the latency of one item is the round's
@@ -56,6 +68,7 @@ struct WBlockDev {
   int rc0, n_rc;         // its row chunks (Gram partial slots rc0 ..)
   int cc0, n_cc;         // its constraint chunks
   const double* CAt;     // [N_Gamma][nCp] C A_i transposed, nCp = n_C rounded up to 8
+  const WRowMeta* meta;  // [nrows]
 };
 
 struct WPart { int blk, which, t0, t1; };     // a run of tiles of one decoder
@@ -426,11 +439,9 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
   const int pos = tile * 32 + lane;
   const int mu = A.act[min(pos, nact - 1)] & 0xffffff;
   const double* gI = A.gj + ((size_t)tile * A.S + B.dec[0].gj_off) * 32 + lane;
-  const StRows& RW = B.rows;
   auto pair_sync = [&]() {
     if constexpr (NH == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + sp) : "memory");
   };
-  const int nr = B.nrows;
   // offset of an entry's g value from gI (its Jacobian row follows it):
   // interior output c, or interface output -1 - c of the block's second decoder
   const long long goff = (long long)(B.dec[1].gj_off - B.dec[0].gj_off) * 32;
@@ -456,13 +467,23 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
   // adding their exact zeros changes no sum.
   constexpr int NSL = 11 + MAXE * LM;
   double* pbuf = red + (size_t)sp * 2 * NSL * 32 + lane;
+  // The rows' own tables (columns, coefficients: one 256-byte WRowMeta per row)
+  // run two rows further ahead through a 4-deep ring per warp, lane l copying
+  // word l: the record of row r + 1 is in shared memory when its lines are
+  // requested, and nothing in the loop waits on a global load.
+  double* mring = red + (size_t)NSPLIT * 2 * NSL * 32 + (size_t)warp * 4 * 32;
+  const double* mglob = reinterpret_cast<const double*>(B.meta);
+  auto fetch_meta = [&](int it) {
+    if (it < r1) wide_cp8(mring + ((it - r0) & 3) * 32 + lane, mglob + (size_t)it * 32 + lane);
+  };
+  auto meta_of = [&](int it) { return reinterpret_cast<const WRowMeta*>(mring + ((it - r0) & 3) * 32); };
   // this warp's share of a row's lines: all of them, or every other one
   auto mine = [&](int line) { return NH == 1 || (line & 1) == H; };
-  auto fetch = [&](int row, double* buf) {
-    const int cu = __ldg(RW.src_gu + row), cv = __ldg(RW.src_gv + row);
+  auto fetch = [&](int it, double* buf) {
+    const WRowMeta* m = meta_of(it);
 #pragma unroll
     for (int e = 0; e < MAXE; ++e) {
-      const int ce = __ldg(RW.src + e * nr + row);
+      const int ce = m->c[e];
       const double* src = gI + slot(ce);
       if (mine(e)) wide_cp8(buf + e * 32, src);
       const int le = ce >= 0 ? NI : NG;
@@ -470,33 +491,39 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
       for (int d = 0; d < LM; ++d)
         if (d < le && mine(11 + e * LM + d)) wide_cp8(buf + (11 + e * LM + d) * 32, src + (1 + d) * 32);
     }
-    if (mine(6)) wide_cp8(buf + 6 * 32, gI + slot(cu));
-    if (mine(7)) wide_cp8(buf + 7 * 32, gI + slot(cv));
-    const double* bvp = A.bvT + (size_t)(B.row_off + row) * 3 * A.bpad + mu;
+    if (mine(6)) wide_cp8(buf + 6 * 32, gI + slot(m->cu));
+    if (mine(7)) wide_cp8(buf + 7 * 32, gI + slot(m->cv));
+    const double* bvp = A.bvT + (size_t)(B.row_off + it) * 3 * A.bpad + mu;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
       if (mine(8 + i)) wide_cp8(buf + (8 + i) * 32, bvp + (size_t)i * A.bpad);
   };
+  fetch_meta(r0); fetch_meta(r0 + 1); fetch_meta(r0 + 2);
+  wide_cp_commit();
+  wide_cp_wait<0>();
+  __syncwarp();
   if (r0 < r1) fetch(r0, pbuf);
   wide_cp_commit();
   for (int row = r0; row < r1; ++row) {
     const int par = (row - r0) & 1;
     pair_sync();                       // the pair is done with the row before (its buffer is refilled now)
     if (row + 1 < r1) fetch(row + 1, pbuf + (par ^ 1) * NSL * 32);
+    fetch_meta(row + 3);
     wide_cp_commit();
-    wide_cp_wait<1>();
+    wide_cp_wait<1>();                 // row's lines and the record of row + 2 have landed
+    __syncwarp();
     pair_sync();                       // both halves of this row have landed
     const double* buf = pbuf + par * NSL * 32;
-    const int ne = __ldg(RW.nent + row);
-    const int cu = __ldg(RW.src_gu + row), cv = __ldg(RW.src_gv + row);
+    const WRowMeta* m = meta_of(row);
+    const int ne = m->ne, cu = m->cu, cv = m->cv;
     int c[MAXE];
     double bxc[MAXE], byc[MAXE], cdc[MAXE], xe[MAXE];
 #pragma unroll
     for (int e = 0; e < MAXE; ++e) {
-      c[e] = __ldg(RW.src + e * nr + row);
-      bxc[e] = __ldg(RW.bxc + e * nr + row);
-      byc[e] = __ldg(RW.byc + e * nr + row);
-      cdc[e] = __ldg(RW.cdc + e * nr + row);
+      c[e] = m->c[e];
+      bxc[e] = m->bxc[e];
+      byc[e] = m->byc[e];
+      cdc[e] = m->cdc[e];
       xe[e] = buf[e * 32];
     }
     const double xu = buf[6 * 32], xv = buf[7 * 32];
@@ -514,8 +541,20 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
     double R[W];
 #pragma unroll
     for (int d = 0; d < W; ++d) R[d] = 0.0;
+    // chain rule, the Jacobian row of entry e + 1 read while entry e is used
+    double vn[LM];
+#pragma unroll
+    for (int d = 0; d < LM; ++d) vn[d] = d < (c[0] >= 0 ? NI : NG) ? buf[(11 + d) * 32] : 0.0;
 #pragma unroll
     for (int e = 0; e < MAXE; ++e) {
+      double v[LM];
+#pragma unroll
+      for (int d = 0; d < LM; ++d) v[d] = vn[d];
+      if (e + 1 < MAXE) {
+#pragma unroll
+        for (int d = 0; d < LM; ++d)
+          vn[d] = d < (c[e + 1] >= 0 ? NI : NG) ? buf[(11 + (e + 1) * LM + d) * 32] : 0.0;
+      }
       // diag(Bx x - b) E_u + diag(x_u) Bx + diag(x_v) By + diag(By x - b) E_v + Cd
       double j = 0.0;
       if (c[e] == cu) j = tx;
@@ -524,13 +563,12 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
       j = __dadd_rn(j, __dmul_rn(xv, byc[e]));
       j = __dadd_rn(j, cdc[e]);
       if (e >= ne) j = 0.0;
-      const double* jr = buf + (11 + e * LM) * 32;
       if (c[e] >= 0) {
 #pragma unroll
-        for (int d = 0; d < NI; ++d) R[d] = fma(j, jr[d * 32], R[d]);
+        for (int d = 0; d < NI; ++d) R[d] = fma(j, v[d], R[d]);
       } else {
 #pragma unroll
-        for (int d = 0; d < NG; ++d) R[NI + d] = fma(j, jr[d * 32], R[NI + d]);
+        for (int d = 0; d < NG; ++d) R[NI + d] = fma(j, v[d], R[NI + d]);
       }
     }
     // H += R^T R (rows I0 .. I1 of the upper triangle), R^T r, r^T r
@@ -868,7 +906,8 @@ static void wide_part_sizes(int (&part_tiles)[2], int& row_chunk, int& con_chunk
   if (const char* e = getenv("DDNM_WIDE_ROWS")) row_chunk = std::max(4, atoi(e));
 }
 
-int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, std::string& why) {
+int wide_build(const ddnm_artifacts* a, const Params& P, const WideHostRows* rows, int sms, Wide** out,
+               std::string& why) {
   *out = nullptr;
   if (const char* r = wide_ineligible(a)) { why = r; return 0; }
   const int ni = a->blocks[0].n_int, ng = a->blocks[0].n_gam;
@@ -913,6 +952,22 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
       for (int m = 0; m < 2; ++m) wide_plan_parts(pd.tiles, part_tiles[m], b, which, parts[m]);
     }
     WB.rows = P.blk[b].rows;
+    {
+      const WideHostRows& hr = rows[b];
+      std::vector<WRowMeta> meta(k.n_rows);
+      for (int r = 0; r < k.n_rows; ++r) {
+        WRowMeta& m = meta[r];
+        std::memset(&m, 0, sizeof m);
+        for (int e = 0; e < MAXE; ++e) {
+          m.c[e] = hr.src[(size_t)e * k.n_rows + r];
+          m.bxc[e] = hr.bxc[(size_t)e * k.n_rows + r];
+          m.byc[e] = hr.byc[(size_t)e * k.n_rows + r];
+          m.cdc[e] = hr.cdc[(size_t)e * k.n_rows + r];
+        }
+        m.cu = hr.sgu[r]; m.cv = hr.sgv[r]; m.ne = hr.nent[r];
+      }
+      if (!wup(w, meta, &WB.meta)) return delete w, -1;
+    }
     WB.nrows = k.n_rows;
     WB.row_off = P.blk[b].row_off;
     WB.eb_off = P.blk[b].eb_off;
@@ -963,8 +1018,10 @@ int wide_build(const ddnm_artifacts* a, const Params& P, int sms, Wide** out, st
   // reduction scratch of a row / constraint CTA, aliased with its row buffers
   {
     const int nh = K->nh, nsplit = 4 / nh;
-    w->red_smem = std::max((size_t)3 * std::max(A.NQ, 8 * (ng + 1)) * 32,
-                           (size_t)nsplit * 2 * (11 + MAXE * std::max(ni, ng)) * 32) * sizeof(double);
+    const size_t rowbuf = (size_t)nsplit * 2 * (11 + MAXE * std::max(ni, ng)) * 32;
+    const size_t meta = (size_t)4 * 4 * 32;               // 4 warps x 4 records
+    const size_t reduce = std::max((size_t)(nsplit - 1) * nh * A.NQ, (size_t)3 * 8 * (ng + 1)) * 32;
+    w->red_smem = (std::max(rowbuf, reduce) + meta) * sizeof(double);
   }
   if (cudaFuncSetAttribute(K->dec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->ring_smem) != cudaSuccess ||
       cudaFuncSetAttribute(K->rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->red_smem) != cudaSuccess)

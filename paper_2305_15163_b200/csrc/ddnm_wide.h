@@ -28,6 +28,12 @@ namespace ddnm {
 
 void set_error(const std::string& msg);   // ddnm_abi.cu: the thread's ddnm_last_error
 
+// host copy of one block's sampled rows (build_stencil), entry e of row r at [e * nrows + r]
+struct WideHostRows {
+  const int *src, *sgu, *sgv, *nent;
+  const double *bxc, *byc, *cdc;
+};
+
 struct Wide;   // the wide program of one instance (device tables)
 
 // scratch of one solve of up to `cap` mu
@@ -49,7 +55,7 @@ struct WideBuffers {
 };
 
 // *out stays null (return 0) when the instance is not eligible (why says so)
-int wide_build(const ddnm_artifacts* a, const Params& P, int sms,
+int wide_build(const ddnm_artifacts* a, const Params& P, const WideHostRows* rows, int sms,
                Wide** out, std::string& why);
 void wide_free(Wide* w);
 int wide_alloc(const Wide* w, int B, WideBuffers* b, std::string& err);
