@@ -688,7 +688,7 @@ extern __shared__ __align__(16) double wide_red[];
 
 // CTA items: row chunks (x NH triangle parts) first, then the constraint chunks
 template <int NI, int NG, int NH>
-__global__ void __launch_bounds__(WROW_THREADS, NH == 2 ? 3 : 2) k_wide_rows(const __grid_constant__ WArgs A) {
+__global__ void __launch_bounds__(WROW_THREADS, 2) k_wide_rows(const __grid_constant__ WArgs A) {
   const int nact = A.ctl[0];
   if (nact <= 0) return;
   __shared__ int s_item;
@@ -1154,7 +1154,7 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   if (cudaLaunchKernel(w->K->dec, dim3(ctas), dim3(w->dec_warps * 32), args, w->ring_smem, s) != cudaSuccess)
     return -1;
   if (!chk("k_wide_dec")) return -1;
-  if (cudaLaunchKernel(w->K->rows, dim3(ctas * (w->K->nh == 2 ? 3 : 2)), dim3(WROW_THREADS), args, w->red_smem, s) != cudaSuccess)
+  if (cudaLaunchKernel(w->K->rows, dim3(ctas * 2), dim3(WROW_THREADS), args, w->red_smem, s) != cudaSuccess)
     return -1;
   if (!chk("k_wide_rows")) return -1;
   // lanes of the round are only known on the device: the grid covers the
