@@ -1853,6 +1853,13 @@ int ddnm_dd_begin(ddnm_ctx* c, int32_t B, const double* d_mu, const double* d_x0
   P.work = c->work;
   P.counters = c->counters;
   P.prof = nullptr;
+  if (getenv("DDNM_PROF")) {           // phase clocks of the step kernel
+    if (!c->prof && cudaMalloc(&c->prof, 16 * sizeof(unsigned long long)) != cudaSuccess)
+      return bail(fail(DDNM_ECUDA, "cudaMalloc failed"));
+    if (cudaMemsetAsync(c->prof, 0, 16 * sizeof(unsigned long long), s) != cudaSuccess)
+      return bail(fail(DDNM_ECUDA, "memset failed"));
+    P.prof = c->prof;
+  }
   P.b_lo = blk_lo;
   P.b_hi = blk_hi;
   P.dd_st = bf.st;

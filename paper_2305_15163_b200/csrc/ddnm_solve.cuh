@@ -2405,6 +2405,15 @@ __device__ __forceinline__ void dd_step_body(const Params& P) {
   const unsigned mask = dd_load_state<G>(V, s_mu, mu0, mu_hi);
   if (mask == 0) return;
   if (tid == 0) s_kkts = 0;
+  // phase clocks of the step (DDNM_PROF=1: fetch = state load, sqp_state =
+  // decisions, kkt_* = the KKT stage, init = write back)
+  __shared__ unsigned long long s_prof[16];
+  if (P.prof) {
+    if (tid < 16) s_prof[tid] = 0;
+    V.prof = s_prof;
+    __syncthreads();
+    if (tid == 0) s_prof[15] = clock64();
+  }
   zero_slots(V);
   // state, current eval buffer (slot 0) and the gathered trial evaluation
   // (slot 1; slot 0 for the first evaluation of a new mu).  With the
@@ -2431,6 +2440,7 @@ __device__ __forceinline__ void dd_step_body(const Params& P) {
     s_k[tid] = on && P.dd_kof ? P.dd_kof[s_mu[tid]] : 1;
   }
   __syncthreads();
+  DDNM_MARK(V, 0);
   for (int j = 0;; ++j) {
     bool any = false;
     for (int s = 0; s < G; ++s) any = any || (s_go[s] && j < s_k[s]);
@@ -2465,7 +2475,9 @@ __device__ __forceinline__ void dd_step_body(const Params& P) {
     }
     __syncthreads();
   }
+  DDNM_MARK(V, 6);
   kkt_advance<G, NI, NG, KG>(V, s_cur, s_kres, s_kflag, &s_kkts);
+  DDNM_MARK(V, 7);
   if (warp < G && ((mask >> warp) & 1u) && st[warp].phase == PH_DONE) slot_write(V, warp);
   __syncthreads();
   for (int s = 0; s < G; ++s) {
@@ -2487,6 +2499,9 @@ __device__ __forceinline__ void dd_step_body(const Params& P) {
     if (st[tid].phase != PH_DONE) atomicAdd(P.dd_active, 1);
   }
   if (tid == 0) atomicAdd(P.counters + 1, s_kkts);
+  DDNM_MARK(V, 5);
+  if (P.prof && tid == 0)
+    for (int i = 0; i < 15; ++i) atomicAdd(P.prof + i, s_prof[i]);
 }
 
 template <int G, int NI, int NG, bool KG>
