@@ -649,10 +649,18 @@ def _subdomain_one(P, torch, dist, world, dev, stream, flush, path, batch, desc,
     inst = P.RomInstance.load(path)
     mu = P.seeded_parameters(batch, seed=2000)
     out = {"workload": desc, "batch": batch, "scaling": "strong", "ranks": world,
-           "kernels": "k_dd_eval + k_dd_step per SQP round"}
+           "kernels": "per SQP round: each rank's blocks by the wide kernels (k_wide_dec / k_wide_rows, "
+                      "one packet per mu) or by k_dd_eval (the *_slots entries and p2p), exchange, "
+                      "k_dd_step on the rank's mu slice"}
+    variants = []
     for transport in transports:
+        if transport == "nccl":
+            variants += [("nccl", "nccl", None), ("nccl_slots", "nccl", False)]
+        else:
+            variants.append((transport, transport, False))
+    for key, transport, wide in variants:
         try:
-            P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport)   # warm-up
+            P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport, wide=wide)   # warm-up
             times, res = [], None
             for _ in range(reps):
                 flush.fill_(2.0)
@@ -662,7 +670,7 @@ def _subdomain_one(P, torch, dist, world, dev, stream, flush, path, batch, desc,
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                res = P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport)
+                res = P.solve_rom_batch_subdomain_sharded(inst, mu, transport=transport, wide=wide)
                 e1.record(stream)
                 e1.synchronize()
                 times.append(e0.elapsed_time(e1))
@@ -671,11 +679,11 @@ def _subdomain_one(P, torch, dist, world, dev, stream, flush, path, batch, desc,
                 t = torch.tensor([ms], device=dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
-            out[transport] = {"solves_per_s": batch / (ms / 1e3), "ms_per_batch": ms,
+            out[key] = {"solves_per_s": batch / (ms / 1e3), "ms_per_batch": ms,
                               "rounds": int(res.rounds), "mean_n_iter": float(res.n_iter.mean()),
                               "status_counts": np.bincount(res.status, minlength=4).tolist()}
         except Exception as exc:      # reported per transport, never fatal
-            out[transport] = {"error": f"{type(exc).__name__}: {exc}"}
+            out[key] = {"error": f"{type(exc).__name__}: {exc}"}
     return out
 
 

@@ -387,7 +387,11 @@ int ddnm_dd_end(ddnm_dd* dd);
  * WFPC coupling, collocation HR, banded decoders).  ddnm_dd_eval then writes
  * one packet per LANE (a running mu may come with several candidate step
  * lengths per round), so d_packets must hold max(2 * roundup32(B), 1024) rows;
- * ddnm_dd_step reads them from the same buffer with nranks = 1.  ddnm_solve_batch[_device] takes this path by
+ * ddnm_dd_step reads them from the same buffer with nranks = 1.
+ * on = 2: one candidate per mu and packets [B][pk_stride] exactly as
+ * ddnm_dd_eval lays them out, for any block range -- the evaluation of a rank
+ * of a subdomain-sharded solve (the all-gather and ddnm_dd_step are unchanged;
+ * not with ddnm_dd_eval_p2p).  ddnm_solve_batch[_device] takes this path by
  * itself for large batches (DDNM_WIDE=0/1 forces). */
 int ddnm_dd_set_wide(ddnm_dd* dd, int32_t on);
 

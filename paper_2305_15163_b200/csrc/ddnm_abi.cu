@@ -1726,6 +1726,7 @@ struct ddnm_dd {
   DdBuffers buf;
   cudaStream_t stream = nullptr;  // the caller's stream of the last call
   bool wide = false;              // evaluations by the batch-wide kernels (ddnm_wide.h)
+  bool wide_by_mu = false;        // ... one candidate per mu, packets by mu (sharded ranks)
   size_t wide_pk_cap = 0;         // doubles in the caller's packet buffer when known
   const void* step_kern = nullptr; // step kernel / shared memory of the wide solve (null: the context's)
   size_t step_smem = 0;
@@ -1893,9 +1894,10 @@ int ddnm_dd_eval(ddnm_dd* d, double* d_packets, int64_t pk_stride, void* stream)
   d->P.dd_pk = d_packets;
   d->P.pk_stride = (int)pk_stride;
   if (d->wide) {
-    if ((size_t)pk_stride * ddnm::wide_packet_rows(d->buf.wide) > d->wide_pk_cap && d->wide_pk_cap)
+    if (!d->wide_by_mu && (size_t)pk_stride * ddnm::wide_packet_rows(d->buf.wide) > d->wide_pk_cap &&
+        d->wide_pk_cap)
       return fail(DDNM_EINVAL, "packet buffer smaller than one row per lane");
-    if (ddnm::wide_eval(d->c->wide, d->P, d->buf.wide, d_packets, (int)pk_stride, s) != 0)
+    if (ddnm::wide_eval(d->c->wide, d->P, d->buf.wide, d_packets, (int)pk_stride, d->wide_by_mu, s) != 0)
       return fail(DDNM_ECUDA, "wide evaluation launch failed");
     return 0;
   }
@@ -1913,15 +1915,18 @@ int ddnm_dd_set_wide(ddnm_dd* d, int32_t on) {
   }
   ddnm_ctx* c = d->c;
   if (!c->wide) return fail(DDNM_EUNSUPPORTED, "instance not eligible for the wide evaluation: " + c->wide_why);
-  if (d->P.b_lo != 0 || d->P.b_hi != d->P.nb)
-    return fail(DDNM_EUNSUPPORTED, "the wide evaluation needs every block on this rank");
+  const bool by_mu = on == 2;
+  if (!by_mu && (d->P.b_lo != 0 || d->P.b_hi != d->P.nb))
+    return fail(DDNM_EUNSUPPORTED, "the wide evaluation with candidates needs every block on this rank "
+                                   "(use mode 2: one packet per mu)");
   CUDA_TRY(cudaSetDevice(c->device));
   std::string err;
   if (ddnm::wide_alloc(c->wide, d->B, &d->buf.wide, err) != 0) return fail(DDNM_ENOMEM, err);
   if (ddnm::wide_begin(c->wide, d->P, d->buf.wide, d->stream) != 0)
     return fail(DDNM_ECUDA, "wide boundary-value launch failed");
-  d->P.dd_vbase = d->buf.wide.vbase;
-  d->P.dd_kof = d->buf.wide.kof;
+  d->P.dd_vbase = by_mu ? nullptr : d->buf.wide.vbase;
+  d->P.dd_kof = by_mu ? nullptr : d->buf.wide.kof;
+  d->wide_by_mu = by_mu;
   // the step kernel runs alone: KKT-sized shared scratch, dense fallback in a
   // global workspace, two CTAs per SM when compiled (DDNM_STEP2=0: the plain one)
   if (c->step_scr > 0 && !getenv("DDNM_STEP_FULL")) {

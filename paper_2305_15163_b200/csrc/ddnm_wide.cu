@@ -84,6 +84,10 @@ struct WArgs {
   const WRowChunk* rcs;
   const WConChunk* ccs;
   int nb, nparts[2], nrc, ncc;
+  // the blocks this call evaluates ([b_lo, b_hi): a rank of a subdomain-sharded
+  // solve) as ranges of the part / chunk tables (sorted by block), and where
+  // the packets go: by lane (with speculative candidates) or one row per mu
+  int b_lo, b_hi, part_lo[2], part_hi[2], rc_lo, rc_hi, cc_lo, cc_hi, by_mu;
   int S;                 // g/J slots per lane
   int NQ;                // doubles per Gram partial: W (W + 1) / 2 + W + 1
   int nC, nCp, NI, NG;
@@ -93,6 +97,7 @@ struct WArgs {
   int* kof;              // [B] its candidates this round
   int* ctl;              // [0] lanes, [1] decoder items, [2] row / constraint items
   unsigned long long* lanes_total;   // evaluations launched since wide_begin (incl. unused candidates)
+  unsigned long long* counters;      // [0] block evaluations consumed (by_mu: counted here)
   const double* trial;
   int rec;
   const SlotState* st;   // [B] SQP state (phase, rejected trials, step length)
@@ -115,7 +120,7 @@ struct WArgs {
 // coarse ones would leave warps of the machine without an item
 constexpr int WIDE_FILL_ITEMS = 4096;
 __device__ __forceinline__ int wide_mode(const WArgs& A, int nlane) {
-  return (long long)A.nparts[0] * ((nlane + 31) >> 5) < WIDE_FILL_ITEMS ? 1 : 0;
+  return (long long)(A.part_hi[0] - A.part_lo[0]) * ((nlane + 31) >> 5) < WIDE_FILL_ITEMS ? 1 : 0;
 }
 
 // --------------------------------------------------------------------------
@@ -131,7 +136,7 @@ __device__ __forceinline__ int wide_mode(const WArgs& A, int nlane) {
 // needed; K = 1 for everybody when the lanes would not fit.
 
 __device__ __forceinline__ int wide_kspec(const WArgs& A, const SlotState& S, bool boost) {
-  if (!A.spec || S.phase != PH_TRIAL || S.n_trials == 0) return 1;
+  if (!A.spec || A.by_mu || S.phase != PH_TRIAL || S.n_trials == 0) return 1;
   const int left = A.max_halvings + 1 - S.n_trials;      // trials the reference may still run
   int k = S.n_trials == 1 ? 2 : (S.n_trials < 4 ? 4 : 8);
   // few lanes: a round costs its latency, not its lanes, so candidates are free
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__(1024) k_wide_compact(const WArgs A) {
       A.ctl[0] = total;
       A.ctl[1] = 0; A.ctl[2] = 0; A.ctl[3] = 0;
       *A.lanes_total += (unsigned long long)total;
+      if (A.by_mu) atomicAdd(A.counters, (unsigned long long)total * (A.b_hi - A.b_lo));
     }
     break;
   }
@@ -386,8 +392,8 @@ __global__ void __launch_bounds__(WDEC_WARPS * 32, 1) k_wide_dec(const __grid_co
   const int nact = A.ctl[0];
   if (nact <= 0) return;
   const int ntile = (nact + 31) >> 5, mode = wide_mode(A, nact);
-  const WPart* parts = A.parts[mode];
-  const long long total = (long long)A.nparts[mode] * ntile;
+  const WPart* parts = A.parts[mode] + A.part_lo[mode];
+  const long long total = (long long)(A.part_hi[mode] - A.part_lo[mode]) * ntile;
   double* wsm = reinterpret_cast<double*>(wide_ring) + (size_t)(threadIdx.x >> 5) * wide_warp_doubles(LPM);
   for (long long item = wide_next(A.ctl + 1); item < total; item = wide_next(A.ctl + 1)) {
     const int pi = (int)(item / ntile), tile = (int)(item - (long long)pi * ntile);
@@ -693,8 +699,8 @@ __global__ void __launch_bounds__(WROW_THREADS, 2) k_wide_rows(const __grid_cons
   if (nact <= 0) return;
   __shared__ int s_item;
   const int ntile = (nact + 31) >> 5;
-  const int nrow_items = A.nrc;
-  const long long total = (long long)(nrow_items + A.ncc) * ntile;
+  const int nrow_items = A.rc_hi - A.rc_lo;
+  const long long total = (long long)(nrow_items + A.cc_hi - A.cc_lo) * ntile;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(A.ctl + 2, 1);
     __syncthreads();
@@ -703,14 +709,14 @@ __global__ void __launch_bounds__(WROW_THREADS, 2) k_wide_rows(const __grid_cons
     if (item >= total) break;
     const int ci = (int)(item / ntile), tile = (int)(item - (long long)ci * ntile);
     if (ci < nrow_items) {
-      const WRowChunk* rc = A.rcs + ci;
+      const WRowChunk* rc = A.rcs + A.rc_lo + ci;
       const int b = __ldg(&rc->blk), r0 = __ldg(&rc->r0), r1 = __ldg(&rc->r1), ps = __ldg(&rc->pslot);
       const WBlockDev& B = A.blk[b];
       // (NH = 2: warps 0, 2 take the first triangle part, warps 1, 3 the second)
       if (NH == 1 || ((threadIdx.x >> 5) & 1) == 0) wide_rows_body<NI, NG, NH, 0>(A, B, r0, r1, ps, tile, nact, wide_red);
       else wide_rows_body<NI, NG, NH, NH - 1>(A, B, r0, r1, ps, tile, nact, wide_red);
     } else {
-      const WConChunk* cc = A.ccs + (ci - nrow_items);
+      const WConChunk* cc = A.ccs + A.cc_lo + (ci - nrow_items);
       const int b = __ldg(&cc->blk), j0 = __ldg(&cc->j0), j1 = __ldg(&cc->j1), cs = __ldg(&cc->cslot);
       wide_con_body<NG>(A, A.blk[b], j0, j1, cs, tile, wide_red);
     }
@@ -725,12 +731,13 @@ __global__ void __launch_bounds__(128) k_wide_pack(const WArgs A) {
   const int nact = A.ctl[0];
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= nact) return;
-  const int b = blockIdx.y;
+  const int b = A.b_lo + blockIdx.y;
   const WBlockDev& B = A.blk[b];
   const int pstride = A.vpad;
   const int W = A.NI + A.NG, TRI = W * (W + 1) / 2, NG = A.NG, nC = A.nC;
   const int n_rc = B.n_rc, rc0 = B.rc0, n_cc = B.n_cc, cc0 = B.cc0;
-  double* dst = A.packets + (size_t)pos * A.pk_stride + (B.eb_off - A.eb_base);
+  const size_t prow = A.by_mu ? (size_t)(A.act[pos] & 0xffffff) : (size_t)pos;
+  double* dst = A.packets + prow * A.pk_stride + (B.eb_off - A.eb_base);
   const int nq = A.NQ + nC * (NG + 1);
   for (int q = blockIdx.z; q < nq; q += gridDim.z) {
     double v = 0.0;
@@ -780,6 +787,8 @@ struct Wide {
   int total_rows = 0;
   size_t ring_smem = 0, red_smem = 0;
   int dec_warps = WDEC_WARPS;
+  // first part (coarse / fine), row chunk and constraint chunk of every block (+ end)
+  std::vector<int> part0[2], rc0, cc0;
   ~Wide() {
     for (void* p : allocs) cudaFree(p);
   }
@@ -930,6 +939,9 @@ int wide_build(const ddnm_artifacts* a, const Params& P, const WideHostRows* row
     const ddnm_block& k = a->blocks[b];
     WBlockDev& WB = blocks[b];
     std::memset(&WB, 0, sizeof WB);
+    for (int m = 0; m < 2; ++m) w->part0[m].push_back((int)parts[m].size());
+    w->rc0.push_back((int)rcs.size());
+    w->cc0.push_back((int)ccs.size());
     for (int which = 0; which < 2; ++which) {
       const ddnm_decoder& h = which == 0 ? k.interior : k.interface;
       const int L = which == 0 ? ni : ng, LP = (L + 1) & ~1;
@@ -994,6 +1006,9 @@ int wide_build(const ddnm_artifacts* a, const Params& P, const WideHostRows* row
       for (int j = 0; j < ngo; ++j) cat[(size_t)j * nCp + c] = k.CA[(size_t)c * ngo + j];
     if (!wup(w, cat, &WB.CAt)) return delete w, -1;
   }
+  for (int m = 0; m < 2; ++m) w->part0[m].push_back((int)parts[m].size());
+  w->rc0.push_back((int)rcs.size());
+  w->cc0.push_back((int)ccs.size());
   WArgs& A = w->A;
   if (!wup(w, blocks, &A.blk) || !wup(w, rcs, &A.rcs) || !wup(w, ccs, &A.ccs)) return delete w, -1;
   for (int m = 0; m < 2; ++m) {
@@ -1114,8 +1129,14 @@ int wide_begin(const Wide* w, const Params& P, WideBuffers& b, cudaStream_t s) {
 }
 
 int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, int pk_stride,
-              cudaStream_t s) {
+              bool by_mu, cudaStream_t s) {
   WArgs A = w->A;
+  A.b_lo = P.b_lo;
+  A.b_hi = P.b_hi;
+  for (int m = 0; m < 2; ++m) { A.part_lo[m] = w->part0[m][P.b_lo]; A.part_hi[m] = w->part0[m][P.b_hi]; }
+  A.rc_lo = w->rc0[P.b_lo]; A.rc_hi = w->rc0[P.b_hi];
+  A.cc_lo = w->cc0[P.b_lo]; A.cc_hi = w->cc0[P.b_hi];
+  A.by_mu = by_mu ? 1 : 0;
   A.B = P.B;
   A.vpad = b.vpad;
   A.bpad = b.bpad;
@@ -1124,6 +1145,7 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   A.kof = b.kof;
   A.ctl = b.ctl;
   A.lanes_total = b.lanes_total;
+  A.counters = P.counters;
   A.trial = P.dd_trial;
   A.rec = P.dd_rec;
   A.st = P.dd_st;
@@ -1137,7 +1159,7 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   A.bvT = b.bvT;
   A.packets = packets;
   A.pk_stride = pk_stride;
-  A.eb_base = P.blk[0].eb_off;
+  A.eb_base = P.blk[P.b_lo].eb_off;
   // DDNM_WIDE_SYNC=1: synchronise after every kernel and name the one that failed
   static const bool dbg = getenv("DDNM_WIDE_SYNC") != nullptr;
   auto chk = [&](const char* what) {
@@ -1160,7 +1182,7 @@ int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, i
   // lanes of the round are only known on the device: the grid covers the
   // capacity the host can bound (mu still running x candidates)
   const int lanes = std::min(b.vpad, b.lane_bound > 0 ? b.lane_bound : b.vpad);
-  dim3 pg((lanes + 127) / 128, A.nb, 16);
+  dim3 pg((lanes + 127) / 128, A.b_hi - A.b_lo, 16);
   k_wide_pack<<<pg, 128, 0, s>>>(A);
   if (!chk("k_wide_pack")) return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

@@ -61,9 +61,13 @@ void wide_free(Wide* w);
 int wide_alloc(const Wide* w, int B, WideBuffers* b, std::string& err);
 // boundary values of every mu of the batch (once per solve)
 int wide_begin(const Wide* w, const Params& P, WideBuffers& b, cudaStream_t s);
-// one evaluation of every running mu at its trial point -> packets [B][pk_stride]
+// one evaluation of blocks [P.b_lo, P.b_hi) at every running mu's trial point.
+// by_mu = false: packets [lane][pk_stride], a mu's speculative candidates in
+// consecutive rows (k_dd_step finds them through dd_vbase / dd_kof); by_mu =
+// true: one candidate per mu, packets [mu][pk_stride] as k_dd_eval writes them
+// (a rank of a subdomain-sharded solve: the other ranks' state is not here)
 int wide_eval(const Wide* w, const Params& P, WideBuffers& b, double* packets, int pk_stride,
-              cudaStream_t s);
+              bool by_mu, cudaStream_t s);
 // packets the solve must provide: one row per lane
 inline size_t wide_packet_rows(const WideBuffers& b) { return (size_t)b.vpad; }
 

@@ -132,10 +132,13 @@ class DeviceRoundEngine:
             _all_gather(flat, flat[rank * chunk * row:(rank + 1) * chunk * row].clone(), world,
                         group)
 
-    def set_wide(self, on: bool = True) -> None:
+    def set_wide(self, on=True) -> None:
         """Evaluate with the batch-wide kernels (one lane per mu) instead of
-        k_dd_eval; needs every block on this rank."""
-        N.check(N.lib().ddnm_dd_set_wide(self.h, 1 if on else 0))
+        k_dd_eval.  ``True`` / 1: packets by lane with speculative step
+        lengths (needs every block on this rank and ``wide_lanes`` packet
+        rows); 2: one packet per mu as k_dd_eval writes them, for any block
+        range (the ranks of a subdomain-sharded solve)."""
+        N.check(N.lib().ddnm_dd_set_wide(self.h, int(on)))
 
     def eval(self, packets, stride: int) -> None:
         N.check(N.lib().ddnm_dd_eval(self.h, C.c_void_p(packets.data_ptr()), stride,
@@ -179,7 +182,7 @@ class ShardedSolve:
     ``step()``, which returns the number of mu still running."""
 
     def __init__(self, instance, mu, cfg: SqpConfig, rank: int, world: int, *, x0=None,
-                 lam0=None, engine=None, device: int = -1):
+                 lam0=None, engine=None, device: int = -1, wide=None):
         self.eng = engine or DeviceRoundEngine(instance, device)
         nb = self.eng.n_blocks
         self.bounds = block_bounds(nb, world)
@@ -200,6 +203,15 @@ class ShardedSolve:
         self.trials = self.eng.buffer(world * self.chunk * self.rec)
         self.eng.set_trials(self.trials, self.mu_lo, self.mu_hi)
         self.packets = self.eng.buffer(self.B * self.stride)
+        # this rank's blocks through the batch-wide kernels (one packet per mu,
+        # same layout) when the instance has them: None = when eligible
+        self.wide = False
+        if isinstance(self.eng, DeviceRoundEngine) and wide is not False:
+            if self.eng.ctx.info.wide:
+                self.eng.set_wide(2)
+                self.wide = True
+            elif wide:
+                raise NotImplementedError("instance not eligible for the wide evaluation")
         self.rounds = 0
         # every round evaluates one trial point per running mu; a solve takes
         # at most max_iter KKT steps of at most max_halvings + 1 trials each
@@ -314,7 +326,7 @@ class _PeerBuffers:
 
 def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(), *,
                                       x0=None, lam0=None, group=None, device: int = -1,
-                                      engine=None, transport: str = "nccl"):
+                                      engine=None, transport: str = "nccl", wide=None):
     """Batched ``solve_rom`` (driver.py:554-597, compute_error=False) with the
     subdomain blocks sharded over the ranks of ``group`` (every rank passes
     the same ``mus``); every rank returns the same full ``BatchResult``.
@@ -323,7 +335,12 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
     the packets; ``"p2p"`` -- the evaluation kernel stores its packets into
     every rank's gathered buffer over peer memory (CUDA IPC between the
     processes of one node) and a one-element all-reduce orders the ranks
-    before the step (device engine only)."""
+    before the step (device engine only).
+
+    ``wide``: each rank evaluates its blocks with the batch-wide kernels (one
+    lane per mu, csrc/ddnm_wide.h; one packet per mu, the same exchange and
+    steps).  ``None``: when the instance is eligible and the transport is
+    ``"nccl"`` (the fused peer stores are k_dd_eval's); ``False``: k_dd_eval."""
     if transport not in ("nccl", "p2p"):
         raise ValueError("transport must be 'nccl' or 'p2p'")
     import torch.distributed as dist
@@ -334,8 +351,12 @@ def solve_rom_batch_subdomain_sharded(instance, mus, cfg: SqpConfig = SqpConfig(
     rank = dist.get_rank(group) if dist_on else 0
     world = dist.get_world_size(group) if dist_on else 1
     t0 = time.perf_counter()
+    if transport == "p2p":
+        if wide:
+            raise ValueError("the wide evaluation goes with transport='nccl'")
+        wide = False
     sh = ShardedSolve(instance, mu, cfg, rank, world, x0=x0, lam0=lam0, engine=engine,
-                      device=device)
+                      device=device, wide=wide)
     active = sh.active
     peers, own = [], []
     if transport == "p2p" and world > 1:

@@ -275,7 +275,7 @@ def test_device_sharded_world1_equals_megakernel(name, gpu_instances):
         golden_path(name, "artifacts"))
     mu = P.seeded_parameters(64, seed=3)
     ref = P.solve_rom_batch(inst, mu, engine="slots")   # the persistent kernel
-    res = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    res = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)   # k_dd_eval
     for k in ("x", "lam", "n_iter", "n_evals", "status", "n_reg", "merit", "objective",
               "x0", "lam0"):
         np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=k)
@@ -364,7 +364,7 @@ def test_device_sharded_edge_cases(B):
     x0 = base.x0 * (1.0 + 1e-3)
     for kw in ({}, {"x0": x0}, {"x0": x0, "lam0": base.lam0}):
         ref = P.solve_rom_batch(inst, mu, cfg, engine="slots", **kw)
-        res = P.solve_rom_batch_subdomain_sharded(inst, mu, cfg, **kw)
+        res = P.solve_rom_batch_subdomain_sharded(inst, mu, cfg, wide=False, **kw)
         for k in ("x", "lam", "n_iter", "n_evals", "status", "x0", "lam0"):
             np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=f"{k} {kw.keys()}")
         assert np.all(res.n_iter <= 3)
@@ -383,14 +383,14 @@ def test_device_fused_peer_gather(world):
     from paper_2305_15163_b200.subdomain import ShardedSolve
     inst = P.RomInstance.load(golden_path(DD, "artifacts"))
     mu = P.seeded_parameters(20, seed=8)
-    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)
     if world == 1:
         res = P.solve_rom_batch_subdomain_sharded(inst, mu, transport="p2p")
         for k in ("x", "lam", "n_iter", "status"):
             np.testing.assert_array_equal(getattr(res, k), getattr(one, k), err_msg=k)
         return
     cfg = P.SqpConfig()
-    ranks = [ShardedSolve(inst, mu, cfg, r, world) for r in range(world)]
+    ranks = [ShardedSolve(inst, mu, cfg, r, world, wide=False) for r in range(world)]
     n = world * ranks[0].B * ranks[0].stride
     gathered = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
                 for _ in ranks]
@@ -422,8 +422,8 @@ def test_ipc_handle_of_a_device_buffer():
     from paper_2305_15163_b200.subdomain import ShardedSolve, _DevBuffer
     inst = P.RomInstance.load(golden_path(DD, "artifacts"))
     mu = P.seeded_parameters(7, seed=2)
-    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
-    sh = ShardedSolve(inst, mu, P.SqpConfig(), 0, 1)
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)
+    sh = ShardedSolve(inst, mu, P.SqpConfig(), 0, 1, wide=False)
     buf = _DevBuffer(sh.B * sh.stride * 8, torch.cuda.current_device())
     h = C.create_string_buffer(64)
     N.check(N.lib().ddnm_ipc_get_handle(C.c_void_p(buf.data_ptr()), h))
@@ -452,8 +452,8 @@ def test_device_p2p_host_loop_protocol(world):
     from paper_2305_15163_b200.subdomain import CHECK, ShardedSolve
     inst = P.RomInstance.load(golden_path(DD, "artifacts"))
     mu = P.seeded_parameters(19, seed=6)
-    one = P.solve_rom_batch_subdomain_sharded(inst, mu)
-    ranks = [ShardedSolve(inst, mu, P.SqpConfig(), r, world) for r in range(world)]
+    one = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)
+    ranks = [ShardedSolve(inst, mu, P.SqpConfig(), r, world, wide=False) for r in range(world)]
     n = world * ranks[0].B * ranks[0].stride
     bufs = [[torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in ranks]
             for _ in range(2)]
@@ -491,12 +491,12 @@ def test_device_sharded_config4_units():
     g = dict(np.load(golden_path("c4_nm", "golden")))
     mu = g["mu"][:3]
     ref = P.solve_rom_batch(inst, mu, engine="slots")
-    res = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    res = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)
     for k in ("x", "lam", "n_iter", "status"):
         np.testing.assert_array_equal(getattr(res, k), getattr(ref, k), err_msg=k)
     for k in range(3):
         assert _rel(res.x[k], g["x"][k]) < 1e-9 and _rel(res.lam[k], g["lam"][k]) < 1e-9
-    ranks = [ShardedSolve(inst, mu, P.SqpConfig(), r, 2) for r in range(2)]
+    ranks = [ShardedSolve(inst, mu, P.SqpConfig(), r, 2, wide=False) for r in range(2)]
     gathered = torch.empty(2 * ranks[0].B * ranks[0].stride, dtype=torch.float64, device="cuda")
     active = ranks[0].active
     while active:

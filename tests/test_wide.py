@@ -172,3 +172,60 @@ def test_environment_selectors(gpu_instances, monkeypatch):
     monkeypatch.setenv("DDNM_WIDE_MIN_B", "9")
     assert P.solve_rom_batch(inst, mu).rounds == 0
     assert P.solve_rom_batch(inst, P.seeded_parameters(9, seed=2)).rounds > 0
+
+
+def _exchange(ranks):
+    """What the all-gathers of the trial records do between in-process ranks."""
+    from .test_subdomain import _exchange_trials
+    _exchange_trials(ranks)
+
+
+@pytest.mark.parametrize("name,world", [("dd16_nm", 1), ("dd16_nm", 2), ("dd16_nm", 3), ("c0_nm", 2),
+                                        ("c4_nm", 4)])
+def test_sharded_ranks_with_wide_evaluation(name, world, gpu_instances):
+    """Subdomain-sharded rounds whose ranks evaluate their blocks with the
+    wide kernels (one packet per mu, any block range): a block's partial sums
+    do not depend on which rank computes them, so every rank count reproduces
+    the unsharded wide solve bit for bit (speculation changes nothing either)."""
+    import torch
+
+    from paper_2305_15163_b200.subdomain import ShardedSolve
+    from .test_subdomain import _exchange_results
+    inst = gpu_instances[name]
+    B = 6 if name == "c4_nm" else 24
+    mu = P.seeded_parameters(B, seed=4)
+    ref = P.solve_rom_batch(inst, mu, engine="wide")
+    cfg = P.SqpConfig()
+    ranks = [ShardedSolve(inst, mu, cfg, r, world) for r in range(world)]
+    assert all(sh.wide for sh in ranks)
+    gathered = torch.empty(world * ranks[0].B * ranks[0].stride, dtype=torch.float64, device="cuda")
+    active = ranks[0].active
+    while active:
+        parts = [sh.eval().clone() for sh in ranks]
+        torch.cat(parts, out=gathered)
+        active = sum(sh.step(gathered) for sh in ranks)
+        _exchange(ranks)
+    _exchange_results(ranks)
+    for sh in ranks:
+        r = sh.result(group=False)
+        for k in ("x", "lam", "n_iter", "n_evals", "status", "merit"):
+            np.testing.assert_array_equal(getattr(r, k), getattr(ref, k), err_msg=k)
+
+
+def test_sharded_driver_uses_wide_by_default(gpu_instances, goldens):
+    """solve_rom_batch_subdomain_sharded at one rank: wide evaluation when the
+    instance has it (bitwise the wide engine's solve), k_dd_eval on request or
+    for the peer-store transport; the reference goldens either way."""
+    inst, g = gpu_instances["dd16_nm"], goldens["dd16_nm"]
+    mu = g["mu"]
+    ref = P.solve_rom_batch(inst, mu, engine="wide")
+    res = P.solve_rom_batch_subdomain_sharded(inst, mu)
+    np.testing.assert_array_equal(res.x, ref.x)
+    np.testing.assert_array_equal(res.n_evals, ref.n_evals)
+    assert res.counters[0] == int(res.n_evals.sum()) * inst.n_blocks
+    slots = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)
+    for r in (res, slots):
+        for k in range(mu.shape[0]):
+            assert rel(r.x[k], g["x"][k]) < 1e-9 and rel(r.lam[k], g["lam"][k]) < 1e-9
+    with pytest.raises(ValueError):
+        P.solve_rom_batch_subdomain_sharded(inst, mu, transport="p2p", wide=True)
