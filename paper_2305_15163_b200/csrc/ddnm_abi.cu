@@ -1390,7 +1390,11 @@ int ddnm_solve_batch_device(ddnm_ctx* c, int32_t B, const double* d_mu, const do
     return fail(DDNM_EUNSUPPORTED, "instance not eligible for the wide engine: " + c->wide_why);
   if (B > 0 && use_wide(c, B)) {
     CUDA_TRY(cudaSetDevice(c->device));
-    return solve_wide(c, B, d_mu, d_x0, d_lam0, cfg, o, stream ? (cudaStream_t)stream : c->stream);
+    const int rc = solve_wide(c, B, d_mu, d_x0, d_lam0, cfg, o, stream ? (cudaStream_t)stream : c->stream);
+    // the wide engine's scratch grows with the batch (g / J lines of every
+    // lane): when it does not fit, AUTO solves with the persistent kernel
+    if (rc != DDNM_ENOMEM || c->engine == DDNM_ENGINE_WIDE) return rc;
+    cudaGetLastError();
   }
   if (!(cfg->tol > 0) || cfg->max_iter < 1 || !(cfg->armijo_c1 > 0) || !(cfg->backtrack_factor > 0) ||
       !(cfg->backtrack_factor < 1) || cfg->max_halvings < 0)

@@ -1028,6 +1028,7 @@ int wide_build(const ddnm_artifacts* a, const Params& P, const WideHostRows* row
     const int lpm = std::max(wide_lp(ni), wide_lp(ng));
     const size_t per_warp = (size_t)wide_warp_doubles(lpm) * sizeof(double);
     w->dec_warps = (int)std::min<size_t>(WDEC_WARPS, (size_t)(227 * 1024 - 1024) / per_warp);
+    if (const char* e = getenv("DDNM_WIDE_DEC_WARPS")) w->dec_warps = std::max(1, std::min(w->dec_warps, atoi(e)));
     w->ring_smem = per_warp * w->dec_warps;
   }
   // reduction scratch of a row / constraint CTA, aliased with its row buffers
