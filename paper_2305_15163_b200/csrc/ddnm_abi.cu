@@ -1376,6 +1376,7 @@ static int wide_min_batch() {
 }
 static bool use_wide(const ddnm_ctx* c, int B) {
   if (!c->wide || c->engine == DDNM_ENGINE_SLOTS) return false;
+  if (B >= (1 << 23)) return false;     // lane entries hold mu in 24 bits (candidate index above)
   if (c->engine == DDNM_ENGINE_WIDE) return true;
   if (const char* e = getenv("DDNM_WIDE")) return atoi(e) != 0;
   return B >= wide_min_batch();
