@@ -285,6 +285,7 @@ class _Context:
         slot per mu), ``"wide"`` (one lane per mu, rounds of evaluation and
         SQP-step kernels) or ``"auto"`` (wide when the instance is eligible)."""
         N.check(N.lib().ddnm_ctx_set_engine(self.h, ENGINES[engine]))
+        self.engine = engine
 
     def lanes(self) -> int:
         """Evaluations the wide engine launched in the last solve (with the
@@ -378,7 +379,8 @@ def _solve_arrays(inst: RomInstance, mu: np.ndarray, cfg: SqpConfig, x0=None, la
     if engine not in ENGINES:
         raise ValueError(f"engine must be one of {sorted(ENGINES)}")
     ctx = inst.context(device, slots)
-    ctx.set_engine(engine)
+    prev = getattr(ctx, "engine", "auto")          # a choice made on the context stays
+    ctx.set_engine(engine if engine != "auto" else prev)
     B = mu.shape[0]
     nD, nC, K = inst.n_primal, inst.n_mult, cfg.max_iter
     out = dict(
@@ -395,11 +397,13 @@ def _solve_arrays(inst: RomInstance, mu: np.ndarray, cfg: SqpConfig, x0=None, la
     if lam0 is not None:
         lam0 = N.f64(lam0).reshape(B, nC)
     t0 = time.perf_counter()
-    N.check(N.lib().ddnm_solve_batch(ctx.h, B, N.ptr(mu), N.ptr(x0), N.ptr(lam0),
-                                     C.byref(_cfg_struct(cfg)), C.byref(so)))
+    try:
+        N.check(N.lib().ddnm_solve_batch(ctx.h, B, N.ptr(mu), N.ptr(x0), N.ptr(lam0),
+                                         C.byref(_cfg_struct(cfg)), C.byref(so)))
+    finally:
+        ctx.set_engine(prev)
     dt = time.perf_counter() - t0
     rounds, launches = ctx.rounds()
-    ctx.set_engine("auto")
     return BatchResult(mu=mu, seconds=dt, tol=cfg.tol, counters=ctx.counters(), rounds=rounds,
                        launches=launches, **out)
 
