@@ -42,11 +42,13 @@ for name in ("tiny_nm", "tiny_ls", "c0_nm", "tiny_srpc", "c0_nmg", "c0_lss", "dd
 
 inst = load("dd16_nm")
 mu = P.seeded_parameters(5, seed=9)
-one = P.solve_rom_batch_subdomain_sharded(inst, mu)
+one = P.solve_rom_batch_subdomain_sharded(inst, mu, wide=False)     # k_dd_eval, like the peer-store path
 p2p = P.solve_rom_batch_subdomain_sharded(inst, mu, transport="p2p")
 assert np.array_equal(one.x, p2p.x)
+wide = P.solve_rom_batch_subdomain_sharded(inst, mu)                 # the ranks' blocks by the wide kernels
+assert np.array_equal(wide.x, P.solve_rom_batch(inst, mu, engine="wide").x)
 cfg = P.SqpConfig(max_iter=3)
-ranks = [ShardedSolve(inst, mu, cfg, r, 3) for r in range(3)]
+ranks = [ShardedSolve(inst, mu, cfg, r, 3, wide=False) for r in range(3)]
 n = 3 * ranks[0].B * ranks[0].stride
 bufs = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in ranks]
 active = ranks[0].active
