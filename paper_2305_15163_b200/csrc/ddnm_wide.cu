@@ -144,43 +144,65 @@ __device__ __forceinline__ int wide_kspec(const WArgs& A, const SlotState& S, bo
   return max(1, min(k, left));
 }
 
+// exclusive prefix of one count per thread over the CTA (1024 threads): warp
+// shuffles, the 32 warp totals scanned by warp 0; returns the CTA total too
+__device__ __forceinline__ int wide_block_scan(int n, int* s_warp, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  __syncthreads();                      // s_warp of an earlier scan has been read
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_warp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    s_warp[32 + lane] = w;              // inclusive warp totals
+  }
+  __syncthreads();
+  total = s_warp[32 + 31];
+  return incl - n + (warp > 0 ? s_warp[32 + warp - 1] : 0);
+}
+
 __global__ void __launch_bounds__(1024) k_wide_compact(const WArgs A) {
-  __shared__ int s_cnt[1024];
+  __shared__ int s_warp[64];
   const int tid = threadIdx.x, T = blockDim.x;
   const int per = (A.B + T - 1) / T;
   const int lo = min(A.B, tid * per), hi = min(A.B, lo + per);
-  // policy 2: boosted candidates (few lanes), 1: by rejections seen, 0: one each
-  for (int policy = 2; policy >= 0; --policy) {
-    int n = 0;
-    for (int mu = lo; mu < hi; ++mu)
-      if (A.trial[(size_t)mu * A.rec] != 0.0) n += policy ? wide_kspec(A, A.st[mu], policy == 2) : 1;
-    __syncthreads();                  // the previous policy's totals have been read
-    s_cnt[tid] = n;
-    __syncthreads();
-    // inclusive scan (Hillis-Steele on 1024 counts)
-    for (int o = 1; o < T; o <<= 1) {
-      const int v = tid >= o ? s_cnt[tid - o] : 0;
-      __syncthreads();
-      s_cnt[tid] += v;
-      __syncthreads();
+  // candidates of this thread's mu under each policy: 2 boosted (few lanes),
+  // 1 by the rejections seen, 0 one each
+  int n[3] = {0, 0, 0};
+  for (int mu = lo; mu < hi; ++mu)
+    if (A.trial[(size_t)mu * A.rec] != 0.0) {
+      const SlotState S = A.st[mu];
+      n[0] += 1;
+      n[1] += wide_kspec(A, S, false);
+      n[2] += wide_kspec(A, S, true);
     }
-    const int total = s_cnt[T - 1];
-    if (policy > 0 && total > (policy == 2 ? min(WSPEC_BOOST_LANES, A.vpad) : A.vpad)) continue;
-    int at = s_cnt[tid] - n;
-    for (int mu = lo; mu < hi; ++mu)
-      if (A.trial[(size_t)mu * A.rec] != 0.0) {
-        const int k = policy ? wide_kspec(A, A.st[mu], policy == 2) : 1;
-        A.vbase[mu] = at;
-        A.kof[mu] = k;
-        for (int j = 0; j < k; ++j) A.act[at++] = mu | (j << 24);
-      }
-    if (tid == T - 1) {
-      A.ctl[0] = total;
-      A.ctl[1] = 0; A.ctl[2] = 0; A.ctl[3] = 0;
-      *A.lanes_total += (unsigned long long)total;
-      if (A.by_mu) atomicAdd(A.counters, (unsigned long long)total * (A.b_hi - A.b_lo));
+  int policy = 2, at = 0, total = 0;
+  for (; policy >= 0; --policy) {
+    at = wide_block_scan(n[policy], s_warp, total);
+    if (policy == 0 || total <= (policy == 2 ? min(WSPEC_BOOST_LANES, A.vpad) : A.vpad)) break;
+  }
+  for (int mu = lo; mu < hi; ++mu)
+    if (A.trial[(size_t)mu * A.rec] != 0.0) {
+      const int k = policy ? wide_kspec(A, A.st[mu], policy == 2) : 1;
+      A.vbase[mu] = at;
+      A.kof[mu] = k;
+      for (int j = 0; j < k; ++j) A.act[at++] = mu | (j << 24);
     }
-    break;
+  if (tid == T - 1) {
+    A.ctl[0] = total;
+    A.ctl[1] = 0; A.ctl[2] = 0; A.ctl[3] = 0;
+    *A.lanes_total += (unsigned long long)total;
+    if (A.by_mu) atomicAdd(A.counters, (unsigned long long)total * (A.b_hi - A.b_lo));
   }
 }
 
