@@ -486,7 +486,7 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
   double rr = 0.0;
   // Every value a row needs from memory -- the g of its <= 6 columns and of
   // the node's (u, v), its boundary values, the Jacobian rows of its columns:
-  // WROW_SLOTS coalesced 256-byte lines per warp -- has an address that
+  // NSL (= 11 + 6 LM) coalesced 256-byte lines per warp -- has an address that
   // depends on the row only, so row r + 1 is fetched into shared memory with
   // cp.async (each lane its own 8 bytes of every line) while row r is computed:
   // ~90 lines in flight per warp instead of what fits in registers.  A lane
@@ -613,7 +613,6 @@ __device__ __forceinline__ void wide_rows_body(const WArgs& A, const WBlockDev& 
       rr = fma(r, r, rr);
     }
   }
-  constexpr int NR = NA + (H == 0 ? W + 1 : 0);     // values per lane
   constexpr int NRM = TRI + W + 1;                   // room of one (split, part) region
   wide_cp_wait<0>();
   __syncthreads();                                   // the reduction scratch aliases the row buffers

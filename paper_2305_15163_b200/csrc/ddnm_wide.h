@@ -6,14 +6,17 @@
 // of decoder outputs, so every weight, index and stencil coefficient is a
 // warp-uniform load shared by 32 mu and every per-mu value is a coalesced
 // 256-byte row.  One SQP round of the batch is then
-//   k_wide_compact  running mu -> dense list (the trial records' flags)
-//   k_wide_dec      hidden layer (a 32-unit ring per warp in shared memory)
-//                   + banded output sweep, g and its latent Jacobian
-//                   (hyper.py:184-197) -> g/J rows [tile][slot][32 lanes]
-//   k_wide_rows     HR stencil rows, chain rule, Gram partials per row chunk
-//                   (partition.py:427-464, driver.py:422-429, sqp.py:124-133)
-//   k_wide_con      WFPC constraint partials C A_i g, C A_i J (driver.py:371-373)
-//   k_wide_pack     partials summed in chunk order -> the per-mu packets that
+//   k_wide_compact  running mu -> dense lane list (the trial records' flags),
+//                   with the line search's next step lengths as extra lanes
+//   k_wide_dec      hidden layer (a 32-unit ring per warp in shared memory,
+//                   weights staged by cp.async) + banded output sweep, g and
+//                   its latent Jacobian (hyper.py:184-197)
+//                   -> g/J lines [tile][slot][32 lanes]
+//   k_wide_rows     HR stencil rows (prefetched by cp.async), chain rule, Gram
+//                   partials per row chunk (partition.py:427-464,
+//                   driver.py:422-429, sqp.py:124-133); WFPC constraint
+//                   partials C A_i g, C A_i J (driver.py:371-373)
+//   k_wide_pack     partials summed in chunk order -> the packets that
 //                   k_dd_step (the SQP decision + KKT of ddnm_solve.cuh) reads
 // i.e. it replaces k_dd_eval in the round-synchronous solve.
 #pragma once
