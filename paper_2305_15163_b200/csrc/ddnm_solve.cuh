@@ -1368,8 +1368,8 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
   double* rhs = work + (size_t)n * ld + n;
   double* res = rhs + n;
   double* tmp = res + n;
-  __shared__ double s_rhsn, s_delta, s_red[32];
-  __shared__ int s_fin;
+  __shared__ double s_rhsn, s_delta, s_red[32], s_pbest[4];
+  __shared__ int s_fin, s_pidx[4];
   for (int i = tid; i < n; i += T) rhs[i] = -(i < P.n_D ? e[P.eb_rho + i] : e[P.eb_con + i - P.n_D]);
   __syncthreads();
   if (warp == 0) {
@@ -1414,11 +1414,18 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
     constexpr int NB = 8;
     for (int j0 = 0; j0 < n; j0 += NB) {
       const int j1 = min(n, j0 + NB);
-      if (warp == 0) {
+      // the panel is factored by the first PT <= 128 threads (rows dealt
+      // round-robin, one or two per thread at n <= 256) meeting on a named
+      // barrier: per column a warp argmax each, the 4 candidates combined with
+      // the same "first maximum" rule, then every thread scales and updates
+      // its own rows.  Same operations per element as a single thread would do.
+      const int PT = min(128, T);
+      if (tid < PT) {
+        auto panel_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(PT) : "memory"); };
         for (int k = j0; k < j1; ++k) {
           double best = -1.0;
           int bi = n;
-          for (int i = k + lane; i < n; i += WARP) {
+          for (int i = k + tid; i < n; i += PT) {
             const double a = fabs(K[i * ld + k]);
             if (a > best || (a == best && i < bi)) { best = a; bi = i; }
           }
@@ -1428,28 +1435,32 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
             const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
             if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
           }
-          if (lane == 0) piv[k] = bi;
+          if (lane == 0) { s_pbest[warp] = best; s_pidx[warp] = bi; }
+          panel_sync();
+          for (int w = 0; w < PT / WARP; ++w) {
+            const double ob = s_pbest[w];
+            const int oi = s_pidx[w];
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+          }
+          if (tid == 0) piv[k] = bi;
           if (bi != k)
-            for (int j = j0 + lane; j < j1; j += WARP) {
+            for (int j = j0 + tid; j < j1; j += PT) {
               const double t = K[k * ld + j];
               K[k * ld + j] = K[bi * ld + j];
               K[bi * ld + j] = t;
             }
-          __syncwarp();
+          panel_sync();
           const double pv = K[k * ld + k];
           if (pv != 0.0) {
             const double rp = fabs(pv) >= 2.2250738585072014e-308 ? rcp_fast(pv) : 0.0;
-            for (int i = k + 1 + lane; i < n; i += WARP) {
+            for (int i = k + 1 + tid; i < n; i += PT) {
               const double v = K[i * ld + k];
-              K[i * ld + k] = rp != 0.0 ? v * rp : v / pv;
-            }
-            __syncwarp();
-            for (int i = k + 1 + lane; i < n; i += WARP) {
-              const double l = K[i * ld + k];
+              const double l = rp != 0.0 ? v * rp : v / pv;
+              K[i * ld + k] = l;
               for (int j = k + 1; j < j1; ++j) K[i * ld + j] = fma(-l, K[k * ld + j], K[i * ld + j]);
             }
           }
-          __syncwarp();
+          panel_sync();
         }
       }
       __syncthreads();
@@ -1474,14 +1485,28 @@ __device__ int cta_kkt(const Params& P, const double* e, double* work, double* s
           for (int i = k + 1; i < j1; ++i) K[i * ld + c] = fma(-K[i * ld + k], u, K[i * ld + c]);
         }
       __syncthreads();
-      // trailing update A22 -= L21 U12, k in pivot order per element
-      const int m = n - j1;
-      for (int idx = tid; idx < m * m; idx += T) {
-        const int i = j1 + idx / m, c = j1 + idx % m;
-        double a = K[i * ld + c];
-        for (int k = j0; k < j1; ++k)
-          if (K[k * ld + k] != 0.0) a = fma(-K[i * ld + k], K[k * ld + c], a);
-        K[i * ld + c] = a;
+      // trailing update A22 -= L21 U12, k in pivot order per element.  A
+      // thread keeps one column's panel-row entries U[k][c] in registers and
+      // walks that column's rows (threads of a warp: consecutive columns of
+      // the same row, so L[i][k] is a broadcast): 9 shared loads per element
+      // instead of 25, no index divisions.
+      {
+        const int cl = min(128, T), tx = tid % cl, ty = tid / cl, nty = T / cl;
+        bool nz[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) nz[k] = j0 + k < j1 && K[(j0 + k) * ld + (j0 + k)] != 0.0;
+        for (int c = j1 + tx; c < n; c += cl) {
+          double u[NB];
+#pragma unroll
+          for (int k = 0; k < NB; ++k) u[k] = nz[k] ? K[(j0 + k) * ld + c] : 0.0;
+          for (int i = j1 + ty; i < n; i += nty) {
+            double a = K[i * ld + c];
+#pragma unroll
+            for (int k = 0; k < NB; ++k)
+              if (nz[k]) a = fma(-K[i * ld + j0 + k], u[k], a);
+            K[i * ld + c] = a;
+          }
+        }
       }
       __syncthreads();
     }
