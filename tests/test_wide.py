@@ -69,6 +69,9 @@ def test_engines_agree(name, gpu_instances, goldens):
     rw = P.solve_rom_batch(inst, mu, engine="wide")
     assert rs.rounds == 0 and rs.launches == 1
     assert rw.rounds > 0 and rw.launches == 2 + 5 * rw.rounds
+    # lanes launched (with the unused speculative candidates) vs evaluations consumed
+    lanes = inst.context().lanes()
+    assert int(rw.n_evals.sum()) <= lanes <= 2 * int(rw.n_evals.sum())
     for r in (rs, rw):
         for k in range(mu.shape[0]):
             assert rel(r.x[k], g["x"][k]) < 1e-9 and rel(r.lam[k], g["lam"][k]) < 1e-9
