@@ -241,8 +241,11 @@ int ddnm_solve_batch(ddnm_ctx* ctx, int32_t B, const double* mu,
                      const double* x0, const double* lam0,
                      const ddnm_sqp_cfg* cfg, ddnm_solve_out* out);
 
-/* Same with device-resident inputs/outputs, asynchronous on `stream`
- * (a cudaStream_t; NULL = the context's stream). */
+/* Same with device-resident inputs/outputs, on `stream` (a cudaStream_t;
+ * NULL = the context's stream).  The slot engine is one asynchronous launch;
+ * the wide engine (ddnm_ctx_set_engine below) enqueues its SQP rounds on the
+ * stream, reads the running count every few rounds, and returns when the batch
+ * is solved. */
 int ddnm_solve_batch_device(ddnm_ctx* ctx, int32_t B, const double* d_mu,
                             const double* d_x0, const double* d_lam0,
                             const ddnm_sqp_cfg* cfg, ddnm_solve_out* d_out,
